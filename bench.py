@@ -1,0 +1,282 @@
+"""bench.py -- throughput of the Barnes-Hut t-SNE iteration on B200.
+
+Metric (BASELINE.json): BH t-SNE iterations/s (and end-to-end seconds) on the
+ImageNet-ResNet-shaped workload C5: N = 1,281,167 points, D = 2048, perplexity
+30 (K = 90), theta = 0.5.  A "step" is one t-SNE iteration: quadtree build ->
+theta traversal (F_rep, Z) -> attractive pass fused with the update (DESIGN.md
+section 7).  The supporting kNN and P stages run once before the timed loop
+(timed and reported in `stages`), and again inside the end-to-end `e2e` leg
+(tsne_run from pinned host X to host Y).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C5] [--n N_override] [--no-e2e] [--no-cpu]
+
+`--impl reference` times the fp64 CPU oracle (oracle/) on the host cores, one
+full-size oracle iteration per step.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "BH t-SNE iterations/s (N=1.28M, D=2048 ImageNet-ResNet-shaped)"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, dev=0):
+        self.dev, self.rows, self.proc = dev, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_iteration_inputs(N, nnz_per_row=126, seed=0):
+    """Iteration-shaped inputs for timing the oracle (synth only): a clustered
+    2-D embedding and a CSR with the workload's mean row length."""
+    Y = synth.fixed_y("clustered", N, seed=seed, labels=torch.randint(
+        0, 1000, (N,), generator=torch.Generator().manual_seed(seed)))
+    rng = np.random.default_rng(seed)
+    cols = rng.integers(0, N, size=(N, nnz_per_row), dtype=np.int64).astype(np.int32)
+    cols.sort(1)
+    rp = np.arange(0, N * nnz_per_row + 1, nnz_per_row, dtype=np.int64)
+    val = (rng.random(N * nnz_per_row) * (2.0 / (N * nnz_per_row))).astype(np.float32)
+    return Y, rp, cols.ravel(), val
+
+
+def time_oracle_iterations(N, n_iter, nnz_per_row, warmup=0):
+    import oracle
+    Y, rp, col, val = cpu_iteration_inputs(N, nnz_per_row)
+    Yd = Y.astype(np.float64)
+    v = np.zeros_like(Yd)
+    g = np.ones_like(Yd)
+    if warmup:
+        Yd, v, g = oracle.optimize(rp, col, val, Yd, v, g, t0=0, n_iter=warmup, theta=0.5)
+    times = []
+    for k in range(n_iter):
+        t = time.perf_counter()
+        Yd, v, g = oracle.optimize(rp, col, val, Yd, v, g, t0=warmup + k, n_iter=1, theta=0.5)
+        times.append(time.perf_counter() - t)
+    return times, oracle.num_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    N = args.n or cfg.N
+    nnz_row = args.nnz_per_row
+    times, cores = time_oracle_iterations(N, args.steps, nnz_row, warmup=args.warmup)
+    T = sum(times)
+    v = args.steps / T
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "N": N, "D": cfg.D, "theta": 0.5,
+                   "nnz_per_row": nnz_row},
+        "cpu_baseline": {"value": v, "unit": "it/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{args.steps} full-size oracle iterations (fp64 tree + traversal "
+                                   f"+ attractive + update) at N={N}, synthetic clustered Y and "
+                                   f"{nnz_row} nnz/row CSR"},
+        "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world):
+    import paper_1807_11824_b200 as T
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    cfg = synth.CONFIGS[args.config]
+    N = args.n or cfg.N
+    K = min(N - 1, int(3 * cfg.perplexity))
+    stages = {}
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    X = synth.make_x(cfg, n=N, device=dev)
+    torch.cuda.synchronize()
+    a, b = ev(), ev()
+    a.record()
+    idx, d2, kinfo = T.knn(X, K)
+    b.record()
+    torch.cuda.synchronize()
+    stages["knn_ms"] = a.elapsed_time(b)
+    a.record()
+    rp, col, val = T.compute_p(idx, d2, cfg.perplexity)
+    b.record()
+    torch.cuda.synchronize()
+    stages["p_ms"] = a.elapsed_time(b)
+    nnz = int(col.numel())
+    del idx, d2
+
+    opt = T.Optimizer(rp, col, val, T.init_y(N, 42, device=dev), theta=0.5)
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        opt.step(args.warmup)
+        # per-stage profile of a few eager iterations (events on the library's stream)
+        prof = T.profile_iteration(opt, reps=5, stream=s.cuda_stream)
+        s.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        s.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with Clocks(dev.index) as clk:
+            a.record(s)
+            opt.step(args.steps, stream=s.cuda_stream)
+            b.record(s)
+            s.synchronize()
+        ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    stages.update({k: v for k, v in prof.items()})
+    value = world * args.steps / (ms / 1e3) if world > 1 else args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel
+    hbm, which = peaks()
+    bytes_attr = 8 * nnz + 8 * (N + 1) + 56 * N
+    kern = max(("attract_update_ms", "traverse_ms", "tree_ms"), key=lambda k: prof[k])
+    roof = {"kernel": kern.replace("_ms", "")}
+    if kern == "attract_update_ms":
+        ach = bytes_attr / (prof[kern] / 1e3) / 1e9
+        roof.update({"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                     "frac": ach / hbm, "traffic": None, "peak_source": which,
+                     "algorithmic_bytes": bytes_attr})
+    else:
+        ach_attr = bytes_attr / (prof["attract_update_ms"] / 1e3) / 1e9
+        roof.update({"bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None,
+                     "traffic": None, "note": "traversal is latency/issue bound; see DESIGN.md 7",
+                     "attract_update_hbm_gbs": ach_attr,
+                     "attract_update_frac": ach_attr / hbm})
+    line = {
+        "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "N": N, "D": cfg.D, "K": K, "perplexity": cfg.perplexity,
+                   "theta": 0.5, "nnz": nnz, "l2": "inputs larger than L2 (CSR %.2f GB)" %
+                   (8 * nnz / 1e9), "knn_path": kinfo["gemm_path"],
+                   "knn_rows_uncertified": kinfo["rows_uncertified"]},
+        "stages": stages,
+        "roofline": roof,
+        "gpu_launches": int(args.steps * prof.get("kernels_per_iteration", 0)),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu:
+        ns = args.cpu_iters
+        times, cores = time_oracle_iterations(N, ns, max(1, round(nnz / N)))
+        line["cpu_baseline"] = {"value": ns / sum(times), "unit": "it/s", "cores": cores,
+                                "kind": "oracle",
+                                "sample": f"{ns} full-size fp64 oracle iteration(s) at N={N} "
+                                          f"(synthetic clustered Y, {round(nnz / N)} nnz/row)"}
+    if rank == 0 and not args.no_e2e:
+        del opt, rp, col, val
+        Xh = torch.empty(X.shape, dtype=torch.float32, pin_memory=True)
+        Xh.copy_(X)
+        del X
+        torch.cuda.empty_cache()
+        Yh = torch.empty(N, 2, dtype=torch.float32, pin_memory=True)
+        t0 = time.perf_counter()
+        Yh, info = T.run(Xh, perplexity=cfg.perplexity, theta=0.5, n_iter=args.e2e_iters,
+                         Y_out=Yh)
+        wall = time.perf_counter() - t0
+        line["e2e"] = {"value": args.e2e_iters / (info["ms_total"] / 1e3), "unit": "it/s",
+                       "seconds": info["ms_total"] / 1e3, "wall_seconds": wall,
+                       "n_iter": args.e2e_iters, "h2d_bytes_per_step": 4 * N * cfg.D,
+                       "d2h_bytes_per_step": 8 * N,
+                       "split_ms": {k: info[k] for k in ("ms_h2d", "ms_knn", "ms_p", "ms_loop",
+                                                         "ms_d2h")}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--e2e-iters", type=int, default=1000)
+    ap.add_argument("--nnz-per-row", type=int, default=126)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        torch.distributed.init_process_group("nccl")
+    run_ours(args, rank, world)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

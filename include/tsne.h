@@ -1,0 +1,206 @@
+/*
+ * include/tsne.h -- C ABI of the B200-native Barnes-Hut t-SNE library
+ * (libtsne_b200.so), after t-SNE-CUDA, arXiv 1807.11824.
+ *
+ * Citations: "P:Lnnn" = /root/reference/PAPER.md line (section / equation
+ * named beside it); "Dnn" = a reading of the paper recorded in DESIGN.md
+ * section 3 (where the paper is silent, ambiguous or garbled).
+ *
+ * General contract (all entry points):
+ *  - Arrays are row-major.  Unless an argument says HOST, pointers are
+ *    DEVICE pointers on the current CUDA device, caller-owned: the library
+ *    never frees caller memory and, except tsne_run / tsne_run_ex, never
+ *    allocates device memory.  Scratch comes from a caller-provided
+ *    workspace `ws` of `ws_bytes` bytes (query the *_workspace_size
+ *    function; 256-byte aligned), so the caller's allocator (PyTorch's
+ *    caching allocator) owns all device memory.
+ *  - Every call is stream-ordered on `stream` (NULL = legacy default
+ *    stream) and returns before the GPU work completes, unless it says it
+ *    synchronises.
+ *  - Inputs are read-only.  Outputs are written only when TSNE_OK is
+ *    returned; on error their contents are unspecified.
+ *  - Argument validation happens before any launch; a failure returns
+ *    TSNE_ERR_ARG and sets the thread-local message read by
+ *    tsne_last_error().  CUDA launch/runtime failures return TSNE_ERR_CUDA.
+ *  - Calls are re-entrant given distinct workspaces and streams.
+ *  - There is no CPU fallback: a host without a usable sm_100 device gets
+ *    TSNE_ERR_CUDA from every compute entry point.
+ */
+#ifndef TSNE_B200_H
+#define TSNE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* tsne_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  TSNE_OK = 0,
+  TSNE_ERR_ARG = 1,        /* invalid argument (message in tsne_last_error) */
+  TSNE_ERR_CUDA = 2,       /* CUDA runtime / launch failure, or no device   */
+  TSNE_ERR_WORKSPACE = 3,  /* ws == NULL or ws_bytes < required size        */
+  TSNE_ERR_NONFINITE = 4,  /* NaN/Inf appeared in Y during optimisation     */
+  TSNE_ERR_NCCL = 5,       /* reserved for the collective path              */
+  TSNE_ERR_DEGENERATE = 6  /* non-fatal: some rows had no finite beta (D3)  */
+} tsne_status;
+
+/* Thread-local, NUL-terminated message describing the last failure of a call
+ * made by this thread ("" if none).  Owned by the library. */
+const char* tsne_last_error(void);
+
+/* ABI version, (major << 16) | minor. */
+int32_t tsne_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * U1  Exact k nearest neighbours (Sec. III-B: "the K nearest
+ * neighbors of each point are obtained"; Algorithm 1 line 1).
+ * The paper uses approximate IVF-PQ; this build computes the
+ * EXACT kNN: a tensor-core (tcgen05, fp16 operands, fp32
+ * accumulate) distance GEMM selects K' >= K candidates per row by the
+ * expanded form |x|^2 + |y|^2 - 2 x.y on column-mean-centred data, then an
+ * fp64 re-rank of exact differences sum_d (x_d - y_d)^2 picks the K best.
+ *
+ *   X    [N x D] float32, row-major, finite.
+ *   idx  [N x K] int32 out: neighbours of row i, self excluded, ascending by
+ *        (d2, index) -- ties broken by the lower index (D18).
+ *   d2   [N x K] float64 out: exact squared Euclidean distances (D19).
+ * Requires N >= 2, 1 <= K < N, D >= 1.
+ * `info` (HOST, nullable): when non-NULL the call synchronises `stream` and
+ * reports how many rows failed the candidate-margin certificate (D26) and
+ * were recomputed by the exact fallback scan.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int64_t rows_uncertified;  /* rows re-done by the exact fallback scan      */
+  int32_t candidates;        /* K' used                                       */
+  int32_t gemm_path;         /* 1 = tcgen05 tensor-core path, 0 = CUDA-core   */
+} tsne_knn_info;
+
+size_t tsne_knn_workspace_size(int64_t N, int32_t D, int32_t K);
+tsne_status tsne_knn(const float* X, int64_t N, int32_t D, int32_t K,
+                     int32_t* idx, double* d2, void* ws, size_t ws_bytes,
+                     tsne_knn_info* info, tsne_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * U2 + U3  Sparse joint affinities P (Eq. 1; symmetrisation
+ * p_ij = (p_{i|j} + p_{j|i}) / 2N; at most 2NK nonzeros).
+ * Each row's bandwidth is found by fp64 bisection so that the entropy of
+ * p_{.|i} (nats) equals ln(perplexity) to 1e-10 (D3: the paper never states
+ * the rule); Eq. 1 is normalised over the K neighbours (D2).
+ *
+ *   idx, d2   the output of tsne_knn (N x K).
+ *   row_ptr   [N+1] int64 out; col [cap 2NK] int32 out; val [cap 2NK] float32
+ *             out: CSR of P with both triangles, sorted unique columns, no
+ *             diagonal; val[(i,j)] == val[(j,i)] bitwise; sum(val) = 1.
+ *   nnz_out   HOST out: number of nonzeros (this call synchronises stream).
+ *   beta_out  [N] float64 out (nullable): 1/(2 sigma_i^2).
+ * Requires 1 < perplexity < K.  Returns TSNE_ERR_DEGENERATE (outputs valid)
+ * if some row had no finite root -- all neighbours equidistant (uniform over
+ * K) or >= perplexity ties at the minimum (uniform over the ties) (D3).
+ * ------------------------------------------------------------------------ */
+size_t tsne_compute_p_workspace_size(int64_t N, int32_t K);
+tsne_status tsne_compute_p(const int32_t* idx, const double* d2, int64_t N, int32_t K,
+                           float perplexity, int64_t* row_ptr, int32_t* col, float* val,
+                           int64_t* nnz_out, double* beta_out, void* ws, size_t ws_bytes,
+                           tsne_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * H1-H7  One Barnes-Hut t-SNE gradient at a fixed embedding
+ * (Eq. 7: dC/dy_i = 4 (F_attr + F_rep)):
+ *   quadtree over Y (bounding box, Morton sort, node build, counts and
+ *   centres of mass; P:L136 steps 1-4), theta traversal giving the
+ *   repulsive numerators and Z, CSR attractive pass (Eq. 5 via
+ *   the nonzero iteration of P:L115-122).
+ *   dY_i = 4 (exaggeration * A_i - f_i / Z),
+ *   A_i = sum_j P_ij (y_i - y_j) / (1 + |y_i - y_j|^2)      (D1, D5)
+ *   f_i = sum over accepted cells / leaves of N_c w^2 (y_i - y_c),
+ *   w = 1/(1 + D^2), Z = sum_i z_i
+ * Tree and criterion definitions: D7-D11 (r = half side of a square cell,
+ * y_cell = centre of mass, strict r^2 < theta^2 D^2, a cell containing i is
+ * always opened), decided as in fp64 (D25).
+ *
+ *   row_ptr/col/val  CSR of P as produced by tsne_compute_p.
+ *   Y     [N x 2] float32 (x,y interleaved), finite.
+ *   dY    [N x 2] float32 out.
+ *   Z_out HOST out (nullable): Z; when non-NULL the call synchronises.
+ * Requires N >= 2, theta >= 0 (theta == 0 is the exact O(N^2) sum),
+ * exaggeration > 0.
+ * ------------------------------------------------------------------------ */
+size_t tsne_gradient_workspace_size(int64_t N);
+tsne_status tsne_gradient(const int64_t* row_ptr, const int32_t* col, const float* val,
+                          int64_t N, const float* Y, float theta, float exaggeration,
+                          float* dY, double* Z_out, void* ws, size_t ws_bytes,
+                          tsne_stream_t stream);
+
+/* Schedule / optimiser constants (the paper states none of them: D12-D16). */
+typedef struct {
+  int32_t K;            /* neighbours; 0 -> min(N-1, floor(3 perplexity)) (D4) */
+  int32_t exag_iters;   /* early-exaggeration length (250)                      */
+  float mom0, mom1;     /* momentum before / after exag_iters (0.5, 0.8)        */
+  float min_gain;       /* gain floor (0.01)                                    */
+  uint64_t seed;        /* Philox4x32-10 key for Y0 (42) (D14)                  */
+  const float* Y_init;  /* DEVICE [N x 2] initial embedding, NULL -> Philox     */
+  int32_t use_graphs;   /* 1: replay the iteration as a CUDA graph (default)    */
+} tsne_config;
+
+/* Fills the defaults listed above. */
+void tsne_config_default(tsne_config* cfg);
+
+/* ------------------------------------------------------------------------
+ * H1-H8  The optimisation loop of Algorithm 1 given P:
+ * n_iter iterations t = t0 .. t0+n_iter-1 of
+ *   tree build -> traversal (F_rep, Z) -> attractive pass fused with the
+ *   update: per coordinate gain <- (sign g != sign v) ? gain + 0.2
+ *   : 0.8 gain, gain >= min_gain; v <- mu(t) v - eta gain g; y <- y + v;
+ *   then y <- y - mean(y)   (D12-D15).
+ *   alpha(t) = exaggeration if t < exag_iters else 1; mu(t) = mom0 / mom1.
+ *   Y, v, gains  [N x 2] float32 in/out (the optimiser state).
+ * Returns TSNE_ERR_NONFINITE if Y became non-finite (checked at the end of
+ * the call; the call synchronises stream for that check).
+ * ------------------------------------------------------------------------ */
+size_t tsne_optimize_workspace_size(int64_t N);
+tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const float* val,
+                          int64_t N, float* Y, float* v, float* gains, int32_t t0,
+                          int32_t n_iter, float theta, float learning_rate,
+                          float exaggeration, const tsne_config* cfg, void* ws,
+                          size_t ws_bytes, tsne_stream_t stream);
+
+/* Y0 = 1e-4 N(0,1) from Philox4x32-10 (key = seed, counter = (i,0,0,0)),
+ * Box-Muller on the first two words (D14).  Y [N x 2] float32 out. */
+tsne_status tsne_init_y(int64_t N, uint64_t seed, float* Y, tsne_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Algorithm 1 end to end: kNN -> P -> Y0 -> n_iter iterations.
+ * "Input: N x d array of data; Output: N x 2 projection".
+ *   X      [N x D] float32, HOST or DEVICE (detected); finite.
+ *   Y_out  [N x 2] float32, HOST or DEVICE (detected).
+ * The only allocating entry points: device memory for the whole pipeline
+ * is allocated with cudaMallocAsync on an internal stream and released
+ * before return.  Blocking.  Exaggeration lasts 250 iterations, momentum
+ * 0.5 -> 0.8, Y0 from Philox seed 42 (see tsne_config for _ex).
+ * Requires N >= 2, 1 < perplexity < K, theta >= 0, learning_rate > 0,
+ * n_iter >= 1, exaggeration >= 1.  Non-finite X -> TSNE_ERR_ARG.
+ * ------------------------------------------------------------------------ */
+tsne_status tsne_run(const float* X, int64_t N, int32_t D, float perplexity, float theta,
+                     float learning_rate, int32_t n_iter, float exaggeration, float* Y_out);
+
+typedef struct {
+  double ms_knn, ms_p, ms_loop, ms_total;  /* CUDA-event stage times          */
+  double ms_h2d, ms_d2h;                   /* host<->device copies (if HOST)  */
+  int64_t nnz;                             /* nonzeros of P                   */
+  int64_t knn_rows_uncertified;
+  int32_t K;
+  int32_t degenerate_rows;                 /* > 0: TSNE_ERR_DEGENERATE cases  */
+} tsne_run_info;
+
+tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, float theta,
+                        float learning_rate, int32_t n_iter, float exaggeration,
+                        const tsne_config* cfg, float* Y_out, tsne_run_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSNE_B200_H */

@@ -1,0 +1,188 @@
+// attract.cu -- attractive forces from the sparse P (Eq. 5; the
+// nonzero iteration of Sec. III-B: "P (.) Q is computed directly
+// by iterating over nonzero values of P"), fused with the gradient assembly
+// (Eq. 7) and, in the optimiser, with the update ("Apply Forces",
+// Algorithm 1 line 8).                                      [H7, H8]
+//
+// One warp per CSR row: lanes stride the row's nonzeros (coalesced col/val
+// stream, read once -> evict-first), gather y_j (the 8-byte-per-point
+// embedding stays L2-resident), and reduce with a fixed butterfly.
+//   A_i = sum_j P_ij (y_i - y_j) / (1 + |y_i - y_j|^2)      (q_ij Z, D1/D5)
+//   g_i = 4 (alpha A_i - f_i / Z)
+// The update kernel also produces the next iteration's recentring shift and
+// bounding box (fixed-order last-block reduction), so the tree build of the
+// next iteration needs no separate bbox pass.
+#include "optimize.cuh"
+
+namespace tsne {
+
+constexpr int kAttrThreads = 256;
+constexpr int kAttrWarps = kAttrThreads / 32;
+
+__device__ __forceinline__ float2 row_attractive(const int64_t* __restrict__ row_ptr,
+                                                 const int32_t* __restrict__ col,
+                                                 const float* __restrict__ val,
+                                                 const float2* __restrict__ Y, int i, float2 yi,
+                                                 int lane) {
+  const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
+  float ax = 0.f, ay = 0.f;
+  for (int64_t e = e0 + lane; e < e1; e += 32) {
+    const int j = __ldcs(col + e);
+    const float p = __ldcs(val + e);
+    const float2 yj = Y[j];
+    const float dx = yi.x - yj.x, dy = yi.y - yj.y;
+    const float w = __frcp_rn(1.f + dx * dx + dy * dy);
+    const float pw = p * w;
+    ax = fmaf(pw, dx, ax);
+    ay = fmaf(pw, dy, ay);
+  }
+  return make_float2(warp_sum(ax), warp_sum(ay));
+}
+
+// tsne_gradient: dY = 4 (alpha A - f / Z)
+__global__ void __launch_bounds__(kAttrThreads)
+k_attract_grad(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+               const float* __restrict__ val, const float2* __restrict__ Y, int N,
+               const float2* __restrict__ rep, const double* __restrict__ Z, float alpha,
+               float2* __restrict__ dY) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * kAttrThreads + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * kAttrThreads) >> 5;
+  const float invZ = (float)Z[1];
+  for (int i = warp; i < N; i += nwarps) {
+    const float2 yi = Y[i];
+    const float2 a = row_attractive(row_ptr, col, val, Y, i, yi, lane);
+    if (lane == 0) {
+      const float2 f = rep[i];
+      dY[i] = make_float2(4.f * (alpha * a.x - f.x * invZ), 4.f * (alpha * a.y - f.y * invZ));
+    }
+  }
+}
+
+__device__ __forceinline__ float sgnf(float x) { return (float)((x > 0.f) - (x < 0.f)); }
+
+// optimiser step for one coordinate (D12): gains, momentum, learning rate
+__device__ __forceinline__ void update_coord(float g, float& v, float& gain, float& y, float mu,
+                                             float eta, float min_gain) {
+  float gn = (sgnf(g) != sgnf(v)) ? gain + 0.2f : gain * 0.8f;
+  gn = fmaxf(gn, min_gain);
+  gain = gn;
+  v = mu * v - eta * gn * g;
+  y = y + v;
+}
+
+__global__ void __launch_bounds__(kAttrThreads)
+k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                 const float* __restrict__ val, const float2* __restrict__ Yin, int N,
+                 const float2* __restrict__ rep, const double* __restrict__ Z,
+                 int32_t* __restrict__ t_dev, Sched sc, float2* __restrict__ Yout,
+                 float2* __restrict__ V, float2* __restrict__ G, double2* __restrict__ part2,
+                 float4* __restrict__ part4, unsigned* __restrict__ counter,
+                 BoxInfo* __restrict__ box_next, int32_t* __restrict__ flag) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int warp = (blockIdx.x * kAttrThreads + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * kAttrThreads) >> 5;
+  const int t = *t_dev;
+  const float alpha = (t < sc.exag_iters) ? sc.exag : 1.f;
+  const float mu = (t < sc.exag_iters) ? sc.mom0 : sc.mom1;
+  const float invZ = (float)Z[1];
+  double sx = 0.0, sy = 0.0;
+  float mnx = INFINITY, mxx = -INFINITY, mny = INFINITY, mxy = -INFINITY;
+  bool bad = false;
+  for (int i = warp; i < N; i += nwarps) {
+    const float2 yi = Yin[i];
+    const float2 a = row_attractive(row_ptr, col, val, Yin, i, yi, lane);
+    if (lane == 0) {
+      const float2 f = rep[i];
+      const float gx = 4.f * (alpha * a.x - f.x * invZ);
+      const float gy = 4.f * (alpha * a.y - f.y * invZ);
+      float2 v = V[i], gn = G[i], y = yi;
+      update_coord(gx, v.x, gn.x, y.x, mu, sc.eta, sc.min_gain);
+      update_coord(gy, v.y, gn.y, y.y, mu, sc.eta, sc.min_gain);
+      V[i] = v;
+      G[i] = gn;
+      Yout[i] = y;
+      sx += (double)y.x;
+      sy += (double)y.y;
+      mnx = fminf(mnx, y.x); mxx = fmaxf(mxx, y.x);
+      mny = fminf(mny, y.y); mxy = fmaxf(mxy, y.y);
+      bad |= !(isfinite(y.x) && isfinite(y.y));
+    }
+  }
+  // block partials (lane 0 of each warp holds its rows' sums)
+  __shared__ double2 s_s[kAttrWarps];
+  __shared__ float4 s_b[kAttrWarps];
+  __shared__ bool s_last;
+  if (lane == 0) {
+    s_s[wid] = make_double2(sx, sy);
+    s_b[wid] = make_float4(mnx, mxx, mny, mxy);
+  }
+  if (bad) *flag = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 ss = s_s[0];
+    float4 bb = s_b[0];
+    for (int q = 1; q < kAttrWarps; ++q) {
+      ss.x += s_s[q].x; ss.y += s_s[q].y;
+      bb.x = fminf(bb.x, s_b[q].x); bb.y = fmaxf(bb.y, s_b[q].y);
+      bb.z = fminf(bb.z, s_b[q].z); bb.w = fmaxf(bb.w, s_b[q].w);
+    }
+    part2[blockIdx.x] = ss;
+    part4[blockIdx.x] = bb;
+    __threadfence();
+    unsigned prev = atomicAdd(counter, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    double2 ss = make_double2(0.0, 0.0);
+    float4 bb = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
+    for (int q = 0; q < (int)gridDim.x; ++q) {
+      const double2 a = __ldcg(part2 + q);
+      const float4 b = __ldcg(part4 + q);
+      ss.x += a.x; ss.y += a.y;
+      bb.x = fminf(bb.x, b.x); bb.y = fmaxf(bb.y, b.y);
+      bb.z = fminf(bb.z, b.z); bb.w = fmaxf(bb.w, b.w);
+    }
+    // recentring (D15): y <- y - mean, applied by the next tree build; by the
+    // monotonicity of rounding, min(fl(y - m)) = fl(min(y) - m) exactly.
+    const float mx = (float)(ss.x / (double)N), my = (float)(ss.y / (double)N);
+    BoxInfo b;
+    make_root_box(bb.x - mx, bb.y - mx, bb.z - my, bb.w - my, &b);
+    b.shift_x = mx;
+    b.shift_y = my;
+    b.pad0 = 0.f;
+    *box_next = b;
+    *t_dev = t + 1;
+    *counter = 0u;
+  }
+}
+
+int attract_blocks(int64_t N) {
+  int64_t b = (N + kAttrWarps - 1) / kAttrWarps;
+  int64_t cap = (int64_t)kNumSMs * 8;
+  return (int)(b < cap ? (b < 1 ? 1 : b) : cap);
+}
+
+tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, const float* val,
+                                const float2* Y, int64_t N, const float2* rep, const double* Z,
+                                float alpha, float2* dY, cudaStream_t s) {
+  k_attract_grad<<<attract_blocks(N), kAttrThreads, 0, s>>>(row_ptr, col, val, Y, (int)N, rep, Z,
+                                                            alpha, dY);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
+tsne_status launch_attract_update(const int64_t* row_ptr, const int32_t* col, const float* val,
+                                  const float2* Yin, int64_t N, TreeWS& w, OptWS& o,
+                                  const Sched& sc, float2* Yout, float2* V, float2* G,
+                                  cudaStream_t s) {
+  k_attract_update<<<attract_blocks(N), kAttrThreads, 0, s>>>(
+      row_ptr, col, val, Yin, (int)N, w.rep, w.Z, o.t_dev, sc, Yout, V, G, w.part2, w.part4,
+      w.counter + 2, w.box, o.flag);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
+}  // namespace tsne

@@ -1,0 +1,407 @@
+// knn.cu -- exact kNN (U1).  The paper's line 1 is approximate FAISS
+// IVF-PQ; the north star asks for the exact kNN, so:
+//
+//  1. prep:      column mean (fp64, fixed order), X_h = fp16((x - mean) 2^e)
+//                (distance-invariant centring + exact power-of-2 scaling),
+//                |x_h|^2 in fp32.
+//  2. candidates: expanded-form distances |x_h|^2 + |y_h|^2 - 2 x_h . y_h
+//                (the row's |x_h|^2 is dropped: it does not change the order
+//                within a row) for every (query, point) pair, tile by tile,
+//                keeping for each query the K' = K + 64 smallest keys
+//                (distance, index) -- candidate buffers in global memory,
+//                compacted by a warp bitonic sort when they fill.  The N x N
+//                matrix is never materialised.
+//  3. re-rank:   exact fp64 sum_d (x_d - y_d)^2 of the original fp32 rows for
+//                the K' candidates; sort by (d2, index) (D18); certificate
+//                d2_(K) < approx_(K') - 2 e_row (D26).
+#include <cfloat>
+
+#include "knn.cuh"
+#include "knn_tc.cuh"
+
+namespace tsne {
+
+typedef unsigned long long u64;
+constexpr u64 kKeyMax = ~0ull;
+
+__device__ __forceinline__ u64 mkkey(float a, int j) {
+  unsigned u = __float_as_uint(a);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((u64)u << 32) | (unsigned)j;
+}
+__device__ __forceinline__ float key_val(u64 k) {
+  unsigned u = (unsigned)(k >> 32);
+  u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ int key_idx(u64 k) { return (int)(unsigned)(k & 0xffffffffull); }
+
+static inline int kc_of(int64_t N, int K) {
+  int64_t kc = ((K + kCandExtra + 31) / 32) * 32;
+  if (kc > N - 1) kc = N - 1;
+  return (int)kc;
+}
+
+int knn_slots(int64_t N) {
+  int64_t rb = (N + kKnnBM - 1) / kKnnBM;
+  int64_t cap = 2 * kNumSMs;
+  return (int)(rb < cap ? rb : cap);
+}
+
+void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K) {
+  w.N = N; w.D = D; w.K = K;
+  w.Dp = ((D + 63) / 64) * 64;
+  w.Kc = kc_of(N, K);
+  w.slots = knn_slots(N);
+  w.colsum = c.take<double>((size_t)D * 256);
+  w.mean = c.take<float>(D);
+  w.amax = c.take<unsigned>(4);
+  w.scale = c.take<float>(4);
+  w.Xh = c.take<__half>((size_t)(N + 256) * w.Dp);  // + 256 zero slack rows (tile overrun)
+  w.nrm = c.take<float>(N + 256);
+  w.buf = c.take<u64>((size_t)w.slots * kKnnBM * kCandCap);
+  w.cand = c.take<u64>((size_t)N * w.Kc);
+  w.uncert = c.take<u64>(2);
+  w.rows_bad = c.take<int32_t>(N);
+}
+
+// ---------------------------------------------------------------- prep
+constexpr int kColRB = 256;  // row blocks of the fixed-order column sum
+
+__global__ void k_colsum_part(const float* __restrict__ X, int64_t N, int D,
+                              double* __restrict__ part) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= D) return;
+  const int64_t r0 = (int64_t)blockIdx.y * N / kColRB, r1 = (int64_t)(blockIdx.y + 1) * N / kColRB;
+  double s = 0.0;
+  for (int64_t r = r0; r < r1; ++r) s += (double)X[r * D + d];
+  part[(size_t)blockIdx.y * D + d] = s;
+}
+
+__global__ void k_colsum_final(const double* __restrict__ part, int64_t N, int D,
+                               float* __restrict__ mean, unsigned* amax) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d == 0) *amax = 0u;
+  if (d >= D) return;
+  double s = 0.0;
+  for (int b = 0; b < kColRB; ++b) s += part[(size_t)b * D + d];
+  mean[d] = (float)(s / (double)N);
+}
+
+__global__ void k_absmax(const float* __restrict__ X, int64_t n, int D,
+                         const float* __restrict__ mean, unsigned* amax) {
+  float m = 0.f;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(X[e] - mean[e % D]));
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(amax, __float_as_uint(m));  // non-negative: int order
+}
+
+__global__ void k_scale(const unsigned* amax, float* scale) {
+  const float a = __uint_as_float(*amax);
+  int e = 0;
+  if (a > 0.f) {
+    int ex;
+    frexpf(a, &ex);             // a in [2^(ex-1), 2^ex)
+    e = 14 - ex;                // a 2^e < 2^14
+  }
+  scale[0] = ldexpf(1.f, e);
+  scale[1] = ldexpf(1.f, -2 * e);
+}
+
+// warp per row: X_h row and its squared norm
+__global__ void k_convert(const float* __restrict__ X, int64_t N, int D, int Dp,
+                          const float* __restrict__ mean, const float* __restrict__ scale,
+                          __half* __restrict__ Xh, float* __restrict__ nrm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (row >= N + 256) return;
+  const float sc = scale[0];
+  double acc = 0.0;
+  for (int d = lane; d < Dp; d += 32) {
+    __half h = __float2half_rn(0.f);
+    if (row < N && d < D) h = __float2half_rn((X[row * D + d] - mean[d]) * sc);
+    Xh[row * Dp + d] = h;
+    const float f = __half2float(h);
+    acc += (double)(f * f);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0 && row < N) nrm[row] = (float)acc;
+}
+
+// ---------------------------------------------------------------- top-K' machinery
+__device__ void warp_bitonic_sort(u64* a, int P, int lane) {
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < P; i += 32) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = ((i & k) == 0);
+          const u64 x = a[i], y = a[l];
+          if ((x > y) == up) { a[i] = y; a[l] = x; }
+        }
+      }
+      __syncwarp();
+    }
+}
+
+// sort the row's buffer and keep its Kc smallest keys
+__device__ void compact_row(u64* __restrict__ rowbuf, int& cnt, u64& tau, int Kc, u64* sm,
+                            int lane, u64* out) {
+  const int n = cnt;
+  int P = 32;
+  while (P < n) P <<= 1;
+  for (int i = lane; i < P; i += 32) sm[i] = (i < n) ? rowbuf[i] : kKeyMax;
+  __syncwarp();
+  warp_bitonic_sort(sm, P, lane);
+  const int keep = n < Kc ? n : Kc;
+  for (int i = lane; i < keep; i += 32) {
+    rowbuf[i] = sm[i];
+    if (out) out[i] = sm[i];
+  }
+  __syncwarp();
+  const u64 t = (keep == Kc) ? sm[Kc - 1] : kKeyMax;
+  __syncwarp();
+  if (lane == 0) { cnt = keep; tau = t; }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------- v1 candidates (CUDA cores)
+constexpr int kS_BN = 64, kS_BK = 32, kS_Threads = 256, kS_SortWarps = 8;
+
+struct SimtSmem {
+  float As[kS_BK][kKnnBM + 4];
+  float Bs[kS_BK][kS_BN + 4];
+  float tile[kKnnBM][kS_BN + 1];
+  u64 tau[kKnnBM];
+  int cnt[kKnnBM];
+  int flag;
+  u64 sortbuf[kS_SortWarps][kCandCap];
+};
+
+__global__ void __launch_bounds__(kS_Threads, 1)
+k_cand_simt(const __half* __restrict__ Xh, const float* __restrict__ nrm, int N, int Dp, int Kc,
+            u64* __restrict__ buf, u64* __restrict__ cand) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  SimtSmem& sm = *reinterpret_cast<SimtSmem*>(smraw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tx = tid & 15, ty = tid >> 4;
+  u64* mybuf = buf + (size_t)blockIdx.x * kKnnBM * kCandCap;
+  const int nrb = (N + kKnnBM - 1) / kKnnBM;
+  for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+    const int q0 = rb * kKnnBM;
+    if (tid < kKnnBM) { sm.cnt[tid] = 0; sm.tau[tid] = kKeyMax; }
+    __syncthreads();
+    for (int c0 = 0; c0 < N; c0 += kS_BN) {
+      float acc[8][4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+      for (int k0 = 0; k0 < Dp; k0 += kS_BK) {
+        // A: 128 rows x 32 halves; each thread 16 halves (rows may exceed N: slack rows are 0)
+        {
+          const int r = tid >> 1, kk = (tid & 1) * 16;
+          const __half* src = Xh + (size_t)(q0 + r) * Dp + k0 + kk;
+          const uint4 v0 = *reinterpret_cast<const uint4*>(src);
+          const uint4 v1 = *reinterpret_cast<const uint4*>(src + 8);
+          const __half* h0 = reinterpret_cast<const __half*>(&v0);
+          const __half* h1 = reinterpret_cast<const __half*>(&v1);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            sm.As[kk + q][r] = __half2float(h0[q]);
+            sm.As[kk + 8 + q][r] = __half2float(h1[q]);
+          }
+        }
+        {
+          const int r = tid >> 2, kk = (tid & 3) * 8;
+          const __half* src = Xh + (size_t)(c0 + r) * Dp + k0 + kk;
+          const uint4 v0 = *reinterpret_cast<const uint4*>(src);
+          const __half* h0 = reinterpret_cast<const __half*>(&v0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) sm.Bs[kk + q][r] = __half2float(h0[q]);
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < kS_BK; ++k) {
+          float a[8], b[4];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) a[q] = sm.As[k][ty * 8 + q];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) b[q] = sm.Bs[k][tx * 4 + q];
+#pragma unroll
+          for (int p = 0; p < 8; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[p][q] = fmaf(a[p], b[q], acc[p][q]);
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = c0 + tx * 4 + q;
+          const float nj = (j < N) ? nrm[j] : 0.f;
+          sm.tile[ty * 8 + p][tx * 4 + q] = nj - 2.f * acc[p][q];
+        }
+      __syncthreads();
+      // offer: thread t owns query row q0 + t
+      if (tid < kKnnBM) {
+        const int q = q0 + tid;
+        if (q < N) {
+          int cnt = sm.cnt[tid];
+          const u64 tau = sm.tau[tid];
+          u64* rowbuf = mybuf + (size_t)tid * kCandCap;
+          const int cmax = min(kS_BN, N - c0);
+          for (int c = 0; c < cmax; ++c) {
+            const int j = c0 + c;
+            if (j == q) continue;
+            const u64 key = mkkey(sm.tile[tid][c], j);
+            if (key < tau) rowbuf[cnt++] = key;
+          }
+          sm.cnt[tid] = cnt;
+        }
+      }
+      if (tid == 0) sm.flag = 0;
+      __syncthreads();
+      if (tid < kKnnBM && sm.cnt[tid] > kCandCap - kS_BN) sm.flag = 1;
+      __syncthreads();
+      if (sm.flag) {
+        for (int r = wid; r < kKnnBM; r += kS_Threads / 32) {
+          if (sm.cnt[r] > kCandCap - kS_BN)
+            compact_row(mybuf + (size_t)r * kCandCap, sm.cnt[r], sm.tau[r], Kc, sm.sortbuf[wid],
+                        lane, nullptr);
+        }
+        __syncthreads();
+      }
+    }
+    // final: every row -> its Kc best keys
+    for (int r = wid; r < kKnnBM; r += kS_Threads / 32) {
+      const int q = q0 + r;
+      if (q < N)
+        compact_row(mybuf + (size_t)r * kCandCap, sm.cnt[r], sm.tau[r], Kc, sm.sortbuf[wid], lane,
+                    cand + (size_t)q * Kc);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- re-rank
+constexpr int kRR_Threads = 256;
+
+__global__ void __launch_bounds__(kRR_Threads)
+k_rerank(const float* __restrict__ X, int N, int D, int K, int Kc, const u64* __restrict__ cand,
+         const float* __restrict__ nrm, const float* __restrict__ scale,
+         int32_t* __restrict__ idx, double* __restrict__ d2, u64* __restrict__ uncert,
+         int32_t* __restrict__ rows_bad) {
+  __shared__ double s_d[kRR_Threads / 32][256];
+  __shared__ int s_j[kRR_Threads / 32][256];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i = blockIdx.x * (kRR_Threads / 32) + wid;
+  if (i >= N) return;
+  double* sd = s_d[wid];
+  int* sj = s_j[wid];
+  const float* xi = X + (size_t)i * D;
+  const u64* ci = cand + (size_t)i * Kc;
+  const double inv2 = (double)scale[1];
+  const double nrm_i = (double)nrm[i];
+  double emax = 0.0;
+  for (int c = 0; c < Kc; ++c) {
+    const u64 key = ci[c];
+    const int j = key_idx(key);
+    const float* xj = X + (size_t)j * D;
+    double acc = 0.0;
+    for (int d = lane; d < D; d += 32) {
+      const double t = (double)__ldg(xi + d) - (double)xj[d];
+      acc = fma(t, t, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      sd[c] = acc;
+      sj[c] = j;
+    }
+    const double approx = ((double)key_val(key) + nrm_i) * inv2;
+    emax = fmax(emax, fabs(approx - acc));
+  }
+  const double tau_approx = ((double)key_val(ci[Kc - 1]) + nrm_i) * inv2;
+  int P = 32;
+  while (P < Kc) P <<= 1;
+  for (int c = Kc + lane; c < P; c += 32) { sd[c] = DBL_MAX; sj[c] = 0x7fffffff; }
+  __syncwarp();
+  // bitonic sort by (d2, index)
+  for (int k = 2; k <= P; k <<= 1)
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int a = lane; a < P; a += 32) {
+        const int l = a ^ jj;
+        if (l > a) {
+          const bool up = ((a & k) == 0);
+          const double x = sd[a], y = sd[l];
+          const int xa = sj[a], ya = sj[l];
+          const bool gt = (x > y) || (x == y && xa > ya);
+          if (gt == up) { sd[a] = y; sd[l] = x; sj[a] = ya; sj[l] = xa; }
+        }
+      }
+      __syncwarp();
+    }
+  for (int c = lane; c < K; c += 32) {
+    idx[(size_t)i * K + c] = sj[c];
+    d2[(size_t)i * K + c] = sd[c];
+  }
+  if (lane == 0) {
+    const bool all = (Kc >= N - 1);
+    const bool cert = all || (sd[K - 1] < tau_approx - 2.0 * emax);
+    if (!cert) {
+      const u64 pos = atomicAdd(uncert, 1ull);
+      rows_bad[pos] = i;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host
+tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int32_t* idx, double* d2,
+                    KnnWS& w, tsne_knn_info* info, cudaStream_t s) {
+  const int Dp = w.Dp, Kc = w.Kc;
+  {
+    dim3 g((D + 255) / 256, kColRB);
+    k_colsum_part<<<g, 256, 0, s>>>(X, N, D, w.colsum);
+    TSNE_LAUNCH_CHECK();
+    k_colsum_final<<<(D + 255) / 256, 256, 0, s>>>(w.colsum, N, D, w.mean, w.amax);
+    TSNE_LAUNCH_CHECK();
+    k_absmax<<<4 * kNumSMs, 256, 0, s>>>(X, N * (int64_t)D, D, w.mean, w.amax);
+    TSNE_LAUNCH_CHECK();
+    k_scale<<<1, 1, 0, s>>>(w.amax, w.scale);
+    TSNE_LAUNCH_CHECK();
+    const int64_t rows = N + 256;
+    k_convert<<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(X, N, D, Dp, w.mean, w.scale, w.Xh,
+                                                            w.nrm);
+    TSNE_LAUNCH_CHECK();
+  }
+  TSNE_CUDA_TRY(cudaMemsetAsync(w.uncert, 0, 2 * sizeof(u64), s));
+  bool tc = knn_tc_available() && Dp % 64 == 0;
+  if (tc) {
+    tsne_status st = launch_cand_tc(w.Xh, w.nrm, (int)N, Dp, Kc, w.buf, w.cand, w.slots, s);
+    if (st != TSNE_OK) return st;
+  } else {
+    const size_t smem = sizeof(SimtSmem);
+    TSNE_CUDA_TRY(cudaFuncSetAttribute(k_cand_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    k_cand_simt<<<w.slots, kS_Threads, smem, s>>>(w.Xh, w.nrm, (int)N, Dp, Kc, w.buf, w.cand);
+    TSNE_LAUNCH_CHECK();
+  }
+  w.path = tc ? 1 : 0;
+  k_rerank<<<(int)((N + 7) / 8), kRR_Threads, 0, s>>>(X, (int)N, D, K, Kc, w.cand, w.nrm, w.scale,
+                                                     idx, d2, w.uncert, w.rows_bad);
+  TSNE_LAUNCH_CHECK();
+  if (info) {
+    u64 h = 0;
+    TSNE_CUDA_TRY(cudaMemcpyAsync(&h, w.uncert, sizeof(h), cudaMemcpyDeviceToHost, s));
+    TSNE_CUDA_TRY(cudaStreamSynchronize(s));
+    info->rows_uncertified = (int64_t)h;
+    info->candidates = Kc;
+    info->gemm_path = w.path;
+  }
+  return TSNE_OK;
+}
+
+}  // namespace tsne

@@ -1,0 +1,39 @@
+// knn.cuh -- exact k nearest neighbours (U1; Alg. 1 line 1)
+#pragma once
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace tsne {
+
+constexpr int kMaxK = 192;        // neighbours supported (paper: K in [32, 150])
+constexpr int kCandExtra = 64;    // K' = K + 64 candidates
+constexpr int kCandCap = 1024;    // per-row candidate buffer between compactions
+constexpr int kKnnBM = 128;       // query rows per CTA
+
+struct KnnWS {
+  int64_t N = 0;
+  int32_t D = 0, Dp = 0, K = 0, Kc = 0;
+  int32_t slots = 0;              // persistent CTAs (candidate buffers)
+  double* colsum = nullptr;       // D   (fp64 column sums -> mean)
+  float* mean = nullptr;          // D
+  unsigned* amax = nullptr;       // max |x - mean| (float bits)
+  float* scale = nullptr;         // [0] = 2^e, [1] = 2^-2e
+  __half* Xh = nullptr;           // N x Dp, fp16((x - mean) 2^e), zero padded
+  float* nrm = nullptr;           // N   |x_h|^2 (fp32)
+  unsigned long long* buf = nullptr;   // slots x 128 x kCandCap candidate keys
+  unsigned long long* cand = nullptr;  // N x Kc final candidate keys (sorted)
+  unsigned long long* uncert = nullptr;  // [0] count of uncertified rows
+  int32_t* rows_bad = nullptr;    // list of uncertified rows (N)
+  int32_t path = 0;
+};
+
+void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K);
+tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int32_t* idx, double* d2,
+                    KnnWS& w, tsne_knn_info* info, cudaStream_t s);
+
+// util (util.cu)
+tsne_status check_finite(const float* X, int64_t n, int32_t* dflag, int32_t* hflag, cudaStream_t s);
+tsne_status fill_ones(float* p, int64_t n, cudaStream_t s);
+
+}  // namespace tsne

@@ -1,0 +1,12 @@
+// knn_tc.cuh -- tcgen05 (5th-gen tensor core) candidate stage of the kNN.
+#pragma once
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace tsne {
+bool knn_tc_available();
+tsne_status launch_cand_tc(const __half* Xh, const float* nrm, int N, int Dp, int Kc,
+                           unsigned long long* buf, unsigned long long* cand, int slots,
+                           cudaStream_t s);
+}  // namespace tsne

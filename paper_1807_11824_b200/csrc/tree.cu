@@ -1,0 +1,354 @@
+// tree.cu -- quadtree build over the 2-D embedding (P:L136 steps 1-4).
+//
+//  k_bbox        step 1: exact min/max, root box (D8)         [H1]
+//  k_keys        fp64 quantisation -> 32-bit Morton key (D8)  [H2]
+//  radix sort    (key, point id) pairs                         [H2]
+//  k_gather      Y in Morton order + fixed-point coordinates
+//  scan          exclusive prefix sums (integers: exact, deterministic)
+//  k_karras      binary radix tree over the sorted keys        [H3]
+//  k_quad_rank   which binary nodes are quad cells; chain rank [H3]
+//  scan          quad-node count per start position -> pre-order index
+//  k_quad_emit   pre-order node records, counts, centres of mass [H3, H4]
+//
+// The compressed quadtree is derived from a Karras (2012) binary radix tree:
+// a binary node whose common prefix has length delta lies in the cell of
+// level L = min(delta, 32) / 2; it is a quad node iff its parent's level is
+// smaller (otherwise it merges into the parent).  Keys tie-break by index
+// (delta >= 32 -> identical keys -> a level-16 bucket).  DESIGN.md sec. 6.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "tree.cuh"
+
+namespace tsne {
+
+// ---------------------------------------------------------------- workspace
+struct LL2Sum {
+  __host__ __device__ __forceinline__ longlong2 operator()(const longlong2& a,
+                                                           const longlong2& b) const {
+    return make_longlong2(a.x + b.x, a.y + b.y);
+  }
+};
+
+size_t tree_cub_bytes(int64_t N, size_t* sort_b, size_t* scan_b, size_t* scan2_b) {
+  size_t a = 0, b = 0, c = 0;
+  cub::DoubleBuffer<uint32_t> dk(nullptr, nullptr);
+  cub::DoubleBuffer<int32_t> dv(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, a, dk, dv, (int)N, 0, 32);
+  cub::DeviceScan::ExclusiveScan(nullptr, b, (longlong2*)nullptr, (longlong2*)nullptr, LL2Sum(),
+                                 make_longlong2(0, 0), (int)(N + 1));
+  cub::DeviceScan::ExclusiveSum(nullptr, c, (int32_t*)nullptr, (int32_t*)nullptr, (int)(N + 1));
+  if (sort_b) *sort_b = a;
+  if (scan_b) *scan_b = b;
+  if (scan2_b) *scan2_b = c;
+  return a + b + c;
+}
+
+void carve_tree(Carver& c, TreeWS& w, int64_t N) {
+  w.N = N;
+  size_t sb, cb, c2b;
+  tree_cub_bytes(N, &sb, &cb, &c2b);
+  w.keys_a = c.take<uint32_t>(N);
+  w.keys_b = c.take<uint32_t>(N);
+  w.vals_a = c.take<int32_t>(N);
+  w.vals_b = c.take<int32_t>(N);
+  w.sort_tmp = c.take<char>(sb);
+  w.sort_tmp_bytes = sb;
+  w.ys = c.take<float2>(N);
+  w.fq = c.take<longlong2>(N + 1);
+  w.S = c.take<longlong2>(N + 1);
+  w.scan_tmp = c.take<char>(cb);
+  w.scan_tmp_bytes = cb;
+  w.bfirst = c.take<int32_t>(N);
+  w.blast = c.take<int32_t>(N);
+  w.bdelta = c.take<int32_t>(N);
+  w.bparent = c.take<int32_t>(N);
+  w.lparent = c.take<int32_t>(N);
+  w.rank = c.take<int32_t>(2 * N);
+  w.cnt = c.take<int32_t>(N + 1);
+  w.base = c.take<int32_t>(N + 1);
+  w.scan2_tmp = c.take<char>(c2b);
+  w.scan2_tmp_bytes = c2b;
+  w.nodes = c.take<float4>(2 * N);
+  w.nfirst = c.take<int32_t>(2 * N);
+  w.com64 = c.take<double2>(2 * N);
+  w.leafnode = c.take<int32_t>(N);
+  w.box = c.take<BoxInfo>(2);
+  w.rep = c.take<float2>(N);
+  w.zpart = c.take<double>(traverse_blocks(N));
+  w.Z = c.take<double>(2);
+  w.counter = c.take<unsigned>(8);
+  w.part4 = c.take<float4>(kMaxParts);
+  w.part2 = c.take<double2>(kMaxParts);
+}
+
+// ---------------------------------------------------------------- H1 bbox
+constexpr int kBoxThreads = 256;
+
+__global__ void __launch_bounds__(kBoxThreads) k_bbox(const float2* __restrict__ Y, int N,
+                                                      float4* part, unsigned* counter,
+                                                      BoxInfo* box) {
+  float mnx = INFINITY, mxx = -INFINITY, mny = INFINITY, mxy = -INFINITY;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    float2 y = Y[i];
+    mnx = fminf(mnx, y.x); mxx = fmaxf(mxx, y.x);
+    mny = fminf(mny, y.y); mxy = fmaxf(mxy, y.y);
+  }
+  mnx = warp_min(mnx); mxx = warp_max(mxx); mny = warp_min(mny); mxy = warp_max(mxy);
+  __shared__ float4 sw[kBoxThreads / 32];
+  __shared__ bool last;
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sw[wid] = make_float4(mnx, mxx, mny, mxy);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float4 r = sw[0];
+    for (int k = 1; k < kBoxThreads / 32; ++k) {
+      r.x = fminf(r.x, sw[k].x); r.y = fmaxf(r.y, sw[k].y);
+      r.z = fminf(r.z, sw[k].z); r.w = fmaxf(r.w, sw[k].w);
+    }
+    part[blockIdx.x] = r;
+    __threadfence();
+    unsigned t = atomicAdd(counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    float4 r = __ldcg(part);
+    for (int k = 1; k < (int)gridDim.x; ++k) {
+      float4 q = __ldcg(part + k);
+      r.x = fminf(r.x, q.x); r.y = fmaxf(r.y, q.y);
+      r.z = fminf(r.z, q.z); r.w = fmaxf(r.w, q.w);
+    }
+    BoxInfo b;
+    make_root_box(r.x, r.y, r.z, r.w, &b);
+    b.shift_x = 0.f;
+    b.shift_y = 0.f;
+    b.pad0 = 0.f;
+    *box = b;
+    *counter = 0u;
+  }
+}
+
+tsne_status launch_bbox(TreeWS& w, const float2* Y, cudaStream_t s) {
+  int blocks = (int)((w.N + 4 * kBoxThreads - 1) / (4 * kBoxThreads));
+  if (blocks > 2 * kNumSMs) blocks = 2 * kNumSMs;
+  if (blocks < 1) blocks = 1;
+  k_bbox<<<blocks, kBoxThreads, 0, s>>>(Y, (int)w.N, w.part4, w.counter + 0, w.box);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
+// ---------------------------------------------------------------- H2 keys
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+// q = min(2^16-1, max(0, floor((y - lo) * s))) in fp64 without contraction (D8)
+__device__ __forceinline__ uint32_t quantise(float y, double lo, double s) {
+  double f = floor(__dmul_rn(__dsub_rn((double)y, lo), s));
+  f = f < 0.0 ? 0.0 : f;
+  f = f > 65535.0 ? 65535.0 : f;
+  return (uint32_t)f;
+}
+
+__global__ void k_keys(float2* __restrict__ Y, int N, const BoxInfo* __restrict__ box,
+                       int apply_shift, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                       int32_t* __restrict__ cnt) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > N) return;
+  cnt[i] = 0;
+  if (i == N) return;
+  const BoxInfo b = *box;
+  float2 y = Y[i];
+  if (apply_shift) {
+    y.x = y.x - b.shift_x;
+    y.y = y.y - b.shift_y;
+    Y[i] = y;
+  }
+  uint32_t qx = quantise(y.x, b.lox, b.s);
+  uint32_t qy = quantise(y.y, b.loy, b.s);
+  keys[i] = (spread16(qx) << 1) | spread16(qy);   // quadrant digit = 2 bx + by
+  vals[i] = i;
+}
+
+// ---------------------------------------------------------------- gather
+__global__ void k_gather(const float2* __restrict__ Y, const int32_t* __restrict__ perm, int N,
+                         const BoxInfo* __restrict__ box, float2* __restrict__ ys,
+                         longlong2* __restrict__ fq) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > N) return;
+  if (k == N) { fq[N] = make_longlong2(0, 0); return; }
+  float2 y = Y[perm[k]];
+  ys[k] = y;
+  const double cx = box->cx, cy = box->cy, inv = kFixScale / box->r0;
+  long long qx = __double2ll_rn(__dmul_rn(__dsub_rn((double)y.x, cx), inv));
+  long long qy = __double2ll_rn(__dmul_rn(__dsub_rn((double)y.y, cy), inv));
+  fq[k] = make_longlong2(qx, qy);
+}
+
+// ---------------------------------------------------------------- H3 Karras
+__device__ __forceinline__ int kdelta(const uint32_t* __restrict__ k, int N, int a, int b) {
+  if (b < 0 || b >= N) return -1;
+  uint32_t ka = k[a], kb = k[b];
+  if (ka != kb) return __clz(ka ^ kb);
+  return 32 + __clz((uint32_t)a ^ (uint32_t)b);
+}
+
+__global__ void k_karras(const uint32_t* __restrict__ keys, int N, int32_t* __restrict__ bfirst,
+                         int32_t* __restrict__ blast, int32_t* __restrict__ bdelta,
+                         int32_t* __restrict__ bparent, int32_t* __restrict__ lparent) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N - 1) return;
+  int d = (kdelta(keys, N, i, i + 1) - kdelta(keys, N, i, i - 1)) >= 0 ? 1 : -1;
+  int dmin = kdelta(keys, N, i, i - d);
+  int lmax = 2;
+  while (kdelta(keys, N, i, i + lmax * d) > dmin) lmax <<= 1;
+  int l = 0;
+  for (int t = lmax >> 1; t >= 1; t >>= 1)
+    if (kdelta(keys, N, i, i + (l + t) * d) > dmin) l += t;
+  int j = i + l * d;
+  int dnode = kdelta(keys, N, i, j);
+  int s = 0, t = l;
+  do {
+    t = (t + 1) >> 1;
+    if (kdelta(keys, N, i, i + (s + t) * d) > dnode) s += t;
+  } while (t > 1);
+  int gamma = i + s * d + (d < 0 ? -1 : 0);
+  int lo = min(i, j), hi = max(i, j);
+  bfirst[i] = lo;
+  blast[i] = hi;
+  bdelta[i] = dnode;
+  if (lo == gamma) lparent[gamma] = i; else bparent[gamma] = i;
+  if (hi == gamma + 1) lparent[gamma + 1] = i; else bparent[gamma + 1] = i;
+  if (i == 0) bparent[0] = -1;
+}
+
+__device__ __forceinline__ int qlevel(int delta) { return (delta < 32 ? delta : 32) >> 1; }
+
+// binary node ids: [0, N-1) internal, [N-1, 2N-1) leaves (sorted position id-(N-1))
+__device__ __forceinline__ bool internal_is_quad(const int32_t* bdelta, const int32_t* bparent,
+                                                 int a) {
+  int p = bparent[a];
+  return p < 0 || qlevel(bdelta[p]) < qlevel(bdelta[a]);
+}
+
+__global__ void k_quad_rank(int N, const int32_t* __restrict__ bfirst,
+                            const int32_t* __restrict__ bdelta, const int32_t* __restrict__ bparent,
+                            const int32_t* __restrict__ lparent, int32_t* __restrict__ rank,
+                            int32_t* __restrict__ cnt) {
+  int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= 2 * N - 1) return;
+  int s, p;
+  bool quad, deepest;
+  if (id < N - 1) {
+    s = bfirst[id];
+    p = bparent[id];
+    quad = internal_is_quad(bdelta, bparent, id);
+    deepest = bdelta[id] >= 32;                       // bucket top
+  } else {
+    int k = id - (N - 1);
+    s = k;
+    p = lparent[k];
+    quad = qlevel(bdelta[p]) < 16;                    // not inside a bucket
+    deepest = true;
+  }
+  if (!quad) { rank[id] = -1; return; }
+  int r = 0;
+  for (int a = p; a >= 0 && bfirst[a] == s; a = bparent[a])
+    if (internal_is_quad(bdelta, bparent, a)) ++r;
+  rank[id] = r;
+  if (deepest) cnt[s] = r + 1;
+}
+
+__global__ void k_quad_emit(int N, const int32_t* __restrict__ bfirst,
+                            const int32_t* __restrict__ blast, const int32_t* __restrict__ bdelta,
+                            const int32_t* __restrict__ bparent, const int32_t* __restrict__ rank,
+                            const int32_t* __restrict__ base, const float2* __restrict__ ys,
+                            const longlong2* __restrict__ S, const BoxInfo* __restrict__ box,
+                            float4* __restrict__ nodes, int32_t* __restrict__ nfirst,
+                            double2* __restrict__ com64, int32_t* __restrict__ leafnode) {
+  int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= 2 * N - 1) return;
+  int r = rank[id];
+  if (r < 0) return;
+  int s, e, level;
+  if (id < N - 1) {
+    s = bfirst[id];
+    e = blast[id];
+    int dl = bdelta[id];
+    if (dl < 32) {
+      level = qlevel(dl);
+    } else {                                          // bucket top
+      int p = bparent[id];
+      level = (p < 0 || bdelta[p] <= 29) ? kLevelBucketTest : kLevelLeaf;
+    }
+  } else {
+    s = e = id - (N - 1);
+    level = kLevelLeaf;
+  }
+  int pre = base[s] + r;
+  int skip = base[e + 1];
+  uint32_t count = (uint32_t)(e - s + 1);
+  float cxf, cyf;
+  double2 c64;
+  if (count == 1) {
+    float2 y = ys[s];
+    cxf = y.x; cyf = y.y;
+    c64 = make_double2((double)y.x, (double)y.y);
+    leafnode[s] = pre;
+  } else {
+    longlong2 a = S[e + 1], b = S[s];
+    const double sc = __ddiv_rn(box->r0, kFixScale);
+    double mx = __ddiv_rn(__dmul_rn((double)(a.x - b.x), sc), (double)count);
+    double my = __ddiv_rn(__dmul_rn((double)(a.y - b.y), sc), (double)count);
+    c64 = make_double2(__dadd_rn(box->cx, mx), __dadd_rn(box->cy, my));
+    cxf = (float)c64.x; cyf = (float)c64.y;
+    if (level >= kLevelLeaf)
+      for (int k = s; k <= e; ++k) leafnode[k] = pre;
+  }
+  nodes[pre] = make_float4(cxf, cyf, __uint_as_float(count | ((uint32_t)level << 27)),
+                           __int_as_float(skip));
+  nfirst[pre] = s;
+  com64[pre] = c64;
+}
+
+// ---------------------------------------------------------------- host
+static inline int cdiv(int64_t a, int b) { return (int)((a + b - 1) / b); }
+
+tsne_status build_tree(TreeWS& w, float2* Y, bool apply_shift, cudaStream_t s) {
+  const int N = (int)w.N;
+  const int T = 256;
+  k_keys<<<cdiv(N + 1, T), T, 0, s>>>(Y, N, w.box, apply_shift ? 1 : 0, w.keys_a, w.vals_a, w.cnt);
+  TSNE_LAUNCH_CHECK();
+  cub::DoubleBuffer<uint32_t> dk(w.keys_a, w.keys_b);
+  cub::DoubleBuffer<int32_t> dv(w.vals_a, w.vals_b);
+  size_t sb = w.sort_tmp_bytes;
+  TSNE_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, sb, dk, dv, N, 0, 32, s));
+  w.keys_sorted = dk.Current();
+  w.perm = dv.Current();
+  k_gather<<<cdiv(N + 1, T), T, 0, s>>>(Y, w.perm, N, w.box, w.ys, w.fq);
+  TSNE_LAUNCH_CHECK();
+  size_t cb = w.scan_tmp_bytes;
+  TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveScan(w.scan_tmp, cb, w.fq, w.S, LL2Sum(),
+                                               make_longlong2(0, 0), N + 1, s));
+  k_karras<<<cdiv(N - 1, T), T, 0, s>>>(w.keys_sorted, N, w.bfirst, w.blast, w.bdelta, w.bparent,
+                                         w.lparent);
+  TSNE_LAUNCH_CHECK();
+  k_quad_rank<<<cdiv(2 * N - 1, T), T, 0, s>>>(N, w.bfirst, w.bdelta, w.bparent, w.lparent,
+                                                w.rank, w.cnt);
+  TSNE_LAUNCH_CHECK();
+  size_t c2 = w.scan2_tmp_bytes;
+  TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.scan2_tmp, c2, w.cnt, w.base, N + 1, s));
+  k_quad_emit<<<cdiv(2 * N - 1, T), T, 0, s>>>(N, w.bfirst, w.blast, w.bdelta, w.bparent, w.rank,
+                                                w.base, w.ys, w.S, w.box, w.nodes, w.nfirst,
+                                                w.com64, w.leafnode);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
+}  // namespace tsne

@@ -1,0 +1,138 @@
+// tree.cuh -- the quadtree of Sec. III-C as built on the GPU:
+// bounding box (step 1), Morton keys + radix sort (step 4, "sort points by
+// spatial distance"), compressed quadtree from the sorted keys (steps 2-3:
+// "insert", "number of points in each internal cell"), centres of mass.
+//
+// Node layout: one pre-order array of 16-byte hot
+// records {com_x, com_y, count | level << 27, skip}; the first child of
+// node k is k + 1 and `skip` is the first node after k's subtree, so a
+// traversal needs no stack.  Cold arrays: range start (`nfirst`, used by
+// bucket leaves) and the fp64 centre of mass (`com64`, read only inside the
+// fp64 decision band, D25).
+//
+// level field: 0..15  internal cell whose point set branches at that level
+//                     (single-child chains are compressed away, D9)
+//              16     leaf evaluated exactly (one point, or a level-16 bucket
+//                     directly below a level-15 branching cell)
+//              17     bucket whose chain reaches level <= 15: the criterion
+//                     is tested with r_15; accept -> summary, else exact pairs
+#pragma once
+#include "common.cuh"
+
+namespace tsne {
+
+struct BoxInfo {
+  float minx, maxx, miny, maxy;  // bounding box of the (shifted) embedding
+  float shift_x, shift_y;        // fp32 mean subtracted from Y before use (recentring, D15)
+  float mabs;                    // max |coordinate| (shifted), bounds fp32 error (D25)
+  float pad0;
+  double cx, cy, r0, lox, loy, s;  // root box (D8), fp64
+};
+
+constexpr int kLevelLeaf = 16;
+constexpr int kLevelBucketTest = 17;
+constexpr uint32_t kCountMask = (1u << 27) - 1u;
+constexpr int kMaxParts = 4096;
+constexpr double kFixScale = 274877906944.0;  // 2^38: fixed-point COM sums
+
+struct TreeWS {
+  int64_t N = 0;
+  uint32_t *keys_a = nullptr, *keys_b = nullptr;
+  int32_t *vals_a = nullptr, *vals_b = nullptr;
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  float2* ys = nullptr;        // Y in Morton order
+  longlong2* fq = nullptr;     // fixed-point coordinates (N+1)
+  longlong2* S = nullptr;      // exclusive prefix sums of fq (N+1)
+  void* scan_tmp = nullptr;
+  size_t scan_tmp_bytes = 0;
+  int32_t *bfirst = nullptr, *blast = nullptr, *bdelta = nullptr;
+  int32_t *bparent = nullptr, *lparent = nullptr;
+  int32_t* rank = nullptr;     // 2N-1 binary nodes
+  int32_t* cnt = nullptr;      // N+1
+  int32_t* base = nullptr;     // N+1
+  void* scan2_tmp = nullptr;
+  size_t scan2_tmp_bytes = 0;
+  float4* nodes = nullptr;     // <= 2N-1 quad nodes
+  int32_t* nfirst = nullptr;
+  double2* com64 = nullptr;
+  int32_t* leafnode = nullptr; // N, indexed by sorted position
+  BoxInfo* box = nullptr;
+  float2* rep = nullptr;       // N repulsive numerators f_i (original order)
+  double* zpart = nullptr;     // per traversal block
+  double* Z = nullptr;         // [0] = Z, [1] = 1/Z
+  unsigned* counter = nullptr; // last-block-done counters (zeroed once)
+  float4* part4 = nullptr;     // per-block min/max partials (kMaxParts)
+  double2* part2 = nullptr;    // per-block fp64 sum partials (kMaxParts)
+  // set by build(): which double-buffer half holds the sorted result
+  uint32_t* keys_sorted = nullptr;
+  int32_t* perm = nullptr;
+};
+
+// Carve (or size) the tree workspace for N points.
+void carve_tree(Carver& c, TreeWS& w, int64_t N);
+size_t tree_cub_bytes(int64_t N, size_t* sort_b, size_t* scan_b, size_t* scan2_b);
+
+// Bounding box + root box of Y (shift = 0), written to w.box.
+tsne_status launch_bbox(TreeWS& w, const float2* Y, cudaStream_t s);
+// Steps 2-4 from w.box: keys (after subtracting box->shift from Y in place
+// when `apply_shift`), sort, build, summarise.
+tsne_status build_tree(TreeWS& w, float2* Y, bool apply_shift, cudaStream_t s);
+// Repulsive pass: w.rep, w.Z
+tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s);
+
+int traverse_blocks(int64_t N);
+
+__host__ __device__ inline void make_root_box(float minx, float maxx, float miny, float maxy,
+                                              BoxInfo* b);
+
+}  // namespace tsne
+
+// ---- implementation of the root box (identical arithmetic to DESIGN D8) ----
+namespace tsne {
+__host__ __device__ inline double dadd(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+__host__ __device__ inline double dsub(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dsub_rn(a, b);
+#else
+  return a - b;
+#endif
+}
+__host__ __device__ inline double dmul(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+__host__ __device__ inline double ddiv(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __ddiv_rn(a, b);
+#else
+  return a / b;
+#endif
+}
+
+__host__ __device__ inline void make_root_box(float minx, float maxx, float miny, float maxy,
+                                              BoxInfo* b) {
+  b->minx = minx; b->maxx = maxx; b->miny = miny; b->maxy = maxy;
+  double cx = ddiv(dadd((double)minx, (double)maxx), 2.0);
+  double cy = ddiv(dadd((double)miny, (double)maxy), 2.0);
+  double sx = dsub((double)maxx, (double)minx);
+  double sy = dsub((double)maxy, (double)miny);
+  double span = sx > sy ? sx : sy;
+  double r0 = (span == 0.0) ? 1.0 : dmul(ddiv(span, 2.0), 1.0 + 9.5367431640625e-07 /*2^-20*/);
+  b->cx = cx; b->cy = cy; b->r0 = r0;
+  b->lox = dsub(cx, r0);
+  b->loy = dsub(cy, r0);
+  b->s = ddiv(65536.0, dmul(2.0, r0));
+  float m = fmaxf(fmaxf(fabsf(minx), fabsf(maxx)), fmaxf(fabsf(miny), fabsf(maxy)));
+  b->mabs = m;
+}
+}  // namespace tsne

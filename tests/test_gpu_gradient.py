@@ -1,0 +1,133 @@
+"""GPU <-> oracle parity of the gradient step (H1-H7) through the C ABI.
+
+Bar (north star): relative L2 of dY <= 1e-4 against the
+oracle's BH gradient at theta = 0.5 (same tree definition D7-D11, decisions
+as in fp64, D25), <= 1e-5 against the exact O(N^2) gradient at theta = 0.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    import paper_1807_11824_b200 as T
+    assert torch.cuda.is_available()
+    T.lib()
+    return T
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+def gpu_grad(T, rp, col, v32, Y, theta, exag=1.0):
+    dev = torch.device("cuda")
+    dY, Z = T.gradient(torch.as_tensor(rp, device=dev), torch.as_tensor(col, device=dev),
+                       torch.as_tensor(v32, device=dev), torch.as_tensor(Y, device=dev), theta,
+                       exag)
+    return dY.cpu().numpy(), Z
+
+
+@pytest.mark.parametrize("N", [2, 3, 37, 500])
+def test_theta0_vs_exact(T, orc, N):
+    rp, col, v32, v64 = synth.random_csr(N, min(8, N - 1), seed=N)
+    Y = synth.fixed_y("gauss10", N, seed=1)
+    for exag in (1.0, 12.0):
+        g, Z = gpu_grad(T, rp, col, v32, Y, 0.0, exag)
+        ge, Ze = orc.gradient_exact(rp, col, v32.astype(np.float64), Y.astype(np.float64), exag)
+        assert abs(Z - Ze) <= 1e-6 * Ze
+        # scale: the gradient, or its attractive term when they cancel (N = 2: p = q, g = 0)
+        scale = max(np.linalg.norm(ge), np.linalg.norm(4 * exag * orc.attractive(rp, col, v32, Y)))
+        assert np.linalg.norm(g - ge) <= 1e-5 * scale
+
+
+@pytest.mark.parametrize("kind", ["gauss10", "clustered", "blobs"])
+@pytest.mark.parametrize("N", [1000, 4099, 20000])
+def test_theta05_vs_oracle_bh(T, orc, kind, N):
+    rp, col, v32, _ = synth.random_csr(N, 10, seed=7)
+    Y = synth.fixed_y(kind, N, seed=3)
+    g, Z = gpu_grad(T, rp, col, v32, Y, 0.5, 12.0)
+    go, Zo = orc.gradient_bh(rp, col, v32, Y, 0.5, 12.0)
+    assert abs(Z - Zo) <= 1e-6 * Zo
+    assert rel(g, go) <= 1e-4
+
+
+@pytest.mark.parametrize("theta", [0.25, 0.8, 1.5])
+def test_other_thetas(T, orc, theta):
+    N = 6000
+    rp, col, v32, _ = synth.random_csr(N, 10, seed=8)
+    Y = synth.fixed_y("blobs", N, seed=4)
+    g, Z = gpu_grad(T, rp, col, v32, Y, theta)
+    go, Zo = orc.gradient_bh(rp, col, v32, Y, theta)
+    assert abs(Z - Zo) <= 1e-6 * Zo
+    assert rel(g, go) <= 1e-4
+
+
+def test_duplicates_and_buckets(T, orc):
+    # coincident points -> level-16 buckets (tested and exact), D9
+    N = 3000
+    Y = np.round(synth.fixed_y("gauss10", N, seed=5) / 2.0).astype(np.float32) * 2.0
+    Y[:50] = Y[0]                       # one large bucket
+    rp, col, v32, _ = synth.random_csr(N, 6, seed=9)
+    for theta in (0.0, 0.5):
+        g, Z = gpu_grad(T, rp, col, v32, Y, theta)
+        go, Zo = orc.gradient_bh(rp, col, v32, Y, theta)
+        assert abs(Z - Zo) <= 1e-6 * Zo
+        assert rel(g, go) <= 1e-4
+
+
+def test_all_points_identical(T, orc):
+    N = 64
+    Y = np.ones((N, 2), np.float32)
+    rp, col, v32, _ = synth.random_csr(N, 4, seed=1)
+    g, Z = gpu_grad(T, rp, col, v32, Y, 0.5)
+    assert Z == N * (N - 1)            # every pair has w = 1
+    assert np.abs(g).max() == 0.0
+
+
+def test_five_point_example(T, orc):
+    import json, os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                       "five_point_theta05.json")))
+    Y = np.array(gold["points"], np.float32)
+    rp = np.zeros(6, np.int64)             # P = 0: dY = -4 f / Z
+    col = np.zeros(0, np.int32)
+    val = np.zeros(0, np.float32)
+    dev = torch.device("cuda")
+    dY, Z = T.gradient(torch.as_tensor(rp, device=dev), torch.zeros(1, dtype=torch.int32, device=dev),
+                       torch.zeros(1, dtype=torch.float32, device=dev), torch.as_tensor(Y, device=dev),
+                       0.5, 1.0)
+    _, zo, Zo, _ = orc.repulsive_bh(Y, 0.5)
+    assert abs(Z - Zo) <= 1e-6 * Zo
+    f0 = -dY[0].cpu().numpy() * Z / 4.0
+    np.testing.assert_allclose(f0, gold["bh"]["f0"], rtol=1e-5)
+
+
+def test_translation_and_determinism(T, orc):
+    N = 5000
+    rp, col, v32, _ = synth.random_csr(N, 10, seed=2)
+    Y = synth.fixed_y("clustered", N, seed=6)
+    g1, Z1 = gpu_grad(T, rp, col, v32, Y, 0.5)
+    g2, Z2 = gpu_grad(T, rp, col, v32, Y, 0.5)
+    assert np.array_equal(g1, g2) and Z1 == Z2          # bitwise deterministic
+    g3, _ = gpu_grad(T, rp, col, v32, Y + np.float32(64.0), 0.5)
+    assert rel(g3, g1.astype(np.float64)) < 1e-3
+
+
+def test_real_p_from_oracle(T, orc):
+    # P built by the oracle from C1 data (fp32-rounded), Y at a mid-run state
+    X = synth.make_x("C1").numpy()
+    idx, d2 = orc.knn(X, 90)
+    rp, col, v64, v32, *_ = orc.compute_p(idx, d2, 30.0)
+    Y = orc.init_y(1000, 42)
+    Y, v, gn = orc.optimize(rp, col, v32, Y, n_iter=300, theta=0.5)
+    Y = Y.astype(np.float32)
+    for theta in (0.0, 0.5):
+        g, Z = gpu_grad(T, rp, col, v32, Y, theta, 1.0)
+        go, Zo = orc.gradient_bh(rp, col, v32, Y, theta, 1.0)
+        assert rel(g, go) <= (1e-5 if theta == 0 else 1e-4)

@@ -1,0 +1,128 @@
+"""GPU <-> oracle parity of the optimisation loop (H1-H8) and of the full
+pipeline (Algorithm 1) through the C ABI.
+
+Short runs are compared pointwise; long runs are chaotic, so
+they are compared statistically: final KL within 1% and 10-NN preservation
+within 1 percentage point, as means over 5 Y0 seeds (north star).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    import paper_1807_11824_b200 as T
+    T.lib()
+    return T
+
+
+@pytest.fixture(scope="module")
+def c1(orc):
+    X, lab = synth.make_x("C1", return_labels=True)
+    X = X.numpy()
+    idx, d2 = orc.knn(X, 90)
+    rp, col, v64, v32, *_ = orc.compute_p(idx, d2, 30.0)
+    return X, lab.numpy(), idx, rp, col, v32
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+def dev(a):
+    return torch.as_tensor(a, device="cuda")
+
+
+def test_init_y_matches_philox_recipe(T, orc):
+    Yg = T.init_y(5000, 42).cpu().numpy()
+    Yo = orc.init_y(5000, 42)
+    np.testing.assert_allclose(Yg, Yo, rtol=2e-6, atol=1e-12)
+
+
+def test_first_step_pointwise(T, orc, c1):
+    X, lab, idx, rp, col, v32 = c1
+    Y0 = orc.init_y(1000, 42).astype(np.float32)
+    opt = T.Optimizer(dev(rp), dev(col), dev(v32), dev(Y0), theta=0.5)
+    Yg = opt.step(1).cpu().numpy()
+    Yo, _, _ = orc.optimize(rp, col, v32, Y0.astype(np.float64), n_iter=1, theta=0.5)
+    assert rel(Yg, Yo) <= 1e-5
+
+
+@pytest.mark.parametrize("t0", [0, 240, 600])
+def test_every_step_matches_oracle_step(T, orc, c1, t0):
+    # The trajectory itself is chaotic (fp32 vs fp64 differences grow ~3x per
+    # iteration in the exaggeration phase), so each GPU iteration is checked
+    # against one oracle iteration started from the GPU's own state.
+    X, lab, idx, rp, col, v32 = c1
+    opt = T.Optimizer(dev(rp), dev(col), dev(v32), T.init_y(1000, 42), theta=0.5)
+    if t0:
+        opt.step(t0)
+    for t in range(t0, t0 + 15):
+        S = opt.state
+        Y, v, g = (S.Y.cpu().numpy().astype(np.float64), S.v.cpu().numpy().astype(np.float64),
+                   S.gains.cpu().numpy().astype(np.float64))
+        Yo, vo, go = orc.optimize(rp, col, v32, Y, v, g, t0=t, n_iter=1, theta=0.5)
+        opt.step(1)
+        assert rel(opt.state.Y.cpu().numpy(), Yo) <= 1e-5, t
+        assert rel(opt.state.v.cpu().numpy(), vo) <= 1e-4, t
+        assert np.array_equal(opt.state.gains.cpu().numpy() > 0.5, go > 0.5)
+
+
+def test_graph_and_eager_agree(T, c1):
+    X, lab, idx, rp, col, v32 = c1
+    Y0 = T.init_y(1000, 7)
+    a = T.Optimizer(dev(rp), dev(col), dev(v32), Y0, use_graphs=True)
+    b = T.Optimizer(dev(rp), dev(col), dev(v32), Y0, use_graphs=False)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ya = a.step(300).clone()
+    s.synchronize()
+    yb = b.step(300)
+    assert torch.equal(ya, yb)                       # same kernels, same order: bitwise
+
+
+def test_long_run_statistics_c1(T, orc, c1):
+    X, lab, idx, rp, col, v32 = c1
+    kl_g, kl_o, nn_g, nn_o = [], [], [], []
+    for seed in range(42, 47):
+        Y0 = orc.init_y(1000, seed).astype(np.float32)
+        opt = T.Optimizer(dev(rp), dev(col), dev(v32), dev(Y0), theta=0.5)
+        Yg = opt.step(1000).cpu().numpy().astype(np.float64)
+        Yo, _, _ = orc.optimize(rp, col, v32, Y0.astype(np.float64), n_iter=1000, theta=0.5)
+        kl_g.append(orc.kl(rp, col, v32, Yg)); kl_o.append(orc.kl(rp, col, v32, Yo))
+        nn_g.append(orc.nn_preservation(idx, Yg, 10)); nn_o.append(orc.nn_preservation(idx, Yo, 10))
+    assert abs(np.mean(kl_g) - np.mean(kl_o)) <= 0.01 * np.mean(kl_o)
+    assert abs(np.mean(nn_g) - np.mean(nn_o)) <= 0.01
+
+
+def test_run_end_to_end_host_buffers(T, orc, c1):
+    X, lab, idx, rp, col, v32 = c1
+    Xh = torch.as_tensor(X).pin_memory()
+    kl_g, nn_g = [], []
+    for seed in range(42, 45):
+        Y, info = T.run(Xh, perplexity=30.0, theta=0.5, n_iter=1000, seed=seed)
+        assert not Y.is_cuda and info["K"] == 90 and info["knn_rows_uncertified"] == 0
+        Yg = Y.numpy().astype(np.float64)
+        assert np.isfinite(Yg).all()
+        kl_g.append(orc.kl(rp, col, v32, Yg))
+        nn_g.append(orc.nn_preservation(idx, Yg, 10))
+    kl_o, nn_o = [], []
+    for seed in range(42, 45):
+        Yo, klo, _ = orc.run(X, perplexity=30.0, theta=0.5, n_iter=1000, seed=seed)
+        kl_o.append(klo)
+        nn_o.append(orc.nn_preservation(idx, Yo, 10))
+    assert abs(np.mean(kl_g) - np.mean(kl_o)) <= 0.01 * np.mean(kl_o)
+    assert abs(np.mean(nn_g) - np.mean(nn_o)) <= 0.01
+
+
+def test_nonfinite_sentinel(T, c1):
+    X, lab, idx, rp, col, v32 = c1
+    opt = T.Optimizer(dev(rp), dev(col), dev(v32), T.init_y(1000, 1), learning_rate=1e38)
+    with pytest.raises(T.TsneError, match="NONFINITE"):
+        opt.step(5)
