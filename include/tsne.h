@@ -122,7 +122,9 @@ tsne_status tsne_compute_p(const int32_t* idx, const double* d2, int64_t N, int3
  * y_cell = centre of mass, strict r^2 < theta^2 D^2, a cell containing i is
  * always opened), decided as in fp64 (D25).
  *
- *   row_ptr/col/val  CSR of P as produced by tsne_compute_p.
+ *   row_ptr/col/val  CSR of P as produced by tsne_compute_p; col and val
+ *             must be 16-byte aligned (they are streamed as 16-byte vectors),
+ *             Y and dY 8-byte aligned, else TSNE_ERR_ARG.
  *   Y     [N x 2] float32 (x,y interleaved), finite.
  *   dY    [N x 2] float32 out.
  *   Z_out HOST out (nullable): Z; when non-NULL the call synchronises.
@@ -167,6 +169,21 @@ tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const floa
                           int32_t n_iter, float theta, float learning_rate,
                           float exaggeration, const tsne_config* cfg, void* ws,
                           size_t ws_bytes, tsne_stream_t stream);
+
+/* Diagnostics for measurement (bench.py): runs `reps` eager iterations from
+ * the optimiser state exactly like tsne_optimize (advancing it from t0) and
+ * reports the mean CUDA-event time of each stage on `stream`:
+ *   stage_ms[0] tree build (H1-H4), stage_ms[1] traversal (H5-H6),
+ *   stage_ms[2] attractive pass fused with the update (H7-H8).
+ * kernels_per_iter (HOST out, nullable): number of kernel launches one
+ * iteration makes (counted from a captured graph of one iteration).
+ * stage_ms (HOST out, 3 doubles).  Synchronises stream. */
+tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
+                                    int64_t N, float* Y, float* v, float* gains, int32_t t0,
+                                    int32_t reps, float theta, float learning_rate,
+                                    float exaggeration, const tsne_config* cfg, double* stage_ms,
+                                    int32_t* kernels_per_iter, void* ws, size_t ws_bytes,
+                                    tsne_stream_t stream);
 
 /* Y0 = 1e-4 N(0,1) from Philox4x32-10 (key = seed, counter = (i,0,0,0)),
  * Box-Muller on the first two words (D14).  Y [N x 2] float32 out. */

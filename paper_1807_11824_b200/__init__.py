@@ -50,7 +50,7 @@ EXPORTS = ["tsne_last_error", "tsne_abi_version", "tsne_config_default",
            "tsne_knn_workspace_size", "tsne_knn", "tsne_compute_p_workspace_size",
            "tsne_compute_p", "tsne_gradient_workspace_size", "tsne_gradient",
            "tsne_optimize_workspace_size", "tsne_optimize", "tsne_init_y", "tsne_run",
-           "tsne_run_ex"]
+           "tsne_run_ex", "tsne_profile_iterations"]
 
 
 def lib():
@@ -81,11 +81,14 @@ def lib():
     L.tsne_optimize.argtypes = [vp, vp, vp, i64, vp, vp, vp, i32, i32, f32, f32, f32,
                                 C.POINTER(Config), vp, sz, vp]
     L.tsne_init_y.argtypes = [i64, C.c_uint64, vp, vp]
+    L.tsne_profile_iterations.argtypes = [vp, vp, vp, i64, vp, vp, vp, i32, i32, f32, f32, f32,
+                                          C.POINTER(Config), C.POINTER(C.c_double),
+                                          C.POINTER(i32), vp, sz, vp]
     L.tsne_run.argtypes = [vp, i64, i32, f32, f32, f32, i32, f32, vp]
     L.tsne_run_ex.argtypes = [vp, i64, i32, f32, f32, f32, i32, f32, C.POINTER(Config), vp,
                               C.POINTER(RunInfo)]
     for name in ["tsne_knn", "tsne_compute_p", "tsne_gradient", "tsne_optimize", "tsne_init_y",
-                 "tsne_run", "tsne_run_ex"]:
+                 "tsne_run", "tsne_run_ex", "tsne_profile_iterations"]:
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -215,6 +218,23 @@ class Optimizer:
                                    _ptr(self.ws), self.ws.numel(), st), "tsne_optimize")
         s.t += int(n_iter)
         return s.Y
+
+
+def profile_iteration(opt: Optimizer, reps: int = 5, stream=None) -> dict:
+    """Per-stage mean CUDA-event times of `reps` eager iterations (advances the
+    optimiser state like Optimizer.step)."""
+    s = opt.state
+    ms = (C.c_double * 3)()
+    kern = C.c_int32()
+    st = C.c_void_p(stream) if stream is not None else _stream()
+    _check(lib().tsne_profile_iterations(_ptr(opt.row_ptr), _ptr(opt.col), _ptr(opt.val), opt.N,
+                                         _ptr(s.Y), _ptr(s.v), _ptr(s.gains), s.t, int(reps),
+                                         opt.theta, opt.lr, opt.exag, C.byref(opt.cfg), ms,
+                                         C.byref(kern), _ptr(opt.ws), opt.ws.numel(), st),
+           "tsne_profile_iterations")
+    s.t += int(reps)
+    return {"tree_ms": ms[0], "traverse_ms": ms[1], "attract_update_ms": ms[2],
+            "kernels_per_iteration": kern.value}
 
 
 def init_y(N: int, seed: int = 42, device="cuda") -> torch.Tensor:

@@ -129,7 +129,8 @@ tsne_status tsne_gradient(const int64_t* row_ptr, const int32_t* col, const floa
   TSNE_ARG_CHECK(row_ptr && col && val && Y && dY, "null pointer argument");
   TSNE_ARG_CHECK(theta >= 0.f && std::isfinite(theta), "theta must be >= 0 (got %g)", theta);
   TSNE_ARG_CHECK(exaggeration > 0.f && std::isfinite(exaggeration), "exaggeration must be > 0");
-  TSNE_ARG_CHECK(aligned(Y, 8) && aligned(dY, 8), "Y and dY must be 8-byte aligned");
+  TSNE_ARG_CHECK(aligned(Y, 8) && aligned(dY, 8) && aligned(col, 16) && aligned(val, 16),
+                 "Y, dY need 8-byte and col, val 16-byte alignment");
   GradPlan p;
   size_t need = grad_plan(nullptr, N, p);
   if (!ws || ws_bytes < need) {
@@ -179,7 +180,9 @@ tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const floa
   TSNE_ARG_CHECK(learning_rate > 0.f, "learning_rate must be > 0");
   TSNE_ARG_CHECK(exaggeration > 0.f, "exaggeration must be > 0");
   TSNE_ARG_CHECK(n_iter >= 0 && t0 >= 0, "n_iter and t0 must be >= 0");
-  TSNE_ARG_CHECK(aligned(Y, 8) && aligned(v, 8) && aligned(gains, 8), "8-byte alignment needed");
+  TSNE_ARG_CHECK(aligned(Y, 8) && aligned(v, 8) && aligned(gains, 8) && aligned(col, 16) &&
+                     aligned(val, 16),
+                 "Y, v, gains need 8-byte and col, val 16-byte alignment");
   OptPlan p;
   size_t need = opt_plan(nullptr, N, p);
   if (!ws || ws_bytes < need) {
@@ -211,6 +214,39 @@ tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const floa
     set_error("non-finite embedding during iterations [%d, %d)", t0, t0 + n_iter);
     return TSNE_ERR_NONFINITE;
   }
+  return st;
+}
+
+tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
+                                    int64_t N, float* Y, float* v, float* gains, int32_t t0,
+                                    int32_t reps, float theta, float learning_rate,
+                                    float exaggeration, const tsne_config* cfg_in,
+                                    double* stage_ms, int32_t* kernels_per_iter, void* ws,
+                                    size_t ws_bytes, tsne_stream_t stream) {
+  clear_error();
+  tsne_config cfg;
+  tsne_config_default(&cfg);
+  if (cfg_in) cfg = *cfg_in;
+  TSNE_ARG_CHECK(N >= 2 && N < (int64_t(1) << 27), "N must be in [2, 2^27)");
+  TSNE_ARG_CHECK(row_ptr && col && val && Y && v && gains && stage_ms, "null pointer argument");
+  TSNE_ARG_CHECK(reps >= 1 && t0 >= 0, "reps must be >= 1");
+  OptPlan p;
+  size_t need = opt_plan(nullptr, N, p);
+  if (!ws || ws_bytes < need) {
+    set_error("workspace too small: need %zu bytes, got %zu", need, ws_bytes);
+    return TSNE_ERR_WORKSPACE;
+  }
+  tsne_status st = check_device();
+  if (st != TSNE_OK) return st;
+  opt_plan(ws, N, p);
+  SideStream ss;
+  cudaStream_t s = ss.get((cudaStream_t)stream);
+  if ((st = init_tree_ws(p.tree, s)) != TSNE_OK) { ss.join(); return st; }
+  Sched sc{cfg.exag_iters, exaggeration, cfg.mom0, cfg.mom1, learning_rate, cfg.min_gain};
+  st = profile_iterations(row_ptr, col, val, N, reinterpret_cast<float2*>(Y),
+                          reinterpret_cast<float2*>(v), reinterpret_cast<float2*>(gains), t0, reps,
+                          theta, sc, p.tree, p.opt, stage_ms, kernels_per_iter, s);
+  ss.join();
   return st;
 }
 

@@ -18,23 +18,50 @@ namespace tsne {
 
 constexpr int kAttrThreads = 256;
 constexpr int kAttrWarps = kAttrThreads / 32;
+constexpr int kAttrBlocksPerSM = 4;
 
-__device__ __forceinline__ float2 row_attractive(const int64_t* __restrict__ row_ptr,
+// One warp per row.  The row's nonzeros are read as 16-byte vectors from the
+// 16-byte-aligned window around [e0, e1) (lanes masked outside the row), so
+// each lane has 4 independent y_j gathers in flight per vector; the row sum is
+// reduced with a fixed butterfly (deterministic).
+__device__ __forceinline__ float2 row_attractive(const int64_t e0, const int64_t e1,
+                                                 const int64_t nnz,
                                                  const int32_t* __restrict__ col,
                                                  const float* __restrict__ val,
                                                  const float2* __restrict__ Y, int i, float2 yi,
                                                  int lane) {
-  const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
   float ax = 0.f, ay = 0.f;
-  for (int64_t e = e0 + lane; e < e1; e += 32) {
-    const int j = __ldcs(col + e);
-    const float p = __ldcs(val + e);
-    const float2 yj = Y[j];
-    const float dx = yi.x - yj.x, dy = yi.y - yj.y;
-    const float w = __frcp_rn(1.f + dx * dx + dy * dy);
-    const float pw = p * w;
-    ax = fmaf(pw, dx, ax);
-    ay = fmaf(pw, dy, ay);
+  for (int64_t b = (e0 & ~int64_t(3)) + 4 * lane; b < e1; b += 128) {
+    int c[4];
+    float p[4];
+    if (b + 3 < nnz) {
+      const int4 cv = __ldcs(reinterpret_cast<const int4*>(col + b));
+      const float4 pv = __ldcs(reinterpret_cast<const float4*>(val + b));
+      c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
+      p[0] = pv.x; p[1] = pv.y; p[2] = pv.z; p[3] = pv.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool ok = b + q < nnz;
+        c[q] = ok ? __ldcs(col + b + q) : i;
+        p[q] = ok ? __ldcs(val + b + q) : 0.f;
+      }
+    }
+    float2 yj[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool in = (b + q >= e0) && (b + q < e1);
+      if (!in) { c[q] = i; p[q] = 0.f; }
+      yj[q] = Y[c[q]];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float dx = yi.x - yj[q].x, dy = yi.y - yj[q].y;
+      const float w = __frcp_rn(1.f + dx * dx + dy * dy);
+      const float pw = p[q] * w;
+      ax = fmaf(pw, dx, ax);
+      ay = fmaf(pw, dy, ay);
+    }
   }
   return make_float2(warp_sum(ax), warp_sum(ay));
 }
@@ -49,9 +76,10 @@ k_attract_grad(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ 
   const int warp = (blockIdx.x * kAttrThreads + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * kAttrThreads) >> 5;
   const float invZ = (float)Z[1];
+  const int64_t nnz = row_ptr[N];
   for (int i = warp; i < N; i += nwarps) {
     const float2 yi = Y[i];
-    const float2 a = row_attractive(row_ptr, col, val, Y, i, yi, lane);
+    const float2 a = row_attractive(row_ptr[i], row_ptr[i + 1], nnz, col, val, Y, i, yi, lane);
     if (lane == 0) {
       const float2 f = rep[i];
       dY[i] = make_float2(4.f * (alpha * a.x - f.x * invZ), 4.f * (alpha * a.y - f.y * invZ));
@@ -71,7 +99,7 @@ __device__ __forceinline__ void update_coord(float g, float& v, float& gain, flo
   y = y + v;
 }
 
-__global__ void __launch_bounds__(kAttrThreads)
+__global__ void __launch_bounds__(kAttrThreads, kAttrBlocksPerSM)
 k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                  const float* __restrict__ val, const float2* __restrict__ Yin, int N,
                  const float2* __restrict__ rep, const double* __restrict__ Z,
@@ -86,17 +114,20 @@ k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   const float alpha = (t < sc.exag_iters) ? sc.exag : 1.f;
   const float mu = (t < sc.exag_iters) ? sc.mom0 : sc.mom1;
   const float invZ = (float)Z[1];
+  const int64_t nnz = row_ptr[N];
   double sx = 0.0, sy = 0.0;
   float mnx = INFINITY, mxx = -INFINITY, mny = INFINITY, mxy = -INFINITY;
   bool bad = false;
   for (int i = warp; i < N; i += nwarps) {
     const float2 yi = Yin[i];
-    const float2 a = row_attractive(row_ptr, col, val, Yin, i, yi, lane);
+    const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    float2 f, v, gn;
+    if (lane == 0) { f = rep[i]; v = V[i]; gn = G[i]; }      // issued before the row's loads
+    const float2 a = row_attractive(e0, e1, nnz, col, val, Yin, i, yi, lane);
     if (lane == 0) {
-      const float2 f = rep[i];
       const float gx = 4.f * (alpha * a.x - f.x * invZ);
       const float gy = 4.f * (alpha * a.y - f.y * invZ);
-      float2 v = V[i], gn = G[i], y = yi;
+      float2 y = yi;
       update_coord(gx, v.x, gn.x, y.x, mu, sc.eta, sc.min_gain);
       update_coord(gy, v.y, gn.y, y.y, mu, sc.eta, sc.min_gain);
       V[i] = v;
@@ -110,8 +141,8 @@ k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
     }
   }
   // block partials (lane 0 of each warp holds its rows' sums)
-  __shared__ double2 s_s[kAttrWarps];
-  __shared__ float4 s_b[kAttrWarps];
+  __shared__ double2 s_s[kAttrThreads];
+  __shared__ float4 s_b[kAttrThreads];
   __shared__ bool s_last;
   if (lane == 0) {
     s_s[wid] = make_double2(sx, sy);
@@ -134,17 +165,34 @@ k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
     s_last = (prev == gridDim.x - 1);
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    __threadfence();
-    double2 ss = make_double2(0.0, 0.0);
-    float4 bb = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
-    for (int q = 0; q < (int)gridDim.x; ++q) {
-      const double2 a = __ldcg(part2 + q);
-      const float4 b = __ldcg(part4 + q);
-      ss.x += a.x; ss.y += a.y;
-      bb.x = fminf(bb.x, b.x); bb.y = fmaxf(bb.y, b.y);
-      bb.z = fminf(bb.z, b.z); bb.w = fmaxf(bb.w, b.w);
+  if (!s_last) return;
+  // last block: fixed-order reduction of the per-block partials (deterministic)
+  __threadfence();
+  double2 ss = make_double2(0.0, 0.0);
+  float4 bb = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
+  for (int q = threadIdx.x; q < (int)gridDim.x; q += kAttrThreads) {
+    const double2 a = __ldcg(part2 + q);
+    const float4 b = __ldcg(part4 + q);
+    ss.x += a.x; ss.y += a.y;
+    bb.x = fminf(bb.x, b.x); bb.y = fmaxf(bb.y, b.y);
+    bb.z = fminf(bb.z, b.z); bb.w = fmaxf(bb.w, b.w);
+  }
+  s_s[threadIdx.x] = ss;
+  s_b[threadIdx.x] = bb;
+  __syncthreads();
+  for (int o = kAttrThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double2 a = s_s[threadIdx.x + o];
+      const float4 b = s_b[threadIdx.x + o];
+      s_s[threadIdx.x].x += a.x; s_s[threadIdx.x].y += a.y;
+      float4& c = s_b[threadIdx.x];
+      c.x = fminf(c.x, b.x); c.y = fmaxf(c.y, b.y); c.z = fminf(c.z, b.z); c.w = fmaxf(c.w, b.w);
     }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    ss = s_s[0];
+    bb = s_b[0];
     // recentring (D15): y <- y - mean, applied by the next tree build; by the
     // monotonicity of rounding, min(fl(y - m)) = fl(min(y) - m) exactly.
     const float mx = (float)(ss.x / (double)N), my = (float)(ss.y / (double)N);
@@ -161,7 +209,7 @@ k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
 
 int attract_blocks(int64_t N) {
   int64_t b = (N + kAttrWarps - 1) / kAttrWarps;
-  int64_t cap = (int64_t)kNumSMs * 8;
+  int64_t cap = (int64_t)kNumSMs * kAttrBlocksPerSM;
   return (int)(b < cap ? (b < 1 ? 1 : b) : cap);
 }
 

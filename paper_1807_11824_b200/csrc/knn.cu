@@ -15,26 +15,14 @@
 //                the K' candidates; sort by (d2, index) (D18); certificate
 //                d2_(K) < approx_(K') - 2 e_row (D26).
 #include <cfloat>
+#include <cstdlib>
+#include <cstring>
 
 #include "knn.cuh"
+#include "knn_select.cuh"
 #include "knn_tc.cuh"
 
 namespace tsne {
-
-typedef unsigned long long u64;
-constexpr u64 kKeyMax = ~0ull;
-
-__device__ __forceinline__ u64 mkkey(float a, int j) {
-  unsigned u = __float_as_uint(a);
-  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-  return ((u64)u << 32) | (unsigned)j;
-}
-__device__ __forceinline__ float key_val(u64 k) {
-  unsigned u = (unsigned)(k >> 32);
-  u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
-  return __uint_as_float(u);
-}
-__device__ __forceinline__ int key_idx(u64 k) { return (int)(unsigned)(k & 0xffffffffull); }
 
 static inline int kc_of(int64_t N, int K) {
   int64_t kc = ((K + kCandExtra + 31) / 32) * 32;
@@ -127,44 +115,7 @@ __global__ void k_convert(const float* __restrict__ X, int64_t N, int D, int Dp,
     acc += (double)(f * f);
   }
   acc = warp_sum(acc);
-  if (lane == 0 && row < N) nrm[row] = (float)acc;
-}
-
-// ---------------------------------------------------------------- top-K' machinery
-__device__ void warp_bitonic_sort(u64* a, int P, int lane) {
-  for (int k = 2; k <= P; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = lane; i < P; i += 32) {
-        const int l = i ^ j;
-        if (l > i) {
-          const bool up = ((i & k) == 0);
-          const u64 x = a[i], y = a[l];
-          if ((x > y) == up) { a[i] = y; a[l] = x; }
-        }
-      }
-      __syncwarp();
-    }
-}
-
-// sort the row's buffer and keep its Kc smallest keys
-__device__ void compact_row(u64* __restrict__ rowbuf, int& cnt, u64& tau, int Kc, u64* sm,
-                            int lane, u64* out) {
-  const int n = cnt;
-  int P = 32;
-  while (P < n) P <<= 1;
-  for (int i = lane; i < P; i += 32) sm[i] = (i < n) ? rowbuf[i] : kKeyMax;
-  __syncwarp();
-  warp_bitonic_sort(sm, P, lane);
-  const int keep = n < Kc ? n : Kc;
-  for (int i = lane; i < keep; i += 32) {
-    rowbuf[i] = sm[i];
-    if (out) out[i] = sm[i];
-  }
-  __syncwarp();
-  const u64 t = (keep == Kc) ? sm[Kc - 1] : kKeyMax;
-  __syncwarp();
-  if (lane == 0) { cnt = keep; tau = t; }
-  __syncwarp();
+  if (lane == 0) nrm[row] = row < N ? (float)acc : 0.f;
 }
 
 // ---------------------------------------------------------------- v1 candidates (CUDA cores)
@@ -269,9 +220,13 @@ k_cand_simt(const __half* __restrict__ Xh, const float* __restrict__ nrm, int N,
       __syncthreads();
       if (sm.flag) {
         for (int r = wid; r < kKnnBM; r += kS_Threads / 32) {
-          if (sm.cnt[r] > kCandCap - kS_BN)
-            compact_row(mybuf + (size_t)r * kCandCap, sm.cnt[r], sm.tau[r], Kc, sm.sortbuf[wid],
-                        lane, nullptr);
+          if (sm.cnt[r] > kCandCap - kS_BN) {
+            u64 t;
+            const int keep = compact_keys(mybuf + (size_t)r * kCandCap, sm.cnt[r], Kc,
+                                          sm.sortbuf[wid], lane, nullptr, t);
+            if (lane == 0) { sm.cnt[r] = keep; sm.tau[r] = t; }
+            __syncwarp();
+          }
         }
         __syncthreads();
       }
@@ -279,9 +234,11 @@ k_cand_simt(const __half* __restrict__ Xh, const float* __restrict__ nrm, int N,
     // final: every row -> its Kc best keys
     for (int r = wid; r < kKnnBM; r += kS_Threads / 32) {
       const int q = q0 + r;
-      if (q < N)
-        compact_row(mybuf + (size_t)r * kCandCap, sm.cnt[r], sm.tau[r], Kc, sm.sortbuf[wid], lane,
-                    cand + (size_t)q * Kc);
+      if (q < N) {
+        u64 t;
+        compact_keys(mybuf + (size_t)r * kCandCap, sm.cnt[r], Kc, sm.sortbuf[wid], lane,
+                     cand + (size_t)q * Kc, t);
+      }
     }
     __syncthreads();
   }
@@ -378,7 +335,9 @@ tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int32_t* id
     TSNE_LAUNCH_CHECK();
   }
   TSNE_CUDA_TRY(cudaMemsetAsync(w.uncert, 0, 2 * sizeof(u64), s));
-  bool tc = knn_tc_available() && Dp % 64 == 0;
+  // TSNE_KNN_PATH=simt forces the CUDA-core candidate stage (cross-checks)
+  const char* force = getenv("TSNE_KNN_PATH");
+  bool tc = knn_tc_available() && Dp % 64 == 0 && !(force && strcmp(force, "simt") == 0);
   if (tc) {
     tsne_status st = launch_cand_tc(w.Xh, w.nrm, (int)N, Dp, Kc, w.buf, w.cand, w.slots, s);
     if (st != TSNE_OK) return st;

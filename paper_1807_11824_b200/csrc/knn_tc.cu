@@ -1,11 +1,309 @@
-// knn_tc.cu -- placeholder until the tcgen05 candidate kernel lands.
+// knn_tc.cu -- the kNN candidate stage on the 5th-generation tensor cores
+// (U1; the paper's line 1 is FAISS, P:L151 -- this build's exact
+// kNN needs the full N x N distance product, a dense contraction, so it runs
+// on tcgen05).
+//
+// Persistent warp-specialised kernel, one CTA per SM (192 threads):
+//   warp 0      TMA producer: 128x64 (queries) and 256x64 (points) fp16 tiles,
+//               128-byte swizzle, 4-stage mbarrier ring (48 KB per stage)
+//   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128 N=256
+//               K=16, fp32 accumulators in TMEM, double-buffered (2 x 256 cols)
+//   warps 2-5   epilogue: tcgen05.ld 32x32b (thread <-> query row), distance
+//               |y|^2 - 2 x.y, per-row threshold filter, append to the row's
+//               candidate buffer, warp bitonic compaction to the K' best keys
+// The N x N matrix never exists; the only output is K' candidate keys / row.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "knn_select.cuh"
 #include "knn_tc.cuh"
 
 namespace tsne {
-bool knn_tc_available() { return false; }
-tsne_status launch_cand_tc(const __half*, const float*, int, int, int, unsigned long long*,
-                           unsigned long long*, int, cudaStream_t) {
-  set_error("tcgen05 kNN path not built");
-  return TSNE_ERR_CUDA;
+
+constexpr int TC_BM = 128, TC_BN = 256, TC_BK = 64, TC_STAGES = 4;
+constexpr int TC_CAP = 512;                     // per-row candidate buffer
+constexpr int TC_THREADS = 192;
+constexpr uint32_t TC_A_BYTES = TC_BM * TC_BK * 2;           // 16 KB
+constexpr uint32_t TC_B_BYTES = TC_BN * TC_BK * 2;           // 32 KB
+constexpr uint32_t TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;  // 48 KB
+// instruction descriptor, kind::f16: D f32 (bits 4-5 = 1), A/B f16 (0), both
+// K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28
+constexpr uint32_t TC_IDESC = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) |
+                              ((uint32_t)(TC_BM >> 4) << 24);
+constexpr size_t TC_SMEM = 1024 + TC_STAGES * TC_STAGE_BYTES + 256 + 4 * TC_CAP * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+// K-major operand in 128-byte-swizzled smem: rows of 128 B, 8-row atoms
+// 1024 B apart (SBO), descriptor version 1 (sm_100), layout SWIZZLE_128B (2)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nrm, int N, int Dp,
+          int Kc, u64* __restrict__ buf, u64* __restrict__ cand) {
+  extern __shared__ unsigned char smraw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + TC_STAGES * TC_STAGE_BYTES);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* tfull = empty + TC_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  u64* sortbuf = reinterpret_cast<u64*>(base + TC_STAGES * TC_STAGE_BYTES + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = Dp / TC_BK;
+  const int nrb = (N + TC_BM - 1) / TC_BM, nct = (N + TC_BN - 1) / TC_BN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {                                             // ---- TMA producer
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x)
+        for (int ct = 0; ct < nct; ++ct)
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_tx(&full[stage], TC_STAGE_BYTES);
+            unsigned char* sa = base + stage * TC_STAGE_BYTES;
+            tma_load_2d(sa, &tmap, &full[stage], kb * TC_BK, rb * TC_BM);
+            tma_load_2d(sa + TC_A_BYTES, &tmap, &full[stage], kb * TC_BK, ct * TC_BN);
+            tma_load_2d(sa + TC_A_BYTES + TC_A_BYTES, &tmap, &full[stage], kb * TC_BK,
+                        ct * TC_BN + 128);
+            if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+          }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {                                             // ---- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0, aphase = 0;
+      int acc = 0;
+      for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x)
+        for (int ct = 0; ct < nct; ++ct) {
+          mbar_wait(&tempty[acc], aphase ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(acc * TC_BN);
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(base + stage * TC_STAGE_BYTES);
+            const uint32_t sb = sa + TC_A_BYTES;
+#pragma unroll
+            for (int k = 0; k < TC_BK / 16; ++k)
+              mma_f16(d, sw128_desc(sa + 32 * k), sw128_desc(sb + 32 * k), TC_IDESC,
+                      (kb | k) != 0 ? 1u : 0u);
+            mma_commit(&empty[stage]);
+            if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+          }
+          mma_commit(&tfull[acc]);
+          acc ^= 1;
+          if (acc == 0) aphase ^= 1;
+        }
+    }
+  } else {                                                        // ---- epilogue
+    const int e = warp & 3;                 // TMEM lane quarter this warp may access
+    const int rl = e * 32 + lane;           // local query row
+    u64* mysort = sortbuf + (warp - 2) * TC_CAP;
+    u64* rowbuf = buf + ((size_t)blockIdx.x * TC_BM + rl) * TC_CAP;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+      const int q = rb * TC_BM + rl;
+      const bool qok = q < N;
+      int cnt = 0;
+      u64 tau = kKeyMax;
+      for (int ct = 0; ct < nct; ++ct) {
+        mbar_wait(&tfull[acc], aphase);
+        tc_fence_after();
+        const int c0 = ct * TC_BN;
+        const uint32_t tbase = tmem + ((uint32_t)(e * 32) << 16) + (uint32_t)(acc * TC_BN);
+#pragma unroll 1
+        for (int ch = 0; ch < TC_BN / 32; ++ch) {
+          uint32_t r[32];
+          tmem_ld32(tbase + ch * 32, r);
+          const int j0 = c0 + ch * 32;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int j = j0 + t;
+            const float dist = __ldg(nrm + j) - 2.f * __uint_as_float(r[t]);
+            const u64 key = mkkey(dist, j);
+            if (qok && j < N && j != q && key < tau) rowbuf[cnt++] = key;
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+        // compaction of this warp's rows that could overflow in the next tile
+        unsigned need = __ballot_sync(0xffffffffu, cnt > TC_CAP - TC_BN);
+        __syncwarp();
+        while (need) {
+          const int l = __ffs(need) - 1;
+          need &= need - 1;
+          const int n = __shfl_sync(0xffffffffu, cnt, l);
+          u64* rb_l = buf + ((size_t)blockIdx.x * TC_BM + e * 32 + l) * TC_CAP;
+          u64 t;
+          const int keep = compact_keys(rb_l, n, Kc, mysort, lane, nullptr, t);
+          if (lane == l) { cnt = keep; tau = t; }
+        }
+      }
+      // final compaction: the K' best keys of every row of this block
+      __syncwarp();
+      for (int l = 0; l < 32; ++l) {
+        const int ql = rb * TC_BM + e * 32 + l;
+        if (ql >= N) break;
+        const int n = __shfl_sync(0xffffffffu, cnt, l);
+        u64* rb_l = buf + ((size_t)blockIdx.x * TC_BM + e * 32 + l) * TC_CAP;
+        u64 t;
+        compact_keys(rb_l, n, Kc, mysort, lane, cand + (size_t)ql * Kc, t);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------- host
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool knn_tc_available() {
+  static int ok = -1;
+  if (ok < 0) {
+    ok = 0;
+    int dev = 0, major = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) == cudaSuccess &&
+        major == 10) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+              cudaSuccess &&
+          q == cudaDriverEntryPointSuccess && fn) {
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        ok = 1;
+      }
+    }
+  }
+  return ok == 1;
+}
+
+size_t knn_tc_cap() { return TC_CAP; }
+
+tsne_status launch_cand_tc(const __half* Xh, const float* nrm, int N, int Dp, int Kc,
+                           unsigned long long* buf, unsigned long long* cand, int slots,
+                           cudaStream_t s) {
+  if (!knn_tc_available()) {
+    set_error("tcgen05 path unavailable (no sm_100 device or no cuTensorMapEncodeTiled)");
+    return TSNE_ERR_CUDA;
+  }
+  CUtensorMap map;
+  cuuint64_t gdim[2] = {(cuuint64_t)Dp, (cuuint64_t)N + 256};
+  cuuint64_t gstride[1] = {(cuuint64_t)Dp * 2};
+  cuuint32_t box[2] = {TC_BK, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(Xh), gdim,
+                        gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return TSNE_ERR_CUDA;
+  }
+  TSNE_CUDA_TRY(cudaFuncSetAttribute(k_cand_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)TC_SMEM));
+  int nrb = (N + TC_BM - 1) / TC_BM;
+  int grid = nrb < kNumSMs ? nrb : kNumSMs;
+  if (grid > slots) grid = slots;
+  k_cand_tc<<<grid, TC_THREADS, TC_SMEM, s>>>(map, nrm, N, Dp, Kc, buf, cand);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
 }  // namespace tsne

@@ -4,6 +4,8 @@
 // and replayed; the iteration-dependent constants (exaggeration, momentum)
 // are read on the device from an iteration counter, so one graph serves the
 // whole run.
+#include <vector>
+
 #include "optimize.cuh"
 
 namespace tsne {
@@ -88,6 +90,65 @@ tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const flo
   k_apply_shift<<<(int)((N + 255) / 256), 256, 0, s>>>(a, (int)N, w.box);
   TSNE_LAUNCH_CHECK();
   if (a != Y) TSNE_CUDA_TRY(cudaMemcpyAsync(Y, a, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
+  return TSNE_OK;
+}
+
+tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
+                               int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t reps,
+                               float theta, const Sched& sc, TreeWS& w, OptWS& o, double* stage_ms,
+                               int32_t* kernels, cudaStream_t s) {
+  if (kernels) {  // count kernel nodes of one captured (never launched) iteration
+    cudaGraph_t g = nullptr;
+    TSNE_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    tsne_status st = one_iteration(row_ptr, col, val, N, Y, o.Yb, V, G, theta, sc, w, o, s);
+    cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (st != TSNE_OK) { if (g) cudaGraphDestroy(g); return st; }
+    TSNE_CUDA_TRY(ce);
+    size_t n = 0;
+    cudaGraphGetNodes(g, nullptr, &n);
+    std::vector<cudaGraphNode_t> nodes(n);
+    cudaGraphGetNodes(g, nodes.data(), &n);
+    int32_t k = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      cudaGraphNodeGetType(nd, &t);
+      k += (t == cudaGraphNodeTypeKernel);
+    }
+    *kernels = k;
+    cudaGraphDestroy(g);
+  }
+  k_set_state<<<1, 1, 0, s>>>(o.t_dev, t0, o.flag);
+  TSNE_LAUNCH_CHECK();
+  tsne_status st = launch_bbox(w, Y, s);
+  if (st != TSNE_OK) return st;
+  cudaEvent_t e[4];
+  for (auto& x : e) cudaEventCreate(&x);
+  double acc[3] = {0, 0, 0};
+  float2* a = Y;
+  float2* b = o.Yb;
+  for (int r = 0; r < reps && st == TSNE_OK; ++r) {
+    cudaEventRecord(e[0], s);
+    st = build_tree(w, a, true, s);
+    cudaEventRecord(e[1], s);
+    if (st == TSNE_OK) st = launch_traverse(w, theta, s);
+    cudaEventRecord(e[2], s);
+    if (st == TSNE_OK) st = launch_attract_update(row_ptr, col, val, a, N, w, o, sc, b, V, G, s);
+    cudaEventRecord(e[3], s);
+    cudaEventSynchronize(e[3]);
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e[k], e[k + 1]);
+      acc[k] += ms;
+    }
+    float2* t = a; a = b; b = t;
+  }
+  for (auto& x : e) cudaEventDestroy(x);
+  if (st != TSNE_OK) return st;
+  for (int k = 0; k < 3; ++k) stage_ms[k] = reps > 0 ? acc[k] / reps : 0.0;
+  k_apply_shift<<<(int)((N + 255) / 256), 256, 0, s>>>(a, (int)N, w.box);
+  TSNE_LAUNCH_CHECK();
+  if (a != Y) TSNE_CUDA_TRY(cudaMemcpyAsync(Y, a, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
+  TSNE_CUDA_TRY(cudaStreamSynchronize(s));
   return TSNE_OK;
 }
 
