@@ -146,6 +146,10 @@ typedef struct {
   uint64_t seed;        /* Philox4x32-10 key for Y0 (42) (D14)                  */
   const float* Y_init;  /* DEVICE [N x 2] initial embedding, NULL -> Philox     */
   int32_t use_graphs;   /* 1: replay the iteration as a CUDA graph (default)    */
+  int32_t relabel_every; /* period (iterations) of the internal relabelling of
+                           points into the Morton order of the embedding, for
+                           gather locality; 0 = never (64).  Results differ
+                           only by floating-point summation order.              */
 } tsne_config;
 
 /* Fills the defaults listed above. */
@@ -161,9 +165,11 @@ void tsne_config_default(tsne_config* cfg);
  *   alpha(t) = exaggeration if t < exag_iters else 1; mu(t) = mom0 / mom1.
  *   Y, v, gains  [N x 2] float32 in/out (the optimiser state).
  * Returns TSNE_ERR_NONFINITE if Y became non-finite (checked at the end of
- * the call; the call synchronises stream for that check).
+ * the call; the call synchronises stream for that check, and reads nnz =
+ * row_ptr[N] at entry).  The workspace depends on nnz (the library keeps
+ * two relabelled copies of P, see tsne_config.relabel_every).
  * ------------------------------------------------------------------------ */
-size_t tsne_optimize_workspace_size(int64_t N);
+size_t tsne_optimize_workspace_size(int64_t N, int64_t nnz);
 tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const float* val,
                           int64_t N, float* Y, float* v, float* gains, int32_t t0,
                           int32_t n_iter, float theta, float learning_rate,

@@ -31,7 +31,7 @@ STATUS = {0: "TSNE_OK", 1: "TSNE_ERR_ARG", 2: "TSNE_ERR_CUDA", 3: "TSNE_ERR_WORK
 class Config(C.Structure):
     _fields_ = [("K", C.c_int32), ("exag_iters", C.c_int32), ("mom0", C.c_float),
                 ("mom1", C.c_float), ("min_gain", C.c_float), ("seed", C.c_uint64),
-                ("Y_init", C.c_void_p), ("use_graphs", C.c_int32)]
+                ("Y_init", C.c_void_p), ("use_graphs", C.c_int32), ("relabel_every", C.c_int32)]
 
 
 class KnnInfo(C.Structure):
@@ -76,7 +76,7 @@ def lib():
     L.tsne_gradient_workspace_size.restype = sz
     L.tsne_gradient.argtypes = [vp, vp, vp, i64, vp, f32, f32, vp, C.POINTER(C.c_double), vp, sz,
                                 vp]
-    L.tsne_optimize_workspace_size.argtypes = [i64]
+    L.tsne_optimize_workspace_size.argtypes = [i64, i64]
     L.tsne_optimize_workspace_size.restype = sz
     L.tsne_optimize.argtypes = [vp, vp, vp, i64, vp, vp, vp, i32, i32, f32, f32, f32,
                                 C.POINTER(Config), vp, sz, vp]
@@ -197,7 +197,7 @@ class Optimizer:
 
     def __init__(self, row_ptr, col, val, Y: torch.Tensor, theta=0.5, learning_rate=200.0,
                  exaggeration=12.0, exag_iters=250, mom0=0.5, mom1=0.8, min_gain=0.01,
-                 use_graphs=True):
+                 use_graphs=True, relabel_every=64):
         self.row_ptr = _dev(row_ptr, torch.int64, "row_ptr")
         self.col = _dev(col, torch.int32, "col")
         self.val = _dev(val, torch.float32, "val")
@@ -206,8 +206,10 @@ class Optimizer:
         self.state = State(Y, torch.zeros_like(Y), torch.ones_like(Y), 0)
         self.theta, self.lr, self.exag = float(theta), float(learning_rate), float(exaggeration)
         self.cfg = default_config(exag_iters=exag_iters, mom0=mom0, mom1=mom1, min_gain=min_gain,
-                                  use_graphs=1 if use_graphs else 0)
-        self.ws = _ws(lib().tsne_optimize_workspace_size(self.N), Y.device)
+                                  use_graphs=1 if use_graphs else 0,
+                                  relabel_every=int(relabel_every))
+        self.nnz = int(self.col.numel())
+        self.ws = _ws(lib().tsne_optimize_workspace_size(self.N, self.nnz), Y.device)
 
     def step(self, n_iter: int = 1, stream=None):
         s = self.state
@@ -246,7 +248,7 @@ def init_y(N: int, seed: int = 42, device="cuda") -> torch.Tensor:
 # ---------------------------------------------------------------- Algorithm 1
 def run(X: torch.Tensor, perplexity=30.0, theta=0.5, learning_rate=200.0, n_iter=1000,
         exaggeration=12.0, Y_out: torch.Tensor | None = None, Y_init: torch.Tensor | None = None,
-        seed: int = 42, K: int = 0, exag_iters: int = 250, use_graphs=True):
+        seed: int = 42, K: int = 0, exag_iters: int = 250, use_graphs=True, relabel_every=64):
     """End to end (tsne_run_ex).  X may live on the host (pinned for speed) or
     the device; Y_out (optional) likewise.  Returns (Y_out, info dict)."""
     if X.dtype != torch.float32:
@@ -261,7 +263,7 @@ def run(X: torch.Tensor, perplexity=30.0, theta=0.5, learning_rate=200.0, n_iter
         yi = _dev(Y_init, torch.float32, "Y_init")
     cfg = default_config(K=int(K), exag_iters=exag_iters, seed=seed,
                          Y_init=(yi.data_ptr() if yi is not None else None),
-                         use_graphs=1 if use_graphs else 0)
+                         use_graphs=1 if use_graphs else 0, relabel_every=int(relabel_every))
     info = RunInfo()
     if X.is_cuda or Y_out.is_cuda:
         torch.cuda.current_stream().synchronize()   # tsne_run_ex runs on its own stream

@@ -54,10 +54,10 @@ struct OptPlan {
   OptWS opt;
 };
 
-static size_t opt_plan(void* base, int64_t N, OptPlan& p) {
+static size_t opt_plan(void* base, int64_t N, int64_t nnz, OptPlan& p) {
   Carver c(base);
   carve_tree(c, p.tree, N);
-  carve_opt(c, p.opt, N);
+  carve_opt(c, p.opt, N, nnz);
   return c.bytes();
 }
 
@@ -111,6 +111,7 @@ void tsne_config_default(tsne_config* cfg) {
   cfg->seed = 42;
   cfg->Y_init = nullptr;
   cfg->use_graphs = 1;
+  cfg->relabel_every = 64;
 }
 
 // ---------------------------------------------------------------- gradient
@@ -159,10 +160,21 @@ tsne_status tsne_gradient(const int64_t* row_ptr, const int32_t* col, const floa
 }
 
 // ---------------------------------------------------------------- optimise
-size_t tsne_optimize_workspace_size(int64_t N) {
-  if (N < 2) return 0;
+size_t tsne_optimize_workspace_size(int64_t N, int64_t nnz) {
+  if (N < 2 || nnz < 0) return 0;
   OptPlan p;
-  return opt_plan(nullptr, N, p);
+  return opt_plan(nullptr, N, nnz, p);
+}
+
+// nnz = row_ptr[N] (one 8-byte device read; synchronises the stream)
+static tsne_status read_nnz(const int64_t* row_ptr, int64_t N, int64_t* nnz, cudaStream_t s) {
+  TSNE_CUDA_TRY(cudaMemcpyAsync(nnz, row_ptr + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  TSNE_CUDA_TRY(cudaStreamSynchronize(s));
+  if (*nnz < 0) {
+    set_error("row_ptr[N] = %lld < 0", (long long)*nnz);
+    return TSNE_ERR_ARG;
+  }
+  return TSNE_OK;
 }
 
 tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t N,
@@ -183,23 +195,25 @@ tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const floa
   TSNE_ARG_CHECK(aligned(Y, 8) && aligned(v, 8) && aligned(gains, 8) && aligned(col, 16) &&
                      aligned(val, 16),
                  "Y, v, gains need 8-byte and col, val 16-byte alignment");
+  tsne_status st = check_device();
+  if (st != TSNE_OK) return st;
+  int64_t nnz = 0;
+  if ((st = read_nnz(row_ptr, N, &nnz, (cudaStream_t)stream)) != TSNE_OK) return st;
   OptPlan p;
-  size_t need = opt_plan(nullptr, N, p);
+  size_t need = opt_plan(nullptr, N, nnz, p);
   if (!ws || ws_bytes < need) {
     set_error("workspace too small: need %zu bytes, got %zu", need, ws_bytes);
     return TSNE_ERR_WORKSPACE;
   }
-  tsne_status st = check_device();
-  if (st != TSNE_OK) return st;
   if (n_iter == 0) return TSNE_OK;
-  opt_plan(ws, N, p);
+  opt_plan(ws, N, nnz, p);
   SideStream ss;
   cudaStream_t s = ss.get((cudaStream_t)stream);
   if ((st = init_tree_ws(p.tree, s)) != TSNE_OK) { ss.join(); return st; }
   Sched sc{cfg.exag_iters, exaggeration, cfg.mom0, cfg.mom1, learning_rate, cfg.min_gain};
   st = run_iterations(row_ptr, col, val, N, reinterpret_cast<float2*>(Y),
                       reinterpret_cast<float2*>(v), reinterpret_cast<float2*>(gains), t0, n_iter,
-                      theta, sc, cfg.use_graphs != 0, p.tree, p.opt, s);
+                      theta, sc, cfg.use_graphs != 0, cfg.relabel_every, p.tree, p.opt, s);
   int32_t flag = 0;
   if (st == TSNE_OK) {
     cudaError_t e = cudaMemcpyAsync(&flag, p.opt.flag, sizeof(flag), cudaMemcpyDeviceToHost, s);
@@ -230,15 +244,17 @@ tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, 
   TSNE_ARG_CHECK(N >= 2 && N < (int64_t(1) << 27), "N must be in [2, 2^27)");
   TSNE_ARG_CHECK(row_ptr && col && val && Y && v && gains && stage_ms, "null pointer argument");
   TSNE_ARG_CHECK(reps >= 1 && t0 >= 0, "reps must be >= 1");
+  tsne_status st = check_device();
+  if (st != TSNE_OK) return st;
+  int64_t nnz = 0;
+  if ((st = read_nnz(row_ptr, N, &nnz, (cudaStream_t)stream)) != TSNE_OK) return st;
   OptPlan p;
-  size_t need = opt_plan(nullptr, N, p);
+  size_t need = opt_plan(nullptr, N, nnz, p);
   if (!ws || ws_bytes < need) {
     set_error("workspace too small: need %zu bytes, got %zu", need, ws_bytes);
     return TSNE_ERR_WORKSPACE;
   }
-  tsne_status st = check_device();
-  if (st != TSNE_OK) return st;
-  opt_plan(ws, N, p);
+  opt_plan(ws, N, nnz, p);
   SideStream ss;
   cudaStream_t s = ss.get((cudaStream_t)stream);
   if ((st = init_tree_ws(p.tree, s)) != TSNE_OK) { ss.join(); return st; }
@@ -369,7 +385,7 @@ tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, 
   {
     PWS w; Carver c(nullptr); carve_p(c, w, N, K); pb = c.bytes();
   }
-  ob = tsne_optimize_workspace_size(N);
+  ob = tsne_optimize_workspace_size(N, cap);
   // buffers: X (if host), idx, d2, row_ptr, col, val, Y, v, gains, workspace
   Carver plan(nullptr);
   plan.take<float>(x_host ? N * D : 0);
@@ -443,12 +459,12 @@ tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, 
   }
   if (st == TSNE_OK) {
     OptPlan p;
-    opt_plan(ws, N, p);
+    opt_plan(ws, N, nnz, p);
     st = init_tree_ws(p.tree, s);
     Sched sc{cfg.exag_iters, exaggeration, cfg.mom0, cfg.mom1, learning_rate, cfg.min_gain};
     if (st == TSNE_OK)
       st = run_iterations(rp, col, val, N, Y, V, G, 0, n_iter, theta, sc, cfg.use_graphs != 0,
-                          p.tree, p.opt, s);
+                          cfg.relabel_every, p.tree, p.opt, s);
     if (st == TSNE_OK) {
       int32_t flag = 0;
       cudaMemcpyAsync(&flag, p.opt.flag, sizeof(flag), cudaMemcpyDeviceToHost, s);

@@ -118,21 +118,81 @@ k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   double sx = 0.0, sy = 0.0;
   float mnx = INFINITY, mxx = -INFINITY, mny = INFINITY, mxy = -INFINITY;
   bool bad = false;
-  for (int i = warp; i < N; i += nwarps) {
-    const float2 yi = Yin[i];
-    const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
-    float2 f, v, gn;
-    if (lane == 0) { f = rep[i]; v = V[i]; gn = G[i]; }      // issued before the row's loads
-    const float2 a = row_attractive(e0, e1, nnz, col, val, Yin, i, yi, lane);
-    if (lane == 0) {
-      const float gx = 4.f * (alpha * a.x - f.x * invZ);
-      const float gy = 4.f * (alpha * a.y - f.y * invZ);
-      float2 y = yi;
+  // A warp owns 32 consecutive rows; 4 rows are summed at a time by 8-lane
+  // subgroups (16-byte vector loads of col/val over each row's aligned
+  // window), then every lane updates its own row (coalesced state access).
+  const int sg = lane >> 3, sl = lane & 7;
+  const int ngroups = (N + 31) / 32;
+  for (int grp = warp; grp < ngroups; grp += nwarps) {
+    const int r0 = grp * 32;
+    const int rl = r0 + lane;
+    const bool rok = rl < N;
+    const int64_t my_e0 = row_ptr[rok ? rl : N];
+    const int64_t my_e1 = row_ptr[rok ? rl + 1 : N];
+    const float2 my_y = rok ? Yin[rl] : make_float2(0.f, 0.f);
+    float2 amine = make_float2(0.f, 0.f);
+#pragma unroll 1
+    for (int it = 0; it < 8; ++it) {
+      const int src = it * 4 + sg;                       // row r0 + src for this subgroup
+      const int64_t e0 = __shfl_sync(0xffffffffu, my_e0, src);
+      const int64_t e1 = __shfl_sync(0xffffffffu, my_e1, src);
+      const float2 yi = make_float2(__shfl_sync(0xffffffffu, my_y.x, src),
+                                    __shfl_sync(0xffffffffu, my_y.y, src));
+      const int i = r0 + src;
+      float ax = 0.f, ay = 0.f;
+      for (int64_t b = (e0 & ~int64_t(3)) + 4 * sl; b < e1; b += 32) {
+        int c[4];
+        float p[4];
+        if (b + 3 < nnz) {
+          const int4 cv = __ldcs(reinterpret_cast<const int4*>(col + b));
+          const float4 pv = __ldcs(reinterpret_cast<const float4*>(val + b));
+          c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
+          p[0] = pv.x; p[1] = pv.y; p[2] = pv.z; p[3] = pv.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool ok = b + q < nnz;
+            c[q] = ok ? __ldcs(col + b + q) : i;
+            p[q] = ok ? __ldcs(val + b + q) : 0.f;
+          }
+        }
+        float2 yj[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool in = (b + q >= e0) && (b + q < e1);
+          if (!in) { c[q] = i; p[q] = 0.f; }
+          yj[q] = Yin[c[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float dx = yi.x - yj[q].x, dy = yi.y - yj[q].y;
+          const float w = __frcp_rn(1.f + dx * dx + dy * dy);
+          const float pw = p[q] * w;
+          ax = fmaf(pw, dx, ax);
+          ay = fmaf(pw, dy, ay);
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {                  // fixed 8-lane butterfly
+        ax += __shfl_xor_sync(0xffffffffu, ax, o);
+        ay += __shfl_xor_sync(0xffffffffu, ay, o);
+      }
+      // lane L receives row r0 + L (computed at it = L >> 2 by subgroup L & 3)
+      const float vx = __shfl_sync(0xffffffffu, ax, (lane & 3) * 8);
+      const float vy = __shfl_sync(0xffffffffu, ay, (lane & 3) * 8);
+      if ((lane >> 2) == it) amine = make_float2(vx, vy);
+    }
+    if (rok) {
+      const float2 f = rep[rl];
+      float2 v = V[rl], gn = G[rl];
+      const float gx = 4.f * (alpha * amine.x - f.x * invZ);
+      const float gy = 4.f * (alpha * amine.y - f.y * invZ);
+      float2 y = my_y;
       update_coord(gx, v.x, gn.x, y.x, mu, sc.eta, sc.min_gain);
       update_coord(gy, v.y, gn.y, y.y, mu, sc.eta, sc.min_gain);
-      V[i] = v;
-      G[i] = gn;
-      Yout[i] = y;
+      V[rl] = v;
+      G[rl] = gn;
+      Yout[rl] = y;
       sx += (double)y.x;
       sy += (double)y.y;
       mnx = fminf(mnx, y.x); mxx = fmaxf(mxx, y.x);
@@ -140,7 +200,12 @@ k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
       bad |= !(isfinite(y.x) && isfinite(y.y));
     }
   }
-  // block partials (lane 0 of each warp holds its rows' sums)
+  sx = warp_sum(sx);
+  sy = warp_sum(sy);
+  mnx = warp_min(mnx); mxx = warp_max(mxx);
+  mny = warp_min(mny); mxy = warp_max(mxy);
+  bad = __any_sync(0xffffffffu, bad);
+  // block partials
   __shared__ double2 s_s[kAttrThreads];
   __shared__ float4 s_b[kAttrThreads];
   __shared__ bool s_last;
@@ -148,7 +213,7 @@ k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
     s_s[wid] = make_double2(sx, sy);
     s_b[wid] = make_float4(mnx, mxx, mny, mxy);
   }
-  if (bad) *flag = 1;
+  if (bad && lane == 0) *flag = 1;
   __syncthreads();
   if (threadIdx.x == 0) {
     double2 ss = s_s[0];

@@ -51,6 +51,7 @@ void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K) {
   w.cand = c.take<u64>((size_t)N * w.Kc);
   w.uncert = c.take<u64>(2);
   w.rows_bad = c.take<int32_t>(N);
+  w.sync = c.take<unsigned>(knn_tc_sync_words(N));
 }
 
 // ---------------------------------------------------------------- prep
@@ -222,8 +223,8 @@ k_cand_simt(const __half* __restrict__ Xh, const float* __restrict__ nrm, int N,
         for (int r = wid; r < kKnnBM; r += kS_Threads / 32) {
           if (sm.cnt[r] > kCandCap - kS_BN) {
             u64 t;
-            const int keep = compact_keys(mybuf + (size_t)r * kCandCap, sm.cnt[r], Kc,
-                                          sm.sortbuf[wid], lane, nullptr, t);
+            const int keep = reduce_keys(mybuf + (size_t)r * kCandCap, sm.cnt[r], Kc,
+                                         kCandCap - kS_BN, sm.sortbuf[wid], lane, t);
             if (lane == 0) { sm.cnt[r] = keep; sm.tau[r] = t; }
             __syncwarp();
           }
@@ -339,7 +340,7 @@ tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int32_t* id
   const char* force = getenv("TSNE_KNN_PATH");
   bool tc = knn_tc_available() && Dp % 64 == 0 && !(force && strcmp(force, "simt") == 0);
   if (tc) {
-    tsne_status st = launch_cand_tc(w.Xh, w.nrm, (int)N, Dp, Kc, w.buf, w.cand, w.slots, s);
+    tsne_status st = launch_cand_tc(w.Xh, w.nrm, (int)N, Dp, Kc, w.buf, w.cand, w.slots, w.sync, s);
     if (st != TSNE_OK) return st;
   } else {
     const size_t smem = sizeof(SimtSmem);

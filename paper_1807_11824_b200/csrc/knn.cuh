@@ -25,6 +25,7 @@ struct KnnWS {
   unsigned long long* cand = nullptr;  // N x Kc final candidate keys (sorted)
   unsigned long long* uncert = nullptr;  // [0] count of uncertified rows
   int32_t* rows_bad = nullptr;    // list of uncertified rows (N)
+  unsigned* sync = nullptr;       // CTA checkpoint counters of the tcgen05 sweep
   int32_t path = 0;
 };
 

@@ -10,7 +10,7 @@
 //               K=16, fp32 accumulators in TMEM, double-buffered (2 x 256 cols)
 //   warps 2-5   epilogue: tcgen05.ld 32x32b (thread <-> query row), distance
 //               |y|^2 - 2 x.y, per-row threshold filter, append to the row's
-//               candidate buffer, warp bitonic compaction to the K' best keys
+//               candidate buffer, warp pivot compaction (final: bitonic sort)
 // The N x N matrix never exists; the only output is K' candidate keys / row.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -21,8 +21,9 @@
 namespace tsne {
 
 constexpr int TC_BM = 128, TC_BN = 256, TC_BK = 64, TC_STAGES = 4;
-constexpr int TC_CAP = 512;                     // per-row candidate buffer
+constexpr int TC_CAP = 1024;                    // per-row candidate buffer
 constexpr int TC_THREADS = 192;
+constexpr int TC_SYNC_EVERY = 8;                // column tiles between CTA checkpoints
 constexpr uint32_t TC_A_BYTES = TC_BM * TC_BK * 2;           // 16 KB
 constexpr uint32_t TC_B_BYTES = TC_BN * TC_BK * 2;           // 32 KB
 constexpr uint32_t TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;  // 48 KB
@@ -38,11 +39,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
 }
+// try_wait with a suspend-time hint: a waiting thread sleeps instead of
+// spinning, so the producer / MMA threads do not steal issue slots from the
+// epilogue warps sharing their SM sub-partition.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 1000000;\n\t"
       "@P1 bra DONE_%=;\n\t"
       "bra WAIT_%=;\n\t"
       "DONE_%=:\n\t}" ::"r"(smem_u32(b)),
@@ -108,7 +112,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nrm, int N, int Dp,
-          int Kc, u64* __restrict__ buf, u64* __restrict__ cand) {
+          int Kc, u64* __restrict__ buf, u64* __restrict__ cand, unsigned* __restrict__ sync) {
   extern __shared__ unsigned char smraw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -143,8 +147,26 @@ k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nr
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x)
-        for (int ct = 0; ct < nct; ++ct)
+      const int ncp = (nct + TC_SYNC_EVERY - 1) / TC_SYNC_EVERY;
+      int wave = 0;
+      for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x, ++wave)
+        for (int ct = 0; ct < nct; ++ct) {
+          if (sync && ct % TC_SYNC_EVERY == 0) {
+            // keep all CTAs of this wave within 2 checkpoints of each other, so
+            // the database tiles they stream stay L2-resident between CTAs
+            const int members = min((int)gridDim.x, nrb - wave * (int)gridDim.x);
+            const int cp = ct / TC_SYNC_EVERY;
+            unsigned* base_c = sync + (size_t)wave * ncp;
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(base_c + cp) : "memory");
+            if (cp >= 2) {
+              for (int spin = 0; spin < (1 << 22); ++spin) {
+                unsigned v;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(base_c + cp - 2) : "memory");
+                if ((int)v >= members) break;
+                __nanosleep(256);
+              }
+            }
+          }
           for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_tx(&full[stage], TC_STAGE_BYTES);
@@ -155,6 +177,7 @@ k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nr
                         ct * TC_BN + 128);
             if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
           }
+        }
     }
   } else if (warp == 1) {
     if (lane == 0) {                                             // ---- MMA issuer
@@ -202,15 +225,20 @@ k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nr
         const uint32_t tbase = tmem + ((uint32_t)(e * 32) << 16) + (uint32_t)(acc * TC_BN);
 #pragma unroll 1
         for (int ch = 0; ch < TC_BN / 32; ++ch) {
+          const int j0 = c0 + ch * 32;
+          const float nv = __ldg(nrm + j0 + lane);      // |y_j|^2 of this chunk, one per lane
           uint32_t r[32];
           tmem_ld32(tbase + ch * 32, r);
-          const int j0 = c0 + ch * 32;
+          // fast reject in fp32: only dist <= key_val(tau) can enter (ties by index)
+          const float tf = (tau == kKeyMax) ? INFINITY : key_val(tau);
 #pragma unroll
           for (int t = 0; t < 32; ++t) {
-            const int j = j0 + t;
-            const float dist = __ldg(nrm + j) - 2.f * __uint_as_float(r[t]);
-            const u64 key = mkkey(dist, j);
-            if (qok && j < N && j != q && key < tau) rowbuf[cnt++] = key;
+            const float dist = fmaf(-2.f, __uint_as_float(r[t]), __shfl_sync(0xffffffffu, nv, t));
+            if (dist <= tf) {
+              const int j = j0 + t;
+              const u64 key = mkkey(dist, j);
+              if (qok && j < N && j != q && key < tau) rowbuf[cnt++] = key;
+            }
           }
         }
         tc_fence_before();
@@ -226,7 +254,7 @@ k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nr
           const int n = __shfl_sync(0xffffffffu, cnt, l);
           u64* rb_l = buf + ((size_t)blockIdx.x * TC_BM + e * 32 + l) * TC_CAP;
           u64 t;
-          const int keep = compact_keys(rb_l, n, Kc, mysort, lane, nullptr, t);
+          const int keep = reduce_keys(rb_l, n, Kc, TC_CAP - TC_BN, mysort, lane, t);
           if (lane == l) { cnt = keep; tau = t; }
         }
       }
@@ -238,7 +266,9 @@ k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nr
         const int n = __shfl_sync(0xffffffffu, cnt, l);
         u64* rb_l = buf + ((size_t)blockIdx.x * TC_BM + e * 32 + l) * TC_CAP;
         u64 t;
-        compact_keys(rb_l, n, Kc, mysort, lane, cand + (size_t)ql * Kc, t);
+        int nn = n;
+        if (nn > Kc + 64) nn = reduce_keys(rb_l, nn, Kc, 1 << 30, mysort, lane, t);
+        compact_keys(rb_l, nn, Kc, mysort, lane, cand + (size_t)ql * Kc, t);
       }
     }
   }
@@ -276,9 +306,15 @@ bool knn_tc_available() {
 
 size_t knn_tc_cap() { return TC_CAP; }
 
+size_t knn_tc_sync_words(int64_t N) {
+  const int64_t nrb = (N + TC_BM - 1) / TC_BM, nct = (N + TC_BN - 1) / TC_BN;
+  const int64_t waves = (nrb + kNumSMs - 1) / kNumSMs;
+  return (size_t)(waves * ((nct + TC_SYNC_EVERY - 1) / TC_SYNC_EVERY) + 1);
+}
+
 tsne_status launch_cand_tc(const __half* Xh, const float* nrm, int N, int Dp, int Kc,
                            unsigned long long* buf, unsigned long long* cand, int slots,
-                           cudaStream_t s) {
+                           unsigned* sync, cudaStream_t s) {
   if (!knn_tc_available()) {
     set_error("tcgen05 path unavailable (no sm_100 device or no cuTensorMapEncodeTiled)");
     return TSNE_ERR_CUDA;
@@ -301,7 +337,9 @@ tsne_status launch_cand_tc(const __half* Xh, const float* nrm, int N, int Dp, in
   int nrb = (N + TC_BM - 1) / TC_BM;
   int grid = nrb < kNumSMs ? nrb : kNumSMs;
   if (grid > slots) grid = slots;
-  k_cand_tc<<<grid, TC_THREADS, TC_SMEM, s>>>(map, nrm, N, Dp, Kc, buf, cand);
+  if (sync) TSNE_CUDA_TRY(cudaMemsetAsync(sync, 0, sizeof(unsigned) * knn_tc_sync_words(N), s));
+  k_cand_tc<<<grid, TC_THREADS, TC_SMEM, s>>>(map, nrm, N, Dp, Kc, buf, cand,
+                                               grid == kNumSMs ? sync : nullptr);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }

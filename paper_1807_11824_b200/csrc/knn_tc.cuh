@@ -8,5 +8,6 @@ namespace tsne {
 bool knn_tc_available();
 tsne_status launch_cand_tc(const __half* Xh, const float* nrm, int N, int Dp, int Kc,
                            unsigned long long* buf, unsigned long long* cand, int slots,
-                           cudaStream_t s);
+                           unsigned* sync, cudaStream_t s);
+size_t knn_tc_sync_words(int64_t N);
 }  // namespace tsne

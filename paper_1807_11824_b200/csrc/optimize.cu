@@ -6,14 +6,35 @@
 // whole run.
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "optimize.cuh"
 
 namespace tsne {
 
-void carve_opt(Carver& c, OptWS& o, int64_t N) {
+void carve_opt(Carver& c, OptWS& o, int64_t N, int64_t nnz) {
+  o.N = N;
+  o.nnz = nnz;
   o.t_dev = c.take<int32_t>(1);
   o.flag = c.take<int32_t>(1);
+  o.Ya = c.take<float2>(N);
   o.Yb = c.take<float2>(N);
+  o.V = c.take<float2>(N);
+  o.G = c.take<float2>(N);
+  o.tmp = c.take<float2>(2 * N);
+  o.lab = c.take<int32_t>(N);
+  o.lab2 = c.take<int32_t>(N);
+  o.inv = c.take<int32_t>(N);
+  for (int h = 0; h < 2; ++h) {
+    o.rp[h] = c.take<int64_t>(N + 1);
+    o.col[h] = c.take<int32_t>(nnz + 4);
+    o.val[h] = c.take<float>(nnz + 4);
+  }
+  o.len = c.take<int64_t>(N + 1);
+  size_t sb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, sb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(N + 1));
+  o.scan_tmp = c.take<char>(sb);
+  o.scan_tmp_bytes = sb;
 }
 
 __global__ void k_set_state(int32_t* t_dev, int32_t t0, int32_t* flag) {
@@ -21,7 +42,6 @@ __global__ void k_set_state(int32_t* t_dev, int32_t t0, int32_t* flag) {
   *flag = 0;
 }
 
-// the first iteration's box: bbox of Y with zero shift
 static tsne_status one_iteration(const int64_t* row_ptr, const int32_t* col, const float* val,
                                  int64_t N, float2* Yin, float2* Yout, float2* V, float2* G,
                                  float theta, const Sched& sc, TreeWS& w, OptWS& o,
@@ -33,74 +53,185 @@ static tsne_status one_iteration(const int64_t* row_ptr, const int32_t* col, con
   return launch_attract_update(row_ptr, col, val, Yin, N, w, o, sc, Yout, V, G, s);
 }
 
-__global__ void k_apply_shift(float2* Y, int N, const BoxInfo* box) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  float2 y = Y[i];
-  y.x = y.x - box->shift_x;
+// ---------------------------------------------------------------- relabelling
+// new label k <- old label perm[k]: state gathered, P rows permuted and their
+// columns mapped through the inverse permutation (entry order kept).
+__global__ void k_perm_state(const int32_t* __restrict__ perm, int N, const float2* __restrict__ Ys,
+                             const float2* __restrict__ Vs, const float2* __restrict__ Gs,
+                             const int32_t* __restrict__ lab, const int64_t* __restrict__ rp,
+                             float2* __restrict__ Yd, float2* __restrict__ Vd,
+                             float2* __restrict__ Gd, int32_t* __restrict__ lab2,
+                             int32_t* __restrict__ inv, int64_t* __restrict__ len) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > N) return;
+  if (k == N) { len[N] = 0; return; }
+  const int o = perm ? perm[k] : k;
+  Yd[k] = Ys[o];
+  Vd[k] = Vs[o];
+  Gd[k] = Gs[o];
+  lab2[k] = lab ? lab[o] : o;
+  inv[o] = k;
+  len[k] = rp[o + 1] - rp[o];
+}
+
+__global__ void k_relabel_rows(const int32_t* __restrict__ perm, int N,
+                               const int64_t* __restrict__ rp_old, const int32_t* __restrict__ col_old,
+                               const float* __restrict__ val_old, const int32_t* __restrict__ inv,
+                               const int64_t* __restrict__ rp_new, int32_t* __restrict__ col_new,
+                               float* __restrict__ val_new) {
+  const int lane = threadIdx.x & 31;
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (k >= N) return;
+  const int o = perm ? perm[k] : k;
+  const int64_t e0 = rp_old[o], e1 = rp_old[o + 1], d0 = rp_new[k];
+  for (int64_t e = e0 + lane; e < e1; e += 32) {
+    col_new[d0 + (e - e0)] = inv[__ldcs(col_old + e)];
+    val_new[d0 + (e - e0)] = __ldcs(val_old + e);
+  }
+}
+
+__global__ void k_scatter_out(int N, const int32_t* __restrict__ lab, const float2* __restrict__ Y,
+                              const float2* __restrict__ V, const float2* __restrict__ G,
+                              const BoxInfo* __restrict__ box, float2* __restrict__ Yu,
+                              float2* __restrict__ Vu, float2* __restrict__ Gu) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const int o = lab[k];
+  float2 y = Y[k];
+  y.x = y.x - box->shift_x;            // the last update's pending recentring
   y.y = y.y - box->shift_y;
-  Y[i] = y;
+  Yu[o] = y;
+  Vu[o] = V[k];
+  Gu[o] = G[k];
+}
+
+// Relabel (src P, src state, src lab) -> (P half `dst`, o.Ya/o.V/o.G, o.lab).
+static tsne_status relabel(const int32_t* perm, int N, const int64_t* rp, const int32_t* col,
+                           const float* val, const float2* Ys, const float2* Vs, const float2* Gs,
+                           const int32_t* lab, int dst, OptWS& o, cudaStream_t s) {
+  float2* Yn = o.Yb;          // free at iteration boundaries
+  float2* Vn = o.tmp;
+  float2* Gn = o.tmp + N;
+  k_perm_state<<<(N + 256) / 256, 256, 0, s>>>(perm, N, Ys, Vs, Gs, lab, rp, Yn, Vn, Gn, o.lab2,
+                                                o.inv, o.len);
+  TSNE_LAUNCH_CHECK();
+  size_t sb = o.scan_tmp_bytes;
+  TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveSum(o.scan_tmp, sb, o.len, o.rp[dst], N + 1, s));
+  k_relabel_rows<<<(int)(((int64_t)N * 32 + 255) / 256), 256, 0, s>>>(
+      perm, N, rp, col, val, o.inv, o.rp[dst], o.col[dst], o.val[dst]);
+  TSNE_LAUNCH_CHECK();
+  TSNE_CUDA_TRY(cudaMemcpyAsync(o.Ya, Yn, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
+  TSNE_CUDA_TRY(cudaMemcpyAsync(o.V, Vn, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
+  TSNE_CUDA_TRY(cudaMemcpyAsync(o.G, Gn, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
+  TSNE_CUDA_TRY(cudaMemcpyAsync(o.lab, o.lab2, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s));
+  return TSNE_OK;
+}
+
+// Enter the internal label space: Morton order of the caller's Y.
+static tsne_status enter(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t N,
+                         float2* Y, float2* V, float2* G, int32_t t0, TreeWS& w, OptWS& o,
+                         bool morton, cudaStream_t s) {
+  k_set_state<<<1, 1, 0, s>>>(o.t_dev, t0, o.flag);
+  TSNE_LAUNCH_CHECK();
+  tsne_status st = launch_bbox(w, Y, s);
+  if (st != TSNE_OK) return st;
+  const int32_t* perm = nullptr;
+  if (morton) {
+    if ((st = build_tree(w, Y, /*apply_shift=*/false, s)) != TSNE_OK) return st;
+    perm = w.perm;
+  }
+  return relabel(perm, (int)N, row_ptr, col, val, Y, V, G, nullptr, 0, o, s);
+}
+
+static tsne_status leave(int64_t N, const float2* Ycur, float2* Y, float2* V, float2* G, TreeWS& w,
+                         OptWS& o, cudaStream_t s) {
+  k_scatter_out<<<(int)((N + 255) / 256), 256, 0, s>>>((int)N, o.lab, Ycur, o.V, o.G, w.box, Y, V,
+                                                       G);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
+struct Graph {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t e = nullptr;
+  ~Graph() {
+    if (e) cudaGraphExecDestroy(e);
+    if (g) cudaGraphDestroy(g);
+  }
+};
+
+// two iterations Ya -> Yb -> Ya with P half h
+static tsne_status capture_pair(Graph& gr, int h, int64_t N, float theta, const Sched& sc,
+                                TreeWS& w, OptWS& o, cudaStream_t s) {
+  TSNE_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  tsne_status s1 = one_iteration(o.rp[h], o.col[h], o.val[h], N, o.Ya, o.Yb, o.V, o.G, theta, sc,
+                                 w, o, s);
+  tsne_status s2 = (s1 == TSNE_OK) ? one_iteration(o.rp[h], o.col[h], o.val[h], N, o.Yb, o.Ya,
+                                                   o.V, o.G, theta, sc, w, o, s)
+                                   : s1;
+  cudaError_t ce = cudaStreamEndCapture(s, &gr.g);
+  if (s1 != TSNE_OK) return s1;
+  if (s2 != TSNE_OK) return s2;
+  TSNE_CUDA_TRY(ce);
+  TSNE_CUDA_TRY(cudaGraphInstantiate(&gr.e, gr.g, 0));
+  return TSNE_OK;
 }
 
 tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                            int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t n_iter,
-                           float theta, const Sched& sc, bool use_graphs, TreeWS& w, OptWS& o,
-                           cudaStream_t s) {
-  k_set_state<<<1, 1, 0, s>>>(o.t_dev, t0, o.flag);
-  TSNE_LAUNCH_CHECK();
-  tsne_status st = launch_bbox(w, Y, s);   // shift = 0 for the first iteration
+                           float theta, const Sched& sc, bool use_graphs, int relabel_every,
+                           TreeWS& w, OptWS& o, cudaStream_t s) {
+  tsne_status st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, relabel_every > 0, s);
   if (st != TSNE_OK) return st;
-  int32_t done = 0;
-  float2* a = Y;
-  float2* b = o.Yb;
-  // graphs need a non-default stream for capture
-  bool graphs = use_graphs && s != nullptr && n_iter >= 4;
+  int h = 0;                                   // P half in use
+  const bool graphs = use_graphs && s != nullptr && n_iter >= 4;
+  Graph gr[2];
   if (graphs) {
-    cudaGraph_t g = nullptr;
-    cudaGraphExec_t ge = nullptr;
-    TSNE_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    tsne_status s1 = one_iteration(row_ptr, col, val, N, a, b, V, G, theta, sc, w, o, s);
-    tsne_status s2 = (s1 == TSNE_OK)
-                         ? one_iteration(row_ptr, col, val, N, b, a, V, G, theta, sc, w, o, s)
-                         : s1;
-    cudaError_t ce = cudaStreamEndCapture(s, &g);
-    if (s1 != TSNE_OK || s2 != TSNE_OK) {
-      if (g) cudaGraphDestroy(g);
-      return s1 != TSNE_OK ? s1 : s2;
-    }
-    TSNE_CUDA_TRY(ce);
-    TSNE_CUDA_TRY(cudaGraphInstantiate(&ge, g, 0));
-    for (; done + 2 <= n_iter; done += 2) {
-      cudaError_t e = cudaGraphLaunch(ge, s);
-      if (e != cudaSuccess) {
-        cudaGraphExecDestroy(ge);
-        cudaGraphDestroy(g);
-        TSNE_CUDA_TRY(e);
-      }
-    }
-    cudaGraphExecDestroy(ge);
-    cudaGraphDestroy(g);
+    if ((st = capture_pair(gr[0], 0, N, theta, sc, w, o, s)) != TSNE_OK) return st;
+    if (relabel_every > 0 && n_iter > relabel_every &&
+        (st = capture_pair(gr[1], 1, N, theta, sc, w, o, s)) != TSNE_OK)
+      return st;
   }
-  for (; done < n_iter; ++done) {
-    st = one_iteration(row_ptr, col, val, N, a, b, V, G, theta, sc, w, o, s);
-    if (st != TSNE_OK) return st;
-    float2* t = a; a = b; b = t;
+  const int period = relabel_every > 0 ? ((relabel_every + 1) & ~1) : n_iter;
+  int32_t done = 0;
+  float2* cur = o.Ya;
+  while (done < n_iter) {
+    const int chunk = (n_iter - done) < period ? (n_iter - done) : period;
+    int c = 0;
+    if (graphs)
+      for (; c + 2 <= chunk; c += 2) TSNE_CUDA_TRY(cudaGraphLaunch(gr[h].e, s));
+    for (; c < chunk; ++c) {
+      float2* a = (c % 2 == 0) ? o.Ya : o.Yb;
+      float2* b = (c % 2 == 0) ? o.Yb : o.Ya;
+      if ((st = one_iteration(o.rp[h], o.col[h], o.val[h], N, a, b, o.V, o.G, theta, sc, w, o,
+                              s)) != TSNE_OK)
+        return st;
+    }
+    cur = (chunk % 2 == 0) ? o.Ya : o.Yb;
+    done += chunk;
+    if (done < n_iter) {
+      // chunks are even, so the state is in Ya; w.perm is the Morton order of
+      // the last iteration's embedding (a permutation of the current labels).
+      // The pending recentring shift is uniform, so it commutes with relabelling.
+      if ((st = relabel(w.perm, (int)N, o.rp[h], o.col[h], o.val[h], o.Ya, o.V, o.G, o.lab, 1 - h,
+                        o, s)) != TSNE_OK)
+        return st;
+      h = 1 - h;
+    }
   }
-  // the last update left its recentring pending: apply it
-  k_apply_shift<<<(int)((N + 255) / 256), 256, 0, s>>>(a, (int)N, w.box);
-  TSNE_LAUNCH_CHECK();
-  if (a != Y) TSNE_CUDA_TRY(cudaMemcpyAsync(Y, a, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
-  return TSNE_OK;
+  return leave(N, cur, Y, V, G, w, o, s);
 }
 
 tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                                int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t reps,
                                float theta, const Sched& sc, TreeWS& w, OptWS& o, double* stage_ms,
                                int32_t* kernels, cudaStream_t s) {
+  tsne_status st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, true, s);
+  if (st != TSNE_OK) return st;
   if (kernels) {  // count kernel nodes of one captured (never launched) iteration
     cudaGraph_t g = nullptr;
     TSNE_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    tsne_status st = one_iteration(row_ptr, col, val, N, Y, o.Yb, V, G, theta, sc, w, o, s);
+    st = one_iteration(o.rp[0], o.col[0], o.val[0], N, o.Ya, o.Yb, o.V, o.G, theta, sc, w, o, s);
     cudaError_t ce = cudaStreamEndCapture(s, &g);
     if (st != TSNE_OK) { if (g) cudaGraphDestroy(g); return st; }
     TSNE_CUDA_TRY(ce);
@@ -117,14 +248,10 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
     *kernels = k;
     cudaGraphDestroy(g);
   }
-  k_set_state<<<1, 1, 0, s>>>(o.t_dev, t0, o.flag);
-  TSNE_LAUNCH_CHECK();
-  tsne_status st = launch_bbox(w, Y, s);
-  if (st != TSNE_OK) return st;
   cudaEvent_t e[4];
   for (auto& x : e) cudaEventCreate(&x);
   double acc[3] = {0, 0, 0};
-  float2* a = Y;
+  float2* a = o.Ya;
   float2* b = o.Yb;
   for (int r = 0; r < reps && st == TSNE_OK; ++r) {
     cudaEventRecord(e[0], s);
@@ -132,7 +259,8 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
     cudaEventRecord(e[1], s);
     if (st == TSNE_OK) st = launch_traverse(w, theta, s);
     cudaEventRecord(e[2], s);
-    if (st == TSNE_OK) st = launch_attract_update(row_ptr, col, val, a, N, w, o, sc, b, V, G, s);
+    if (st == TSNE_OK)
+      st = launch_attract_update(o.rp[0], o.col[0], o.val[0], a, N, w, o, sc, b, o.V, o.G, s);
     cudaEventRecord(e[3], s);
     cudaEventSynchronize(e[3]);
     for (int k = 0; k < 3; ++k) {
@@ -145,9 +273,7 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
   for (auto& x : e) cudaEventDestroy(x);
   if (st != TSNE_OK) return st;
   for (int k = 0; k < 3; ++k) stage_ms[k] = reps > 0 ? acc[k] / reps : 0.0;
-  k_apply_shift<<<(int)((N + 255) / 256), 256, 0, s>>>(a, (int)N, w.box);
-  TSNE_LAUNCH_CHECK();
-  if (a != Y) TSNE_CUDA_TRY(cudaMemcpyAsync(Y, a, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
+  if ((st = leave(N, a, Y, V, G, w, o, s)) != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaStreamSynchronize(s));
   return TSNE_OK;
 }

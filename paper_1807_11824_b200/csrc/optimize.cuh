@@ -10,13 +10,27 @@ struct Sched {
   float exag, mom0, mom1, eta, min_gain;
 };
 
+// Internal optimiser state.  Points are periodically relabelled into the
+// Morton order of the current embedding (locality of the y_j gathers of the
+// attractive pass and of the tree build); `lab[k]` is the caller's index of
+// internal point k, and P is kept in internal labels (two CSR copies A/B).
 struct OptWS {
+  int64_t N = 0, nnz = 0;
   int32_t* t_dev = nullptr;   // iteration counter read by the update kernel
   int32_t* flag = nullptr;    // non-finite sentinel
-  float2* Yb = nullptr;       // second embedding buffer (double buffering)
+  float2 *Ya = nullptr, *Yb = nullptr;   // embedding (double buffer of the update)
+  float2 *V = nullptr, *G = nullptr;     // velocity, gains
+  float2* tmp = nullptr;                 // permutation scratch
+  int32_t *lab = nullptr, *lab2 = nullptr, *inv = nullptr;
+  int64_t* rp[2] = {nullptr, nullptr};
+  int32_t* col[2] = {nullptr, nullptr};
+  float* val[2] = {nullptr, nullptr};
+  int64_t* len = nullptr;                // N+1 row lengths -> scanned row_ptr
+  void* scan_tmp = nullptr;
+  size_t scan_tmp_bytes = 0;
 };
 
-void carve_opt(Carver& c, OptWS& o, int64_t N);
+void carve_opt(Carver& c, OptWS& o, int64_t N, int64_t nnz);
 
 int attract_blocks(int64_t N);
 tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, const float* val,
@@ -27,11 +41,12 @@ tsne_status launch_attract_update(const int64_t* row_ptr, const int32_t* col, co
                                   const Sched& sc, float2* Yout, float2* V, float2* G,
                                   cudaStream_t s);
 
-// Runs n_iter iterations from state (Y, V, G) starting at iteration t0.
+// Runs n_iter iterations from the caller's state (Y, V, G) starting at t0.
+// relabel_every: period of the Morton relabelling (0 = never).
 tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                            int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t n_iter,
-                           float theta, const Sched& sc, bool use_graphs, TreeWS& w, OptWS& o,
-                           cudaStream_t s);
+                           float theta, const Sched& sc, bool use_graphs, int relabel_every,
+                           TreeWS& w, OptWS& o, cudaStream_t s);
 
 tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                                int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t reps,

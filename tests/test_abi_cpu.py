@@ -40,7 +40,7 @@ def test_abi_version_and_defaults(L):
     import paper_1807_11824_b200 as T
     assert L.tsne_abi_version() >> 16 == 1
     cfg = T.default_config()
-    assert (cfg.exag_iters, cfg.seed, cfg.use_graphs) == (250, 42, 1)
+    assert (cfg.exag_iters, cfg.seed, cfg.use_graphs, cfg.relabel_every) == (250, 42, 1, 64)
     assert abs(cfg.mom0 - 0.5) < 1e-7 and abs(cfg.mom1 - 0.8) < 1e-7
 
 
@@ -51,7 +51,7 @@ def test_workspace_sizes_monotone(L):
     assert L.tsne_gradient_workspace_size(1) == 0
     assert L.tsne_knn_workspace_size(5000, 784, 90) > 5000 * 784 * 2
     assert L.tsne_compute_p_workspace_size(5000, 90) > 2 * 5000 * 90 * 16
-    assert L.tsne_optimize_workspace_size(5000) > L.tsne_gradient_workspace_size(5000)
+    assert L.tsne_optimize_workspace_size(5000, 700000) > L.tsne_gradient_workspace_size(5000)
 
 
 def test_argument_validation_without_device(L):
