@@ -35,7 +35,10 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            const int32_t* __restrict__ leafnode, const int32_t* __restrict__ perm,
            const int32_t* __restrict__ nnodes_p, int N, const BoxInfo* __restrict__ box,
            float theta, float2* __restrict__ rep, double* __restrict__ zpart,
-           unsigned* __restrict__ counter, double* __restrict__ Zout) {
+           unsigned* __restrict__ counter, double* __restrict__ Zout,
+           const int32_t* __restrict__ list, const int32_t* __restrict__ nlist, int row0) {
+  // list (multi-GPU): the sorted positions of the points this rank owns
+  // (original indices [row0, ...)); rep is then indexed by perm[k] - row0.
   // per level l: {r^2 (fp32), margin constant A_l, margin slope B_l}, r^2 (fp64)
   __shared__ float4 s_lv[18];
   __shared__ double s_r2d[18];
@@ -61,8 +64,9 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   if (threadIdx.x == 0) s_done = 0;
   __syncthreads();
   const int nnodes = *nnodes_p;
-  const int k = blockIdx.x * kTravThreads + threadIdx.x;
-  const bool active = k < N;
+  const int tid = blockIdx.x * kTravThreads + threadIdx.x;
+  const bool active = tid < (list ? *nlist : N);
+  const int k = active ? (list ? list[tid] : tid) : 0;
   int cur = active ? 0 : nnodes;
   const float2 yi = active ? ys[k] : make_float2(0.f, 0.f);
   const int Li = active ? leafnode[k] : -1;
@@ -128,7 +132,7 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
     }
     cur = next;
   }
-  if (active) rep[perm[k]] = make_float2(fx, fy);
+  if (active) rep[perm[k] - row0] = make_float2(fx, fy);
 
   // Z: fixed-order fp64 reduction without a block barrier: the last warp of
   // the block to finish sums the block, the last block sums the blocks.
@@ -167,7 +171,18 @@ tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s) {
   const int N = (int)w.N;
   k_traverse<<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
-      w.zpart, w.counter + 1, w.Z);
+      w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
+// multi-GPU: traverse only the listed sorted positions (owned points)
+tsne_status launch_traverse_list(TreeWS& w, float theta, const int32_t* list, const int32_t* nlist,
+                                 int row0, float2* rep_local, double* z_partial, cudaStream_t s) {
+  const int N = (int)w.N;
+  k_traverse<<<traverse_blocks(N), kTravThreads, 0, s>>>(
+      w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta,
+      rep_local, w.zpart, w.counter + 1, z_partial, list, nlist, row0);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }

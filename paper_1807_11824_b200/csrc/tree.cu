@@ -139,6 +139,73 @@ tsne_status launch_bbox(TreeWS& w, const float2* Y, cudaStream_t s) {
   return TSNE_OK;
 }
 
+// Bounding box and recentring shift of Y (multi-GPU path: the replicated
+// embedding is recentred at the start of each rank's iteration, D15).
+__global__ void __launch_bounds__(kBoxThreads) k_bbox_mean(const float2* __restrict__ Y, int N,
+                                                           float4* part, double2* part2,
+                                                           unsigned* counter, BoxInfo* box) {
+  float mnx = INFINITY, mxx = -INFINITY, mny = INFINITY, mxy = -INFINITY;
+  double sx = 0.0, sy = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    float2 y = Y[i];
+    mnx = fminf(mnx, y.x); mxx = fmaxf(mxx, y.x);
+    mny = fminf(mny, y.y); mxy = fmaxf(mxy, y.y);
+    sx += (double)y.x; sy += (double)y.y;
+  }
+  mnx = warp_min(mnx); mxx = warp_max(mxx); mny = warp_min(mny); mxy = warp_max(mxy);
+  sx = warp_sum(sx); sy = warp_sum(sy);
+  __shared__ float4 sw[kBoxThreads / 32];
+  __shared__ double2 ss[kBoxThreads / 32];
+  __shared__ bool last;
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { sw[wid] = make_float4(mnx, mxx, mny, mxy); ss[wid] = make_double2(sx, sy); }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float4 r = sw[0];
+    double2 q2 = ss[0];
+    for (int k = 1; k < kBoxThreads / 32; ++k) {
+      r.x = fminf(r.x, sw[k].x); r.y = fmaxf(r.y, sw[k].y);
+      r.z = fminf(r.z, sw[k].z); r.w = fmaxf(r.w, sw[k].w);
+      q2.x += ss[k].x; q2.y += ss[k].y;
+    }
+    part[blockIdx.x] = r;
+    part2[blockIdx.x] = q2;
+    __threadfence();
+    unsigned t = atomicAdd(counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    float4 r = __ldcg(part);
+    double2 q2 = __ldcg(part2);
+    for (int k = 1; k < (int)gridDim.x; ++k) {
+      float4 q = __ldcg(part + k);
+      double2 a = __ldcg(part2 + k);
+      r.x = fminf(r.x, q.x); r.y = fmaxf(r.y, q.y);
+      r.z = fminf(r.z, q.z); r.w = fmaxf(r.w, q.w);
+      q2.x += a.x; q2.y += a.y;
+    }
+    const float mx = (float)(q2.x / (double)N), my = (float)(q2.y / (double)N);
+    BoxInfo b;
+    make_root_box(r.x - mx, r.y - mx, r.z - my, r.w - my, &b);   // monotone rounding
+    b.shift_x = mx;
+    b.shift_y = my;
+    b.pad0 = 0.f;
+    *box = b;
+    *counter = 0u;
+  }
+}
+
+tsne_status launch_bbox_mean(TreeWS& w, const float2* Y, cudaStream_t s) {
+  int blocks = (int)((w.N + 4 * kBoxThreads - 1) / (4 * kBoxThreads));
+  if (blocks > 2 * kNumSMs) blocks = 2 * kNumSMs;
+  if (blocks < 1) blocks = 1;
+  k_bbox_mean<<<blocks, kBoxThreads, 0, s>>>(Y, (int)w.N, w.part4, w.part2, w.counter + 3, w.box);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
 // ---------------------------------------------------------------- H2 keys
 __device__ __forceinline__ uint32_t spread16(uint32_t x) {
   x = (x | (x << 8)) & 0x00FF00FFu;

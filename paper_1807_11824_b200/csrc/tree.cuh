@@ -80,6 +80,10 @@ tsne_status launch_bbox(TreeWS& w, const float2* Y, cudaStream_t s);
 tsne_status build_tree(TreeWS& w, float2* Y, bool apply_shift, cudaStream_t s);
 // Repulsive pass: w.rep, w.Z
 tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s);
+tsne_status launch_traverse_list(TreeWS& w, float theta, const int32_t* list, const int32_t* nlist,
+                                 int row0, float2* rep_local, double* z_partial, cudaStream_t s);
+// Bounding box + recentring shift (fp64 mean, fixed order) of Y, into w.box.
+tsne_status launch_bbox_mean(TreeWS& w, const float2* Y, cudaStream_t s);
 
 int traverse_blocks(int64_t N);
 

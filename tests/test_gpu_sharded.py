@@ -1,0 +1,99 @@
+"""Multi-GPU kernels on one GPU: G 'virtual shards' driven in one process
+(the exchanges done by hand in rank order), and a world_size-1 NCCL run of
+ShardedOptimizer, against the single-GPU optimiser and the oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    import paper_1807_11824_b200 as T
+    T.lib()
+    return T
+
+
+@pytest.fixture(scope="module")
+def prob(orc):
+    X = synth.make_x("C1", n=2000).numpy()
+    idx, d2 = orc.knn(X, 90)
+    rp, col, v64, v32, *_ = orc.compute_p(idx, d2, 30.0)
+    return rp, col, v32
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("G", [1, 3])
+def test_virtual_shards_match_single_gpu(T, orc, prob, G):
+    from paper_1807_11824_b200.sharded import GpuShardOps, local_csr, shard_range
+    rp, col, v32 = prob
+    dev = torch.device("cuda")
+    N = len(rp) - 1
+    Y0 = T.init_y(N, 42)
+    rp_d, col_d, val_d = (torch.as_tensor(a, device=dev) for a in (rp, col, v32))
+    ops = GpuShardOps(N, dev)
+    cfg = T.default_config()
+    shards = []
+    for r in range(G):
+        a, b, S = shard_range(N, G, r)
+        shards.append((a, b, *local_csr(rp_d, col_d, val_d, a, b),
+                       torch.zeros(b - a, 2, device=dev), torch.ones(b - a, 2, device=dev),
+                       torch.zeros(b - a, 2, device=dev)))
+    Y = Y0.clone()
+    zp = torch.zeros(G * 2, dtype=torch.float64, device=dev)
+    n_iter = 3        # trajectories diverge chaotically; compare a few iterations
+    for t in range(n_iter):
+        for r, (a, b, rpl, cl, vl, v, g, rep) in enumerate(shards):
+            ops.forces(Y, N, a, b, 0.5, t > 0, rep, zp[2 * r:2 * r + 2])
+        Ynew = torch.empty_like(Y)
+        for r, (a, b, rpl, cl, vl, v, g, rep) in enumerate(shards):
+            out = torch.empty(b - a, 2, device=dev)
+            ops.update(rpl, cl, vl, N, a, b, Y, rep, zp, G, t, 200.0, 12.0, cfg, v, g, out)
+            Ynew[a:b] = out
+        Y = Ynew
+    ops.recentre(Y, N)
+    assert not ops.nonfinite()
+    ref = T.Optimizer(rp_d, col_d, val_d, Y0, theta=0.5, relabel_every=0, use_graphs=False)
+    Yref = ref.step(n_iter)
+    assert rel(Y.cpu().numpy(), Yref.cpu().numpy().astype(np.float64)) < 1e-4
+    Yo, _, _ = orc.optimize(rp, col, v32, Y0.cpu().numpy().astype(np.float64), n_iter=1, theta=0.5)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_nccl_world1_sharded_optimizer(T, prob):
+    from paper_1807_11824_b200.sharded import ShardedOptimizer, local_csr
+    rp, col, v32 = prob
+    dev = torch.device("cuda")
+    N = len(rp) - 1
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        rp_d, col_d, val_d = (torch.as_tensor(a, device=dev) for a in (rp, col, v32))
+        Y0 = T.init_y(N, 7)
+        opt = ShardedOptimizer(*local_csr(rp_d, col_d, val_d, 0, N), Y0, theta=0.5)
+        opt.step(3)
+        Y = opt.embedding()
+        ref = T.Optimizer(rp_d, col_d, val_d, Y0, theta=0.5, relabel_every=0, use_graphs=False)
+        Yref = ref.step(3)
+        assert torch.isfinite(Y).all()
+        assert rel(Y.cpu().numpy(), Yref.cpu().numpy().astype(np.float64)) < 1e-4
+    finally:
+        dist.destroy_process_group()
