@@ -29,7 +29,17 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-__global__ void __launch_bounds__(kTravThreads)
+// the rare fp64 re-test of the criterion (D25), kept out of line so the hot
+// loop does not issue its predicated-off instructions
+__device__ __noinline__ bool accept_fp64(const double2* __restrict__ c64, float2 yi, double r2,
+                                         double theta2d) {
+  const double2 c = *c64;
+  const double ex = __dsub_rn((double)yi.x, c.x), ey = __dsub_rn((double)yi.y, c.y);
+  const double D2d = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
+  return r2 < __dmul_rn(theta2d, D2d);
+}
+
+__global__ void __launch_bounds__(kTravThreads, 4)
 k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            const double2* __restrict__ com64, const float2* __restrict__ ys,
            const int32_t* __restrict__ leafnode, const int32_t* __restrict__ perm,
@@ -73,64 +83,53 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   float fx = 0.f, fy = 0.f;
   double z = 0.0;   // fp64: Z sums up to N^2 terms of very different size
 
+  const uint32_t lv_base = (uint32_t)__cvta_generic_to_shared(s_lv);
   while (cur < nnodes) {
     const float4 nd = __ldg(nodes + cur);
-    const uint32_t wv = __float_as_uint(nd.z);
-    const int cnt = (int)(wv & kCountMask);
-    const int lvl = (int)(wv >> 27);
-    const int skip = __float_as_int(nd.w);
-    const bool self_in = (Li >= cur) && (Li < skip);
+    const uint32_t sw = __float_as_uint(nd.w);
+    const int lvl = (int)(sw >> 27);
+    const int skip = (int)(sw & kSkipMask);
+    const float cntf = nd.z;
+    const bool self_in = (unsigned)(Li - cur) < (unsigned)(skip - cur);   // Li in [cur, skip)
     const float dx = yi.x - nd.x, dy = yi.y - nd.y;
     const float D2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-    int next = skip;
-    bool take, bucket = false;
-    if (lvl == kLevelLeaf) {                       // exact leaf
-      take = (cnt == 1) && !self_in;               // one point: the exact pair
-      bucket = cnt > 1;
-    } else if (self_in) {                          // the cell contains i (D11)
-      take = false;
-      if (lvl == kLevelBucketTest) bucket = true; else next = cur + 1;
-    } else {
-      const float4 lv = s_lv[lvl];
-      const float lhs = __fmul_rn(theta2, D2);
-      const float diff = lhs - lv.x;
-      const float marg = fmaf(lv.z, lhs, lv.y);
-      if (diff > marg) {
-        take = true;
-      } else if (diff < -marg) {
-        take = false;
-      } else {                                     // fp64 re-test (D25)
-        const double2 c = com64[cur];
-        const double ex = __dsub_rn((double)yi.x, c.x), ey = __dsub_rn((double)yi.y, c.y);
-        const double D2d = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
-        take = s_r2d[lvl] < __dmul_rn(theta2d, D2d);
-      }
-      if (!take) {
-        if (lvl == kLevelBucketTest) bucket = true; else next = cur + 1;
-      }
-    }
-    if (take) {
-      const float w = rcp_approx(1.f + D2);
-      const float nw = (float)cnt * w;
-      z += (double)nw;
-      const float nww = nw * w;
-      fx = fmaf(nww, dx, fx);
-      fy = fmaf(nww, dy, fy);
-    }
+    const bool leaf = lvl == kLevelLeaf;
+    float4 lv;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(lv.x), "=f"(lv.y), "=f"(lv.z), "=f"(lv.w) : "r"(lv_base + 16u * lvl));
+    // criterion (D10) in fp32 with the D25 margin
+    const float lhs = __fmul_rn(theta2, D2);
+    const float diff = lhs - lv.x;
+    const float marg = fmaf(lv.z, lhs, lv.y);
+    bool acc = diff > marg;
+    if (!leaf && !self_in && fabsf(diff) <= marg)     // inside the band: decide in fp64
+      acc = accept_fp64(com64 + cur, yi, s_r2d[lvl], theta2d);
+    // exact leaf of one point: the exact pair; internal cell: the criterion;
+    // a cell containing i is opened (D11)
+    const bool take = !self_in && (leaf ? cntf == 1.f : acc);
+    const bool bucket = !take && (leaf ? cntf > 1.f : lvl == kLevelBucketTest);
+    const int node = cur;
+    cur = (take || leaf || bucket) ? skip : cur + 1;
+    const float w = rcp_approx(1.f + D2);
+    const float nw = take ? cntf * w : 0.f;
+    z += (double)nw;
+    const float nww = nw * w;
+    fx = fmaf(nww, dx, fx);
+    fy = fmaf(nww, dy, fy);
     if (bucket) {                                  // coincident points: exact pairs
-      const int s0 = nfirst[cur];
+      const int s0 = nfirst[node];
+      const int cnt = (int)cntf;
       for (int m = s0; m < s0 + cnt; ++m) {
         if (m == k) continue;
         const float2 yj = ys[m];
         const float ex = yi.x - yj.x, ey = yi.y - yj.y;
-        const float w = rcp_approx(1.f + ex * ex + ey * ey);
-        z += (double)w;
-        const float ww = w * w;
+        const float wj = rcp_approx(1.f + ex * ex + ey * ey);
+        z += (double)wj;
+        const float ww = wj * wj;
         fx = fmaf(ww, ex, fx);
         fy = fmaf(ww, ey, fy);
       }
     }
-    cur = next;
   }
   if (active) rep[perm[k] - row0] = make_float2(fx, fy);
 

@@ -378,8 +378,8 @@ __global__ void k_quad_emit(int N, const int32_t* __restrict__ bfirst,
     if (level >= kLevelLeaf)
       for (int k = s; k <= e; ++k) leafnode[k] = pre;
   }
-  nodes[pre] = make_float4(cxf, cyf, __uint_as_float(count | ((uint32_t)level << 27)),
-                           __int_as_float(skip));
+  nodes[pre] = make_float4(cxf, cyf, (float)count,
+                           __uint_as_float((uint32_t)skip | ((uint32_t)level << 27)));
   nfirst[pre] = s;
   com64[pre] = c64;
 }

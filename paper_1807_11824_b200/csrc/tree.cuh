@@ -4,7 +4,7 @@
 // "insert", "number of points in each internal cell"), centres of mass.
 //
 // Node layout: one pre-order array of 16-byte hot
-// records {com_x, com_y, count | level << 27, skip}; the first child of
+// records {com_x, com_y, (float) count, skip | level << 27}; the first child of
 // node k is k + 1 and `skip` is the first node after k's subtree, so a
 // traversal needs no stack.  Cold arrays: range start (`nfirst`, used by
 // bucket leaves) and the fp64 centre of mass (`com64`, read only inside the
@@ -31,7 +31,7 @@ struct BoxInfo {
 
 constexpr int kLevelLeaf = 16;
 constexpr int kLevelBucketTest = 17;
-constexpr uint32_t kCountMask = (1u << 27) - 1u;
+constexpr uint32_t kSkipMask = (1u << 27) - 1u;
 constexpr int kMaxParts = 4096;
 constexpr double kFixScale = 274877906944.0;  // 2^38: fixed-point COM sums
 
