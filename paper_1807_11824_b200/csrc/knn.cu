@@ -32,8 +32,11 @@ static inline int kc_of(int64_t N, int K) {
 
 int knn_slots(int64_t N) {
   int64_t rb = (N + kKnnBM - 1) / kKnnBM;
+  rb = (rb + 1) & ~int64_t(1);               // CTA pairs need an even count
   int64_t cap = 2 * kNumSMs;
   return (int)(rb < cap ? rb : cap);
+
+
 }
 
 void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K) {
@@ -51,7 +54,8 @@ void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K) {
   w.cand = c.take<u64>((size_t)N * w.Kc);
   w.uncert = c.take<u64>(2);
   w.rows_bad = c.take<int32_t>(N);
-  w.sync = c.take<unsigned>(knn_tc_sync_words(N));
+  w.sync = c.take<unsigned>(knn_tc_sync_words(N) > knn_tc2_sync_words(N) ? knn_tc_sync_words(N)
+                                                                           : knn_tc2_sync_words(N));
 }
 
 // ---------------------------------------------------------------- prep

@@ -15,8 +15,12 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "knn_select.cuh"
 #include "knn_tc.cuh"
+#include "tc_ptx.cuh"
 
 namespace tsne {
 
@@ -32,83 +36,6 @@ constexpr uint32_t TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;  // 48 KB
 constexpr uint32_t TC_IDESC = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) |
                               ((uint32_t)(TC_BM >> 4) << 24);
 constexpr size_t TC_SMEM = 1024 + TC_STAGES * TC_STAGE_BYTES + 256 + 4 * TC_CAP * 8;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
-}
-// try_wait with a suspend-time hint: a waiting thread sleeps instead of
-// spinning, so the producer / MMA threads do not steal issue slots from the
-// epilogue warps sharing their SM sub-partition.
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 1000000;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n\t"
-      "DONE_%=:\n\t}" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
-      : "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-// K-major operand in 128-byte-swizzled smem: rows of 128 B, 8-row atoms
-// 1024 B apart (SBO), descriptor version 1 (sm_100), layout SWIZZLE_128B (2)
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |
-         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                        uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-        "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nrm, int N, int Dp,
@@ -180,7 +107,8 @@ k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nr
         }
     }
   } else if (warp == 1) {
-    if (lane == 0) {                                             // ---- MMA issuer
+    {                                                            // ---- MMA issuer
+      const uint64_t da0 = sw128_desc(smem_u32(base)), db0 = sw128_desc(smem_u32(base) + TC_A_BYTES);
       int stage = 0;
       uint32_t phase = 0, aphase = 0;
       int acc = 0;
@@ -192,16 +120,18 @@ k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nr
           for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t sa = smem_u32(base + stage * TC_STAGE_BYTES);
-            const uint32_t sb = sa + TC_A_BYTES;
+            const uint64_t off = (uint64_t)((stage * TC_STAGE_BYTES) >> 4);
+            if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < TC_BK / 16; ++k)
-              mma_f16(d, sw128_desc(sa + 32 * k), sw128_desc(sb + 32 * k), TC_IDESC,
-                      (kb | k) != 0 ? 1u : 0u);
-            mma_commit(&empty[stage]);
+              for (int k = 0; k < TC_BK / 16; ++k)
+                mma_f16(d, da0 + off + 2 * k, db0 + off + 2 * k, TC_IDESC, (kb | k) != 0 ? 1u : 0u);
+              mma_commit(&empty[stage]);
+            }
+            __syncwarp();
             if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
           }
-          mma_commit(&tfull[acc]);
+          if (elect_one()) mma_commit(&tfull[acc]);
+          __syncwarp();
           acc ^= 1;
           if (acc == 0) aphase ^= 1;
         }
@@ -331,6 +261,20 @@ tsne_status launch_cand_tc(const __half* Xh, const float* nrm, int N, int Dp, in
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
     return TSNE_ERR_CUDA;
+  }
+  // CTA-pair kernel by default; TSNE_KNN_PATH=tc1 selects the 1-CTA kernel
+  const char* force = getenv("TSNE_KNN_PATH");
+  if (!(force && strcmp(force, "tc1") == 0)) {
+    CUtensorMap map_b;                                   // B half-tiles of the CTA pair
+    cuuint32_t box_b[2] = {TC_BK, (cuuint32_t)knn_tc2_b_rows()};
+    r = g_encode(&map_b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(Xh), gdim,
+                 gstride, box_b, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+      return TSNE_ERR_CUDA;
+    }
+    return launch_cand_tc2(map, map_b, nrm, N, Dp, Kc, buf, cand, slots, sync, s);
   }
   TSNE_CUDA_TRY(cudaFuncSetAttribute(k_cand_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)TC_SMEM));
