@@ -165,3 +165,16 @@ def random_csr(N: int, k: int = 10, seed: int = 3):
     row_ptr = np.cumsum(row_ptr)
     del vals
     return row_ptr, c, sym.astype(np.float32), sym
+
+
+def random_rows_csr(N: int, k: int = 126, seed: int = 11):
+    """A large random CSR (k sorted distinct-ish columns per row, positive
+    values summing to 1) for full-size gradient checks; drawn, not computed
+    by the method."""
+    rng = np.random.default_rng(seed)
+    cols = rng.integers(0, N, size=(N, k), dtype=np.int64).astype(np.int32)
+    cols.sort(1)
+    rp = np.arange(0, N * k + 1, k, dtype=np.int64)
+    val = rng.random(N * k).astype(np.float32)
+    val /= np.float32(val.sum(dtype=np.float64))
+    return rp, cols.ravel(), val
