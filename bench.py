@@ -244,20 +244,30 @@ def run_ours(args, rank, world):
 
     # roofline of the dominant kernel
     hbm, which = peaks()
-    bytes_attr = 8 * nnz + 8 * (N + 1) + 56 * N
-    kern = max(("attract_update_ms", "traverse_ms", "tree_ms"), key=lambda k: prof[k])
-    roof = {"kernel": kern.replace("_ms", "")}
-    if kern == "attract_update_ms":
+    # k_attract_sum, algorithmic bytes per launch: col + val (8 B/nnz), row_ptr
+    # (8 B/row), y_i (8 B/row), A out (8 B/row); the y_j gathers hit L2 (Y = 10 MB)
+    bytes_attr = 8 * nnz + 8 * (N + 1) + 16 * N
+    bytes_upd = 64 * N             # k_update: A, f, y, v, gains in; y', v, gains out
+    stage_kern = {"attract_ms": "k_attract_sum", "traverse_ms": "k_traverse",
+                  "tree_ms": "tree build (10 kernels)", "update_ms": "k_update"}
+    kern = max(stage_kern, key=lambda k: prof[k])
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")      # dram bytes per launch (ncu)
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get(stage_kern[kern])
+    roof = {"kernel": stage_kern[kern], "kernel_ms": prof[kern],
+            "iteration_overlapped_ms": prof.get("iteration_overlapped_ms")}
+    if kern == "attract_ms":
         ach = bytes_attr / (prof[kern] / 1e3) / 1e9
         roof.update({"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                     "frac": ach / hbm, "traffic": None, "peak_source": which,
+                     "frac": ach / hbm, "traffic": traffic, "peak_source": which,
                      "algorithmic_bytes": bytes_attr})
     else:
-        ach_attr = bytes_attr / (prof["attract_update_ms"] / 1e3) / 1e9
+        ach_attr = bytes_attr / (prof["attract_ms"] / 1e3) / 1e9
         roof.update({"bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None,
-                     "traffic": None, "note": "traversal is latency/issue bound; see DESIGN.md 7",
-                     "attract_update_hbm_gbs": ach_attr,
-                     "attract_update_frac": ach_attr / hbm})
+                     "traffic": traffic, "note": "traversal is issue/latency bound; DESIGN.md 7",
+                     "attract_hbm_gbs": ach_attr, "attract_frac": ach_attr / hbm})
+    roof["update_hbm_gbs"] = bytes_upd / (prof["update_ms"] / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,

@@ -176,14 +176,16 @@ tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const floa
                           float exaggeration, const tsne_config* cfg, void* ws,
                           size_t ws_bytes, tsne_stream_t stream);
 
-/* Diagnostics for measurement (bench.py): runs `reps` eager iterations from
- * the optimiser state exactly like tsne_optimize (advancing it from t0) and
- * reports the mean CUDA-event time of each stage on `stream`:
- *   stage_ms[0] tree build (H1-H4), stage_ms[1] traversal (H5-H6),
- *   stage_ms[2] attractive pass fused with the update (H7-H8).
- * kernels_per_iter (HOST out, nullable): number of kernel launches one
- * iteration makes (counted from a captured graph of one iteration).
- * stage_ms (HOST out, 3 doubles).  Synchronises stream. */
+/* Diagnostics for measurement (bench.py): from the optimiser state (advancing
+ * it exactly like tsne_optimize by 2 * reps iterations from t0) it runs `reps`
+ * eager iterations with the stages one after the other, then `reps` normal
+ * (overlapped) iterations, and reports mean CUDA-event times on `stream`:
+ *   stage_ms[0] tree build (H1-H4), [1] traversal (H5-H6), [2] attractive
+ *   sums (H7), [3] update (H8), [4] one overlapped iteration (the attractive
+ *   pass runs on a side stream concurrently with [0] and [1]).
+ * kernels_per_iter (HOST out, nullable): kernel launches per iteration
+ * (counted from a captured graph of one iteration).
+ * stage_ms (HOST out, 5 doubles).  Synchronises stream. */
 tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                                     int64_t N, float* Y, float* v, float* gains, int32_t t0,
                                     int32_t reps, float theta, float learning_rate,

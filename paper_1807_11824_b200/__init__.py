@@ -231,10 +231,10 @@ class Optimizer:
 
 
 def profile_iteration(opt: Optimizer, reps: int = 5, stream=None) -> dict:
-    """Per-stage mean CUDA-event times of `reps` eager iterations (advances the
-    optimiser state like Optimizer.step)."""
+    """Per-stage mean CUDA-event times (tsne_profile_iterations; advances the
+    optimiser state by 2 * reps iterations like Optimizer.step)."""
     s = opt.state
-    ms = (C.c_double * 3)()
+    ms = (C.c_double * 5)()
     kern = C.c_int32()
     st = C.c_void_p(stream) if stream is not None else _stream()
     _check(lib().tsne_profile_iterations(_ptr(opt.row_ptr), _ptr(opt.col), _ptr(opt.val), opt.N,
@@ -242,9 +242,9 @@ def profile_iteration(opt: Optimizer, reps: int = 5, stream=None) -> dict:
                                          opt.theta, opt.lr, opt.exag, C.byref(opt.cfg), ms,
                                          C.byref(kern), _ptr(opt.ws), opt.ws.numel(), st),
            "tsne_profile_iterations")
-    s.t += int(reps)
-    return {"tree_ms": ms[0], "traverse_ms": ms[1], "attract_update_ms": ms[2],
-            "kernels_per_iteration": kern.value}
+    s.t += 2 * int(reps)
+    return {"tree_ms": ms[0], "traverse_ms": ms[1], "attract_ms": ms[2], "update_ms": ms[3],
+            "iteration_overlapped_ms": ms[4], "kernels_per_iteration": kern.value}
 
 
 def init_y(N: int, seed: int = 42, device="cuda") -> torch.Tensor:

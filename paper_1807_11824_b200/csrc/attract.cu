@@ -99,113 +99,65 @@ __device__ __forceinline__ void update_coord(float g, float& v, float& gain, flo
   y = y + v;
 }
 
-__global__ void __launch_bounds__(kAttrThreads, kAttrBlocksPerSM)
-k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                 const float* __restrict__ val, const float2* __restrict__ Yin, int N,
-                 const float2* __restrict__ rep, const double* __restrict__ Z,
-                 int32_t* __restrict__ t_dev, Sched sc, float2* __restrict__ Yout,
-                 float2* __restrict__ V, float2* __restrict__ G, double2* __restrict__ part2,
-                 float4* __restrict__ part4, unsigned* __restrict__ counter,
-                 BoxInfo* __restrict__ box_next, int32_t* __restrict__ flag) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+// Attractive sums only (H7): A_i for every row, written to A.  Independent of
+// the tree, the traversal and Z, so it runs concurrently with them on a side
+// stream; reads the unshifted Y (differences only).
+__global__ void __launch_bounds__(kAttrThreads)
+k_attract_sum(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+              const float* __restrict__ val, const float2* __restrict__ Y, int N,
+              float2* __restrict__ A) {
+  const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * kAttrThreads + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * kAttrThreads) >> 5;
+  const int64_t nnz = row_ptr[N];
+  for (int i = warp; i < N; i += nwarps) {
+    const float2 yi = Y[i];
+    const float2 a = row_attractive(row_ptr[i], row_ptr[i + 1], nnz, col, val, Y, i, yi, lane);
+    if (lane == 0) A[i] = a;
+  }
+}
+
+// The update (H8): Eq. 7 with the traversal's f and Z, the D12 step, the
+// pending recentring (y - shift, D15), Y' = y + v; per-block fp64 sums and
+// min/max of Y' give the next iteration's shift and root box (last block).
+__global__ void __launch_bounds__(kAttrThreads)
+k_update(const float2* __restrict__ Yin, const float2* __restrict__ A, int N,
+         const float2* __restrict__ rep, const double* __restrict__ Z, int32_t* __restrict__ t_dev,
+         Sched sc, float2* __restrict__ Yout, float2* __restrict__ V, float2* __restrict__ G,
+         double2* __restrict__ part2, float4* __restrict__ part4, unsigned* __restrict__ counter,
+         BoxInfo* __restrict__ box, int32_t* __restrict__ flag) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int t = *t_dev;
   const float alpha = (t < sc.exag_iters) ? sc.exag : 1.f;
   const float mu = (t < sc.exag_iters) ? sc.mom0 : sc.mom1;
   const float invZ = (float)Z[1];
-  const int64_t nnz = row_ptr[N];
+  const float shx = box->shift_x, shy = box->shift_y;   // read before the block arrives
   double sx = 0.0, sy = 0.0;
   float mnx = INFINITY, mxx = -INFINITY, mny = INFINITY, mxy = -INFINITY;
   bool bad = false;
-  // A warp owns 32 consecutive rows; 4 rows are summed at a time by 8-lane
-  // subgroups (16-byte vector loads of col/val over each row's aligned
-  // window), then every lane updates its own row (coalesced state access).
-  const int sg = lane >> 3, sl = lane & 7;
-  const int ngroups = (N + 31) / 32;
-  for (int grp = warp; grp < ngroups; grp += nwarps) {
-    const int r0 = grp * 32;
-    const int rl = r0 + lane;
-    const bool rok = rl < N;
-    const int64_t my_e0 = row_ptr[rok ? rl : N];
-    const int64_t my_e1 = row_ptr[rok ? rl + 1 : N];
-    const float2 my_y = rok ? Yin[rl] : make_float2(0.f, 0.f);
-    float2 amine = make_float2(0.f, 0.f);
-#pragma unroll 1
-    for (int it = 0; it < 8; ++it) {
-      const int src = it * 4 + sg;                       // row r0 + src for this subgroup
-      const int64_t e0 = __shfl_sync(0xffffffffu, my_e0, src);
-      const int64_t e1 = __shfl_sync(0xffffffffu, my_e1, src);
-      const float2 yi = make_float2(__shfl_sync(0xffffffffu, my_y.x, src),
-                                    __shfl_sync(0xffffffffu, my_y.y, src));
-      const int i = r0 + src;
-      float ax = 0.f, ay = 0.f;
-      for (int64_t b = (e0 & ~int64_t(3)) + 4 * sl; b < e1; b += 32) {
-        int c[4];
-        float p[4];
-        if (b + 3 < nnz) {
-          const int4 cv = __ldcs(reinterpret_cast<const int4*>(col + b));
-          const float4 pv = __ldcs(reinterpret_cast<const float4*>(val + b));
-          c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
-          p[0] = pv.x; p[1] = pv.y; p[2] = pv.z; p[3] = pv.w;
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const bool ok = b + q < nnz;
-            c[q] = ok ? __ldcs(col + b + q) : i;
-            p[q] = ok ? __ldcs(val + b + q) : 0.f;
-          }
-        }
-        float2 yj[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const bool in = (b + q >= e0) && (b + q < e1);
-          if (!in) { c[q] = i; p[q] = 0.f; }
-          yj[q] = Yin[c[q]];
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float dx = yi.x - yj[q].x, dy = yi.y - yj[q].y;
-          const float w = __frcp_rn(1.f + dx * dx + dy * dy);
-          const float pw = p[q] * w;
-          ax = fmaf(pw, dx, ax);
-          ay = fmaf(pw, dy, ay);
-        }
-      }
-#pragma unroll
-      for (int o = 1; o < 8; o <<= 1) {                  // fixed 8-lane butterfly
-        ax += __shfl_xor_sync(0xffffffffu, ax, o);
-        ay += __shfl_xor_sync(0xffffffffu, ay, o);
-      }
-      // lane L receives row r0 + L (computed at it = L >> 2 by subgroup L & 3)
-      const float vx = __shfl_sync(0xffffffffu, ax, (lane & 3) * 8);
-      const float vy = __shfl_sync(0xffffffffu, ay, (lane & 3) * 8);
-      if ((lane >> 2) == it) amine = make_float2(vx, vy);
-    }
-    if (rok) {
-      const float2 f = rep[rl];
-      float2 v = V[rl], gn = G[rl];
-      const float gx = 4.f * (alpha * amine.x - f.x * invZ);
-      const float gy = 4.f * (alpha * amine.y - f.y * invZ);
-      float2 y = my_y;
-      update_coord(gx, v.x, gn.x, y.x, mu, sc.eta, sc.min_gain);
-      update_coord(gy, v.y, gn.y, y.y, mu, sc.eta, sc.min_gain);
-      V[rl] = v;
-      G[rl] = gn;
-      Yout[rl] = y;
-      sx += (double)y.x;
-      sy += (double)y.y;
-      mnx = fminf(mnx, y.x); mxx = fmaxf(mxx, y.x);
-      mny = fminf(mny, y.y); mxy = fmaxf(mxy, y.y);
-      bad |= !(isfinite(y.x) && isfinite(y.y));
-    }
+  for (int i = blockIdx.x * kAttrThreads + threadIdx.x; i < N; i += gridDim.x * kAttrThreads) {
+    const float2 a = A[i], f = rep[i];
+    float2 v = V[i], gn = G[i], y = Yin[i];
+    y.x = y.x - shx;
+    y.y = y.y - shy;
+    const float gx = 4.f * (alpha * a.x - f.x * invZ);
+    const float gy = 4.f * (alpha * a.y - f.y * invZ);
+    update_coord(gx, v.x, gn.x, y.x, mu, sc.eta, sc.min_gain);
+    update_coord(gy, v.y, gn.y, y.y, mu, sc.eta, sc.min_gain);
+    V[i] = v;
+    G[i] = gn;
+    Yout[i] = y;
+    sx += (double)y.x;
+    sy += (double)y.y;
+    mnx = fminf(mnx, y.x); mxx = fmaxf(mxx, y.x);
+    mny = fminf(mny, y.y); mxy = fmaxf(mxy, y.y);
+    bad |= !(isfinite(y.x) && isfinite(y.y));
   }
   sx = warp_sum(sx);
   sy = warp_sum(sy);
   mnx = warp_min(mnx); mxx = warp_max(mxx);
   mny = warp_min(mny); mxy = warp_max(mxy);
   bad = __any_sync(0xffffffffu, bad);
-  // block partials
   __shared__ double2 s_s[kAttrThreads];
   __shared__ float4 s_b[kAttrThreads];
   __shared__ bool s_last;
@@ -258,7 +210,7 @@ k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   if (threadIdx.x == 0) {
     ss = s_s[0];
     bb = s_b[0];
-    // recentring (D15): y <- y - mean, applied by the next tree build; by the
+    // recentring (D15): y <- y - mean, applied by the next iteration; by the
     // monotonicity of rounding, min(fl(y - m)) = fl(min(y) - m) exactly.
     const float mx = (float)(ss.x / (double)N), my = (float)(ss.y / (double)N);
     BoxInfo b;
@@ -266,7 +218,7 @@ k_attract_update(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
     b.shift_x = mx;
     b.shift_y = my;
     b.pad0 = 0.f;
-    *box_next = b;
+    *box = b;
     *t_dev = t + 1;
     *counter = 0u;
   }
@@ -287,13 +239,24 @@ tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, cons
   return TSNE_OK;
 }
 
-tsne_status launch_attract_update(const int64_t* row_ptr, const int32_t* col, const float* val,
-                                  const float2* Yin, int64_t N, TreeWS& w, OptWS& o,
-                                  const Sched& sc, float2* Yout, float2* V, float2* G,
-                                  cudaStream_t s) {
-  k_attract_update<<<attract_blocks(N), kAttrThreads, 0, s>>>(
-      row_ptr, col, val, Yin, (int)N, w.rep, w.Z, o.t_dev, sc, Yout, V, G, w.part2, w.part4,
-      w.counter + 2, w.box, o.flag);
+int update_blocks(int64_t N) {
+  int64_t b = (N + kAttrThreads - 1) / kAttrThreads;
+  int64_t cap = (int64_t)kNumSMs * 8;
+  return (int)(b < cap ? (b < 1 ? 1 : b) : cap);
+}
+
+tsne_status launch_attract_sum(const int64_t* row_ptr, const int32_t* col, const float* val,
+                               const float2* Y, int64_t N, float2* A, cudaStream_t s) {
+  k_attract_sum<<<attract_blocks(N), kAttrThreads, 0, s>>>(row_ptr, col, val, Y, (int)N, A);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
+tsne_status launch_update(const float2* Yin, const float2* A, int64_t N, TreeWS& w, OptWS& o,
+                          const Sched& sc, float2* Yout, float2* V, float2* G, cudaStream_t s) {
+  k_update<<<update_blocks(N), kAttrThreads, 0, s>>>(Yin, A, (int)N, w.rep, w.Z, o.t_dev, sc, Yout,
+                                                     V, G, w.part2, w.part4, w.counter + 2, w.box,
+                                                     o.flag);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }

@@ -22,6 +22,7 @@ void carve_opt(Carver& c, OptWS& o, int64_t N, int64_t nnz) {
   o.V = c.take<float2>(N);
   o.G = c.take<float2>(N);
   o.tmp = c.take<float2>(2 * N);
+  o.A = c.take<float2>(N);
   o.lab = c.take<int32_t>(N);
   o.lab2 = c.take<int32_t>(N);
   o.inv = c.take<int32_t>(N);
@@ -42,16 +43,39 @@ __global__ void k_set_state(int32_t* t_dev, int32_t t0, int32_t* flag) {
   *flag = 0;
 }
 
+// One iteration: the attractive sums run on a side stream
+// concurrently with the tree build and the traversal (they only need Y);
+// the update joins both.
 static tsne_status one_iteration(const int64_t* row_ptr, const int32_t* col, const float* val,
                                  int64_t N, float2* Yin, float2* Yout, float2* V, float2* G,
                                  float theta, const Sched& sc, TreeWS& w, OptWS& o,
                                  cudaStream_t s) {
-  tsne_status st = build_tree(w, Yin, /*apply_shift=*/true, s);
+  TSNE_CUDA_TRY(cudaEventRecord(o.ev_fork, s));
+  TSNE_CUDA_TRY(cudaStreamWaitEvent(o.side, o.ev_fork, 0));
+  tsne_status st = launch_attract_sum(row_ptr, col, val, Yin, N, o.A, o.side);
   if (st != TSNE_OK) return st;
-  st = launch_traverse(w, theta, s);
-  if (st != TSNE_OK) return st;
-  return launch_attract_update(row_ptr, col, val, Yin, N, w, o, sc, Yout, V, G, s);
+  TSNE_CUDA_TRY(cudaEventRecord(o.ev_join, o.side));
+  if ((st = build_tree(w, Yin, /*apply_shift=*/true, s)) != TSNE_OK) return st;
+  if ((st = launch_traverse(w, theta, s)) != TSNE_OK) return st;
+  TSNE_CUDA_TRY(cudaStreamWaitEvent(s, o.ev_join, 0));
+  return launch_update(Yin, o.A, N, w, o, sc, Yout, V, G, s);
 }
+
+// side stream + fork/join events for the concurrent attractive pass
+struct SideRes {
+  OptWS& o;
+  explicit SideRes(OptWS& ow) : o(ow) {
+    cudaStreamCreateWithFlags(&o.side, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&o.ev_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&o.ev_join, cudaEventDisableTiming);
+  }
+  ~SideRes() {
+    cudaEventDestroy(o.ev_fork);
+    cudaEventDestroy(o.ev_join);
+    cudaStreamDestroy(o.side);
+    o.side = nullptr;
+  }
+};
 
 // ---------------------------------------------------------------- relabelling
 // new label k <- old label perm[k]: state gathered, P rows permuted and their
@@ -181,6 +205,7 @@ tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const flo
                            int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t n_iter,
                            float theta, const Sched& sc, bool use_graphs, int relabel_every,
                            TreeWS& w, OptWS& o, cudaStream_t s) {
+  SideRes side(o);
   tsne_status st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, relabel_every > 0, s);
   if (st != TSNE_OK) return st;
   int h = 0;                                   // P half in use
@@ -226,6 +251,7 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
                                int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t reps,
                                float theta, const Sched& sc, TreeWS& w, OptWS& o, double* stage_ms,
                                int32_t* kernels, cudaStream_t s) {
+  SideRes side(o);
   tsne_status st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, true, s);
   if (st != TSNE_OK) return st;
   if (kernels) {  // count kernel nodes of one captured (never launched) iteration
@@ -248,31 +274,45 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
     *kernels = k;
     cudaGraphDestroy(g);
   }
-  cudaEvent_t e[4];
+  cudaEvent_t e[5];
   for (auto& x : e) cudaEventCreate(&x);
-  double acc[3] = {0, 0, 0};
+  double acc[4] = {0, 0, 0, 0};
   float2* a = o.Ya;
   float2* b = o.Yb;
+  // stages timed one after the other (no overlap), then the overlapped iteration
   for (int r = 0; r < reps && st == TSNE_OK; ++r) {
     cudaEventRecord(e[0], s);
     st = build_tree(w, a, true, s);
     cudaEventRecord(e[1], s);
     if (st == TSNE_OK) st = launch_traverse(w, theta, s);
     cudaEventRecord(e[2], s);
-    if (st == TSNE_OK)
-      st = launch_attract_update(o.rp[0], o.col[0], o.val[0], a, N, w, o, sc, b, o.V, o.G, s);
+    if (st == TSNE_OK) st = launch_attract_sum(o.rp[0], o.col[0], o.val[0], a, N, o.A, s);
     cudaEventRecord(e[3], s);
-    cudaEventSynchronize(e[3]);
-    for (int k = 0; k < 3; ++k) {
+    if (st == TSNE_OK) st = launch_update(a, o.A, N, w, o, sc, b, o.V, o.G, s);
+    cudaEventRecord(e[4], s);
+    cudaEventSynchronize(e[4]);
+    for (int k = 0; k < 4; ++k) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e[k], e[k + 1]);
       acc[k] += ms;
     }
     float2* t = a; a = b; b = t;
   }
+  double overlapped = 0.0;
+  for (int r = 0; r < reps && st == TSNE_OK; ++r) {
+    cudaEventRecord(e[0], s);
+    st = one_iteration(o.rp[0], o.col[0], o.val[0], N, a, b, o.V, o.G, theta, sc, w, o, s);
+    cudaEventRecord(e[1], s);
+    cudaEventSynchronize(e[1]);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e[0], e[1]);
+    overlapped += ms;
+    float2* t = a; a = b; b = t;
+  }
   for (auto& x : e) cudaEventDestroy(x);
   if (st != TSNE_OK) return st;
-  for (int k = 0; k < 3; ++k) stage_ms[k] = reps > 0 ? acc[k] / reps : 0.0;
+  for (int k = 0; k < 4; ++k) stage_ms[k] = reps > 0 ? acc[k] / reps : 0.0;
+  stage_ms[4] = reps > 0 ? overlapped / reps : 0.0;
   if ((st = leave(N, a, Y, V, G, w, o, s)) != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaStreamSynchronize(s));
   return TSNE_OK;

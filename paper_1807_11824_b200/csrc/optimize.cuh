@@ -21,6 +21,9 @@ struct OptWS {
   float2 *Ya = nullptr, *Yb = nullptr;   // embedding (double buffer of the update)
   float2 *V = nullptr, *G = nullptr;     // velocity, gains
   float2* tmp = nullptr;                 // permutation scratch
+  float2* A = nullptr;                   // attractive sums (side stream)
+  cudaStream_t side = nullptr;           // attractive pass runs here, concurrently
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int32_t *lab = nullptr, *lab2 = nullptr, *inv = nullptr;
   int64_t* rp[2] = {nullptr, nullptr};
   int32_t* col[2] = {nullptr, nullptr};
@@ -36,10 +39,10 @@ int attract_blocks(int64_t N);
 tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, const float* val,
                                 const float2* Y, int64_t N, const float2* rep, const double* Z,
                                 float alpha, float2* dY, cudaStream_t s);
-tsne_status launch_attract_update(const int64_t* row_ptr, const int32_t* col, const float* val,
-                                  const float2* Yin, int64_t N, TreeWS& w, OptWS& o,
-                                  const Sched& sc, float2* Yout, float2* V, float2* G,
-                                  cudaStream_t s);
+tsne_status launch_attract_sum(const int64_t* row_ptr, const int32_t* col, const float* val,
+                               const float2* Y, int64_t N, float2* A, cudaStream_t s);
+tsne_status launch_update(const float2* Yin, const float2* A, int64_t N, TreeWS& w, OptWS& o,
+                          const Sched& sc, float2* Yout, float2* V, float2* G, cudaStream_t s);
 
 // Runs n_iter iterations from the caller's state (Y, V, G) starting at t0.
 // relabel_every: period of the Morton relabelling (0 = never).

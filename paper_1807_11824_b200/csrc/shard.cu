@@ -37,6 +37,15 @@ __global__ void k_owned_list(const int32_t* __restrict__ flags, const int32_t* _
   if (flags[k]) list[pos[k]] = k;
 }
 
+__global__ void k_recentre(float2* Y, int N, const BoxInfo* box) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  float2 y = Y[i];
+  y.x = y.x - box->shift_x;
+  y.y = y.y - box->shift_y;
+  Y[i] = y;
+}
+
 tsne_status shard_forces(ShardWS& w, float2* Y, int64_t N, int64_t row0, int64_t row1,
                          float theta, bool recentre, float2* rep_local, double* z_partial,
                          cudaStream_t s) {
@@ -44,7 +53,11 @@ tsne_status shard_forces(ShardWS& w, float2* Y, int64_t N, int64_t row0, int64_t
   TSNE_CUDA_TRY(cudaMemsetAsync(t.counter, 0, 8 * sizeof(unsigned), s));
   tsne_status st = recentre ? launch_bbox_mean(t, Y, s) : launch_bbox(t, Y, s);
   if (st != TSNE_OK) return st;
-  if ((st = build_tree(t, Y, /*apply_shift=*/recentre, s)) != TSNE_OK) return st;
+  if (recentre) {            // the replicated embedding is recentred in place (D15)
+    k_recentre<<<(int)((N + 255) / 256), 256, 0, s>>>(Y, (int)N, t.box);
+    TSNE_LAUNCH_CHECK();
+  }
+  if ((st = build_tree(t, Y, /*apply_shift=*/false, s)) != TSNE_OK) return st;
   const int n = (int)N;
   k_owned_flags<<<(n + 256) / 256, 256, 0, s>>>(t.perm, n, (int)row0, (int)row1, w.flags);
   TSNE_LAUNCH_CHECK();
@@ -53,15 +66,6 @@ tsne_status shard_forces(ShardWS& w, float2* Y, int64_t N, int64_t row0, int64_t
   k_owned_list<<<(n + 255) / 256, 256, 0, s>>>(w.flags, w.pos, n, w.list);
   TSNE_LAUNCH_CHECK();
   return launch_traverse_list(t, theta, w.list, w.pos + n, (int)row0, rep_local, z_partial, s);
-}
-
-__global__ void k_recentre(float2* Y, int N, const BoxInfo* box) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  float2 y = Y[i];
-  y.x = y.x - box->shift_x;
-  y.y = y.y - box->shift_y;
-  Y[i] = y;
 }
 
 tsne_status shard_recentre(ShardWS& w, float2* Y, int64_t N, cudaStream_t s) {

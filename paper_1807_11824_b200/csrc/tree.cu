@@ -223,7 +223,9 @@ __device__ __forceinline__ uint32_t quantise(float y, double lo, double s) {
   return (uint32_t)f;
 }
 
-__global__ void k_keys(float2* __restrict__ Y, int N, const BoxInfo* __restrict__ box,
+// Y is read-only: the pending recentring shift (D15) is applied on the fly,
+// so the attractive pass may read Y concurrently.
+__global__ void k_keys(const float2* __restrict__ Y, int N, const BoxInfo* __restrict__ box,
                        int apply_shift, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
                        int32_t* __restrict__ cnt) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -235,7 +237,6 @@ __global__ void k_keys(float2* __restrict__ Y, int N, const BoxInfo* __restrict_
   if (apply_shift) {
     y.x = y.x - b.shift_x;
     y.y = y.y - b.shift_y;
-    Y[i] = y;
   }
   uint32_t qx = quantise(y.x, b.lox, b.s);
   uint32_t qy = quantise(y.y, b.loy, b.s);
@@ -245,12 +246,16 @@ __global__ void k_keys(float2* __restrict__ Y, int N, const BoxInfo* __restrict_
 
 // ---------------------------------------------------------------- gather
 __global__ void k_gather(const float2* __restrict__ Y, const int32_t* __restrict__ perm, int N,
-                         const BoxInfo* __restrict__ box, float2* __restrict__ ys,
+                         const BoxInfo* __restrict__ box, int apply_shift, float2* __restrict__ ys,
                          longlong2* __restrict__ fq) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k > N) return;
   if (k == N) { fq[N] = make_longlong2(0, 0); return; }
   float2 y = Y[perm[k]];
+  if (apply_shift) {
+    y.x = y.x - box->shift_x;
+    y.y = y.y - box->shift_y;
+  }
   ys[k] = y;
   const double cx = box->cx, cy = box->cy, inv = kFixScale / box->r0;
   long long qx = __double2ll_rn(__dmul_rn(__dsub_rn((double)y.x, cx), inv));
@@ -387,7 +392,7 @@ __global__ void k_quad_emit(int N, const int32_t* __restrict__ bfirst,
 // ---------------------------------------------------------------- host
 static inline int cdiv(int64_t a, int b) { return (int)((a + b - 1) / b); }
 
-tsne_status build_tree(TreeWS& w, float2* Y, bool apply_shift, cudaStream_t s) {
+tsne_status build_tree(TreeWS& w, const float2* Y, bool apply_shift, cudaStream_t s) {
   const int N = (int)w.N;
   const int T = 256;
   k_keys<<<cdiv(N + 1, T), T, 0, s>>>(Y, N, w.box, apply_shift ? 1 : 0, w.keys_a, w.vals_a, w.cnt);
@@ -398,7 +403,7 @@ tsne_status build_tree(TreeWS& w, float2* Y, bool apply_shift, cudaStream_t s) {
   TSNE_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, sb, dk, dv, N, 0, 32, s));
   w.keys_sorted = dk.Current();
   w.perm = dv.Current();
-  k_gather<<<cdiv(N + 1, T), T, 0, s>>>(Y, w.perm, N, w.box, w.ys, w.fq);
+  k_gather<<<cdiv(N + 1, T), T, 0, s>>>(Y, w.perm, N, w.box, apply_shift ? 1 : 0, w.ys, w.fq);
   TSNE_LAUNCH_CHECK();
   size_t cb = w.scan_tmp_bytes;
   TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveScan(w.scan_tmp, cb, w.fq, w.S, LL2Sum(),

@@ -75,9 +75,9 @@ size_t tree_cub_bytes(int64_t N, size_t* sort_b, size_t* scan_b, size_t* scan2_b
 
 // Bounding box + root box of Y (shift = 0), written to w.box.
 tsne_status launch_bbox(TreeWS& w, const float2* Y, cudaStream_t s);
-// Steps 2-4 from w.box: keys (after subtracting box->shift from Y in place
-// when `apply_shift`), sort, build, summarise.
-tsne_status build_tree(TreeWS& w, float2* Y, bool apply_shift, cudaStream_t s);
+// Steps 2-4 from w.box: keys (of Y - box->shift when `apply_shift`; Y itself
+// is not modified), sort, build, summarise.
+tsne_status build_tree(TreeWS& w, const float2* Y, bool apply_shift, cudaStream_t s);
 // Repulsive pass: w.rep, w.Z
 tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s);
 tsne_status launch_traverse_list(TreeWS& w, float theta, const int32_t* list, const int32_t* nlist,
