@@ -164,21 +164,45 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
         tc_fence_after();
         const int c0 = ct * P_BN;
         const uint32_t tbase = tmem + ((uint32_t)(e * 32) << 16) + (uint32_t)(acc * P_BN);
+        const float tf = (tau == kKeyMax) ? INFINITY : key_val(tau);
 #pragma unroll 1
-        for (int ch = 0; ch < P_BN / 32; ++ch) {
+        for (int ch = 0; ch < P_BN / 32; ch += 2) {    // 64 columns per TMEM wait
           const int j0 = c0 + ch * 32;
-          const float nv = __ldg(nrm + j0 + lane);       // |y_j|^2, one per lane
-          uint32_t r[32];
-          tmem_ld32(tbase + ch * 32, r);
-          if (dbg_skip_epilogue) continue;   // diagnostics: MMA pipeline alone
-          const float tf = (tau == kKeyMax) ? INFINITY : key_val(tau);
+          uint32_t r[64];
+          tmem_ld32_nowait(tbase + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld32_nowait(tbase + ch * 32 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          float nv[64];                                  // |y_j|^2: warp-uniform broadcast loads
+          const float4* n4 = reinterpret_cast<const float4*>(nrm + j0);
 #pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const float dist = fmaf(-2.f, __uint_as_float(r[t]), __shfl_sync(0xffffffffu, nv, t));
-            if (dist <= tf) {
-              const int j = j0 + t;
+          for (int u = 0; u < 16; ++u) {
+            const float4 v = __ldg(n4 + u);
+            nv[4 * u] = v.x; nv[4 * u + 1] = v.y; nv[4 * u + 2] = v.z; nv[4 * u + 3] = v.w;
+          }
+          tmem_wait_ld();
+          if (dbg_skip_epilogue) continue;   // diagnostics: MMA pipeline alone
+          // fast path: 2 instructions per distance (FFMA + FMNMX), no branches
+          float mn = INFINITY;
+#pragma unroll
+          for (int t = 0; t < 64; ++t) mn = fminf(mn, fmaf(-2.f, __uint_as_float(r[t]), nv[t]));
+          if (!__any_sync(0xffffffffu, qok && mn <= tf)) continue;
+          // slow path: the columns holding a candidate for some lane of the warp
+          uint64_t m = 0;
+#pragma unroll
+          for (int t = 0; t < 64; ++t)
+            if (fmaf(-2.f, __uint_as_float(r[t]), nv[t]) <= tf) m |= 1ull << t;
+          if (!qok) m = 0;
+          const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)m);
+          const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(m >> 32));
+          uint64_t u = ((uint64_t)hi << 32) | lo;
+          while (u) {                                    // warp-uniform loop over hit columns
+            const int t = __ffsll((long long)u) - 1;
+            u &= u - 1;
+            const uint32_t v = tmem_ld1(tbase + ch * 32 + t);   // re-read the column from TMEM
+            const float dist = fmaf(-2.f, __uint_as_float(v), __ldg(nrm + j0 + t));
+            const int j = j0 + t;
+            if ((m >> t) & 1) {
               const u64 key = mkkey(dist, j);
-              if (qok && j < N && j != q && key < tau) rowbuf[cnt++] = key;
+              if (j < N && j != q && key < tau) rowbuf[cnt++] = key;
             }
           }
         }
