@@ -131,7 +131,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "it/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": cfg.name, "N": N, "D": cfg.D, "theta": 0.5,
                    "nnz_per_row": nnz_row},
@@ -159,6 +159,30 @@ def run_e2e(T, Xh, cfg, N, args):
             "knn_rows_uncertified": info["knn_rows_uncertified"], "nnz": info["nnz"]}
 
 
+def run_e2e_sharded(Xh_local, cfg, N, args, rank, world, dev):
+    """sharded.run on `world` GPUs from each rank's pinned host shard of X to
+    pinned host Y on rank 0; CUDA events on every rank, max over ranks."""
+    from paper_1807_11824_b200 import sharded
+    Yh = torch.empty(N, 2, dtype=torch.float32, pin_memory=True) if rank == 0 else None
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    a.record()
+    _, info = sharded.run(Xh_local, N, perplexity=cfg.perplexity, theta=0.5,
+                          n_iter=args.e2e_iters, Y_out=Yh, device=dev)
+    b.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    t = torch.tensor([a.elapsed_time(b) / 1e3, wall], dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    sec, wall = float(t[0]), float(t[1])
+    return {"value": args.e2e_iters / sec, "unit": "it/s", "seconds": sec, "wall_seconds": wall,
+            "n_iter": args.e2e_iters, "h2d_bytes_per_step": 4 * N * cfg.D,
+            "d2h_bytes_per_step": 8 * N, "api": "paper_1807_11824_b200.sharded.run",
+            "knn_rows_uncertified": info["knn_rows_uncertified"], "nnz": info["nnz"]}
+
+
 def run_ours(args, rank, world):
     import paper_1807_11824_b200 as T
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
@@ -181,12 +205,44 @@ def run_ours(args, rank, world):
         e2e = run_e2e(T, Xh, cfg, N, args)
         X = Xh.to(dev)
         del Xh
+    elif world > 1 and not args.no_e2e:
+        from paper_1807_11824_b200.sharded import shard_range
+        r0, r1, _ = shard_range(N, world, rank)
+        Xh = torch.empty(r1 - r0, cfg.D, dtype=torch.float32, pin_memory=True)
+        Xh.copy_(X[r0:r1])
+        e2e = run_e2e_sharded(Xh, cfg, N, args, rank, world, dev)
+        del Xh
+        torch.cuda.empty_cache()
     a, b = ev(), ev()
-    a.record()
-    idx, d2, kinfo = T.knn(X, K)
-    b.record()
-    torch.cuda.synchronize()
-    stages["knn_ms"] = a.elapsed_time(b)
+    if world > 1:
+        # the kNN sharded by query row (tsne_knn_rows), lists all-gathered
+        from paper_1807_11824_b200.sharded import _all_gather_flat, shard_range
+        r0, r1, S = shard_range(N, world, rank)
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        a.record()
+        il, dl, kinfo = T.knn(X, K, rows=(r0, r1))
+        ip = torch.zeros(S, K, dtype=torch.int32, device=dev)
+        dp = torch.zeros(S, K, dtype=torch.float64, device=dev)
+        ip[: r1 - r0], dp[: r1 - r0] = il, dl
+        idx = torch.empty(world * S, K, dtype=torch.int32, device=dev)
+        d2 = torch.empty(world * S, K, dtype=torch.float64, device=dev)
+        _all_gather_flat(idx, ip)
+        _all_gather_flat(d2, dp)
+        idx, d2 = idx[:N].contiguous(), d2[:N].contiguous()
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b)], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        stages["knn_ms"] = float(t.item())
+        del il, dl, ip, dp
+    else:
+        a.record()
+        idx, d2, kinfo = T.knn(X, K)
+        b.record()
+        torch.cuda.synchronize()
+        stages["knn_ms"] = a.elapsed_time(b)
+    del X
     a.record()
     rp, col, val = T.compute_p(idx, d2, cfg.perplexity)
     b.record()
@@ -290,9 +346,7 @@ def run_ours(args, rank, world):
                                 "kind": "oracle",
                                 "sample": f"{ns} full-size fp64 oracle iteration(s) at N={N} "
                                           f"(synthetic clustered Y, {round(nnz / N)} nnz/row)"}
-    if world > 1:
-        line["e2e"] = {"value": None, "unit": "it/s", "note": "tsne_run (end to end) is the single-GPU entry point"}
-    elif e2e is not None:
+    if e2e is not None:
         line["e2e"] = e2e
     if rank == 0:
         print(json.dumps(line), flush=True)

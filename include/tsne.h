@@ -84,6 +84,18 @@ tsne_status tsne_knn(const float* X, int64_t N, int32_t D, int32_t K,
                      int32_t* idx, double* d2, void* ws, size_t ws_bytes,
                      tsne_knn_info* info, tsne_stream_t stream);
 
+/* The same search for the query rows [q0, q0 + nq) only, against all N
+ * points (the multi-GPU sharding of the kNN by query point):
+ * idx / d2 are nq x K, row r holding the neighbours of point q0 + r, and
+ * are identical to rows q0..q0+nq-1 of tsne_knn's output (the fp16
+ * centring/scaling is computed over all N rows on every call).  Workspace:
+ * tsne_knn_workspace_size(N, D, K).  nq = 0 is a no-op; a range outside
+ * [0, N) is TSNE_ERR_ARG. */
+tsne_status tsne_knn_rows(const float* X, int64_t N, int32_t D, int32_t K,
+                          int64_t q0, int64_t nq, int32_t* idx, double* d2,
+                          void* ws, size_t ws_bytes, tsne_knn_info* info,
+                          tsne_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * U2 + U3  Sparse joint affinities P (Eq. 1; symmetrisation
  * p_ij = (p_{i|j} + p_{j|i}) / 2N; at most 2NK nonzeros).

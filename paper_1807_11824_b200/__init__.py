@@ -47,7 +47,7 @@ class RunInfo(C.Structure):
 
 
 EXPORTS = ["tsne_last_error", "tsne_abi_version", "tsne_config_default",
-           "tsne_knn_workspace_size", "tsne_knn", "tsne_compute_p_workspace_size",
+           "tsne_knn_workspace_size", "tsne_knn", "tsne_knn_rows", "tsne_compute_p_workspace_size",
            "tsne_compute_p", "tsne_gradient_workspace_size", "tsne_gradient",
            "tsne_optimize_workspace_size", "tsne_optimize", "tsne_init_y", "tsne_run",
            "tsne_run_ex", "tsne_profile_iterations", "tsne_shard_workspace_size",
@@ -70,6 +70,7 @@ def lib():
     L.tsne_knn_workspace_size.argtypes = [i64, i32, i32]
     L.tsne_knn_workspace_size.restype = sz
     L.tsne_knn.argtypes = [vp, i64, i32, i32, vp, vp, vp, sz, C.POINTER(KnnInfo), vp]
+    L.tsne_knn_rows.argtypes = [vp, i64, i32, i32, i64, i64, vp, vp, vp, sz, C.POINTER(KnnInfo), vp]
     L.tsne_compute_p_workspace_size.argtypes = [i64, i32]
     L.tsne_compute_p_workspace_size.restype = sz
     L.tsne_compute_p.argtypes = [vp, vp, i64, i32, f32, vp, vp, vp, C.POINTER(i64), vp, vp, sz, vp]
@@ -94,7 +95,7 @@ def lib():
     L.tsne_shard_update.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, vp, i32, i32, f32, f32,
                                     C.POINTER(Config), vp, vp, vp, vp, vp]
     L.tsne_recentre.argtypes = [vp, i64, vp, sz, vp]
-    for name in ["tsne_knn", "tsne_compute_p", "tsne_gradient", "tsne_optimize", "tsne_init_y",
+    for name in ["tsne_knn", "tsne_knn_rows", "tsne_compute_p", "tsne_gradient", "tsne_optimize", "tsne_init_y",
                  "tsne_run", "tsne_run_ex", "tsne_profile_iterations", "tsne_shard_forces",
                  "tsne_shard_update", "tsne_recentre"]:
         getattr(L, name).restype = C.c_int
@@ -138,16 +139,23 @@ def default_config(**kw) -> Config:
 
 
 # ---------------------------------------------------------------- U1
-def knn(X: torch.Tensor, K: int):
-    """Exact kNN: (idx int32 [N,K], d2 float64 [N,K], info dict)."""
+def knn(X: torch.Tensor, K: int, rows=None):
+    """Exact kNN: (idx int32 [n,K], d2 float64 [n,K], info dict).  `rows` =
+    (q0, q1) restricts the queries to points q0..q1-1 (tsne_knn_rows, the
+    multi-GPU shard); by default every point is a query (tsne_knn)."""
     X = _dev(X, torch.float32, "X")
     N, D = X.shape
-    idx = torch.empty(N, K, dtype=torch.int32, device=X.device)
-    d2 = torch.empty(N, K, dtype=torch.float64, device=X.device)
+    q0, q1 = (0, N) if rows is None else (int(rows[0]), int(rows[1]))
+    idx = torch.empty(q1 - q0, K, dtype=torch.int32, device=X.device)
+    d2 = torch.empty(q1 - q0, K, dtype=torch.float64, device=X.device)
     ws = _ws(lib().tsne_knn_workspace_size(N, D, K), X.device)
     info = KnnInfo()
-    _check(lib().tsne_knn(_ptr(X), N, D, K, _ptr(idx), _ptr(d2), _ptr(ws), ws.numel(),
-                          C.byref(info), _stream()), "tsne_knn")
+    if rows is None:
+        _check(lib().tsne_knn(_ptr(X), N, D, K, _ptr(idx), _ptr(d2), _ptr(ws), ws.numel(),
+                              C.byref(info), _stream()), "tsne_knn")
+    else:
+        _check(lib().tsne_knn_rows(_ptr(X), N, D, K, q0, q1 - q0, _ptr(idx), _ptr(d2), _ptr(ws),
+                                   ws.numel(), C.byref(info), _stream()), "tsne_knn_rows")
     return idx, d2, {"rows_uncertified": info.rows_uncertified, "candidates": info.candidates,
                      "gemm_path": "tcgen05" if info.gemm_path == 1 else "cuda-core"}
 

@@ -382,7 +382,34 @@ tsne_status tsne_knn(const float* X, int64_t N, int32_t D, int32_t K, int32_t* i
   if (st != TSNE_OK) return st;
   Carver c(ws);
   carve_knn(c, w, N, D, K);
-  return run_knn(X, N, D, K, idx, d2, w, info, (cudaStream_t)stream);
+  return run_knn(X, N, D, K, 0, N, idx, d2, w, info, (cudaStream_t)stream);
+}
+
+tsne_status tsne_knn_rows(const float* X, int64_t N, int32_t D, int32_t K, int64_t q0, int64_t nq,
+                          int32_t* idx, double* d2, void* ws, size_t ws_bytes,
+                          tsne_knn_info* info, tsne_stream_t stream) {
+  clear_error();
+  TSNE_ARG_CHECK(N >= 2 && N < (int64_t(1) << 31) - 1, "N must be in [2, 2^31-1)");
+  TSNE_ARG_CHECK(D >= 1, "D must be >= 1");
+  TSNE_ARG_CHECK(K >= 1 && K < N && K <= kMaxK, "K must satisfy 1 <= K < N and K <= %d", kMaxK);
+  TSNE_ARG_CHECK(q0 >= 0 && nq >= 0 && q0 + nq <= N, "query rows [q0, q0+nq) must lie in [0, N)");
+  TSNE_ARG_CHECK(X && (nq == 0 || (idx && d2)), "null pointer argument");
+  KnnWS w;
+  Carver c0(nullptr);
+  carve_knn(c0, w, N, D, K);
+  if (!ws || ws_bytes < c0.bytes()) {
+    set_error("workspace too small: need %zu bytes, got %zu", c0.bytes(), ws_bytes);
+    return TSNE_ERR_WORKSPACE;
+  }
+  tsne_status st = check_device();
+  if (st != TSNE_OK) return st;
+  if (nq == 0) {
+    if (info) { info->rows_uncertified = 0; info->candidates = w.Kc; info->gemm_path = 0; }
+    return TSNE_OK;
+  }
+  Carver c(ws);
+  carve_knn(c, w, N, D, K);
+  return run_knn(X, N, D, K, q0, nq, idx, d2, w, info, (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------- P
@@ -518,7 +545,7 @@ tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, 
   }
   if (st == TSNE_OK) {
     KnnWS kw; Carver kc(ws); carve_knn(kc, kw, N, D, K);
-    st = run_knn(Xuse, N, D, K, idx, d2, kw, &kinfo, s);
+    st = run_knn(Xuse, N, D, K, 0, N, idx, d2, kw, &kinfo, s);
   }
   cudaEventRecord(ev[2], s);
   if (st == TSNE_OK) {

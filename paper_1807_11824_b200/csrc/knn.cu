@@ -54,8 +54,8 @@ void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K) {
   w.cand = c.take<u64>((size_t)N * w.Kc);
   w.uncert = c.take<u64>(2);
   w.rows_bad = c.take<int32_t>(N);
-  w.sync = c.take<unsigned>(knn_tc_sync_words(N) > knn_tc2_sync_words(N) ? knn_tc_sync_words(N)
-                                                                           : knn_tc2_sync_words(N));
+  w.sync = c.take<unsigned>(knn_tc_sync_words(N, N) > knn_tc2_sync_words(N, N) ? knn_tc_sync_words(N, N)
+                                                                           : knn_tc2_sync_words(N, N));
 }
 
 // ---------------------------------------------------------------- prep
@@ -137,16 +137,16 @@ struct SimtSmem {
 };
 
 __global__ void __launch_bounds__(kS_Threads, 1)
-k_cand_simt(const __half* __restrict__ Xh, const float* __restrict__ nrm, int N, int Dp, int Kc,
-            u64* __restrict__ buf, u64* __restrict__ cand) {
+k_cand_simt(const __half* __restrict__ Xh, const float* __restrict__ nrm, int N, int qs, int nq,
+            int Dp, int Kc, u64* __restrict__ buf, u64* __restrict__ cand) {
   extern __shared__ __align__(16) unsigned char smraw[];
   SimtSmem& sm = *reinterpret_cast<SimtSmem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int tx = tid & 15, ty = tid >> 4;
   u64* mybuf = buf + (size_t)blockIdx.x * kKnnBM * kCandCap;
-  const int nrb = (N + kKnnBM - 1) / kKnnBM;
+  const int nrb = (nq + kKnnBM - 1) / kKnnBM;
   for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
-    const int q0 = rb * kKnnBM;
+    const int q0 = qs + rb * kKnnBM;                     // first global query row of the block
     if (tid < kKnnBM) { sm.cnt[tid] = 0; sm.tau[tid] = kKeyMax; }
     __syncthreads();
     for (int c0 = 0; c0 < N; c0 += kS_BN) {
@@ -205,7 +205,7 @@ k_cand_simt(const __half* __restrict__ Xh, const float* __restrict__ nrm, int N,
       // offer: thread t owns query row q0 + t
       if (tid < kKnnBM) {
         const int q = q0 + tid;
-        if (q < N) {
+        if (q < qs + nq) {
           int cnt = sm.cnt[tid];
           const u64 tau = sm.tau[tid];
           u64* rowbuf = mybuf + (size_t)tid * kCandCap;
@@ -239,10 +239,10 @@ k_cand_simt(const __half* __restrict__ Xh, const float* __restrict__ nrm, int N,
     // final: every row -> its Kc best keys
     for (int r = wid; r < kKnnBM; r += kS_Threads / 32) {
       const int q = q0 + r;
-      if (q < N) {
+      if (q < qs + nq) {
         u64 t;
         compact_keys(mybuf + (size_t)r * kCandCap, sm.cnt[r], Kc, sm.sortbuf[wid], lane,
-                     cand + (size_t)q * Kc, t);
+                     cand + (size_t)(q - qs) * Kc, t);
       }
     }
     __syncthreads();
@@ -253,19 +253,21 @@ k_cand_simt(const __half* __restrict__ Xh, const float* __restrict__ nrm, int N,
 constexpr int kRR_Threads = 256;
 
 __global__ void __launch_bounds__(kRR_Threads)
-k_rerank(const float* __restrict__ X, int N, int D, int K, int Kc, const u64* __restrict__ cand,
+k_rerank(const float* __restrict__ X, int N, int qs, int nq, int D, int K, int Kc,
+         const u64* __restrict__ cand,
          const float* __restrict__ nrm, const float* __restrict__ scale,
          int32_t* __restrict__ idx, double* __restrict__ d2, u64* __restrict__ uncert,
          int32_t* __restrict__ rows_bad) {
   __shared__ double s_d[kRR_Threads / 32][256];
   __shared__ int s_j[kRR_Threads / 32][256];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int i = blockIdx.x * (kRR_Threads / 32) + wid;
-  if (i >= N) return;
+  const int il = blockIdx.x * (kRR_Threads / 32) + wid;   // local query row
+  if (il >= nq) return;
+  const int i = qs + il;
   double* sd = s_d[wid];
   int* sj = s_j[wid];
   const float* xi = X + (size_t)i * D;
-  const u64* ci = cand + (size_t)i * Kc;
+  const u64* ci = cand + (size_t)il * Kc;
   const double inv2 = (double)scale[1];
   const double nrm_i = (double)nrm[i];
   double emax = 0.0;
@@ -307,8 +309,8 @@ k_rerank(const float* __restrict__ X, int N, int D, int K, int Kc, const u64* __
       __syncwarp();
     }
   for (int c = lane; c < K; c += 32) {
-    idx[(size_t)i * K + c] = sj[c];
-    d2[(size_t)i * K + c] = sd[c];
+    idx[(size_t)il * K + c] = sj[c];
+    d2[(size_t)il * K + c] = sd[c];
   }
   if (lane == 0) {
     const bool all = (Kc >= N - 1);
@@ -321,8 +323,8 @@ k_rerank(const float* __restrict__ X, int N, int D, int K, int Kc, const u64* __
 }
 
 // ---------------------------------------------------------------- host
-tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int32_t* idx, double* d2,
-                    KnnWS& w, tsne_knn_info* info, cudaStream_t s) {
+tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int64_t q0, int64_t nq,
+                    int32_t* idx, double* d2, KnnWS& w, tsne_knn_info* info, cudaStream_t s) {
   const int Dp = w.Dp, Kc = w.Kc;
   {
     dim3 g((D + 255) / 256, kColRB);
@@ -344,17 +346,19 @@ tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int32_t* id
   const char* force = getenv("TSNE_KNN_PATH");
   bool tc = knn_tc_available() && Dp % 64 == 0 && !(force && strcmp(force, "simt") == 0);
   if (tc) {
-    tsne_status st = launch_cand_tc(w.Xh, w.nrm, (int)N, Dp, Kc, w.buf, w.cand, w.slots, w.sync, s);
+    tsne_status st = launch_cand_tc(w.Xh, w.nrm, (int)N, (int)q0, (int)nq, Dp, Kc, w.buf, w.cand, w.slots, w.sync, s);
     if (st != TSNE_OK) return st;
   } else {
     const size_t smem = sizeof(SimtSmem);
     TSNE_CUDA_TRY(cudaFuncSetAttribute(k_cand_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-    k_cand_simt<<<w.slots, kS_Threads, smem, s>>>(w.Xh, w.nrm, (int)N, Dp, Kc, w.buf, w.cand);
+    k_cand_simt<<<w.slots, kS_Threads, smem, s>>>(w.Xh, w.nrm, (int)N, (int)q0, (int)nq, Dp, Kc,
+                                                   w.buf, w.cand);
     TSNE_LAUNCH_CHECK();
   }
   w.path = tc ? 1 : 0;
-  k_rerank<<<(int)((N + 7) / 8), kRR_Threads, 0, s>>>(X, (int)N, D, K, Kc, w.cand, w.nrm, w.scale,
+  k_rerank<<<(int)((nq + 7) / 8), kRR_Threads, 0, s>>>(X, (int)N, (int)q0, (int)nq, D, K, Kc,
+                                                      w.cand, w.nrm, w.scale,
                                                      idx, d2, w.uncert, w.rows_bad);
   TSNE_LAUNCH_CHECK();
   if (info) {

@@ -30,8 +30,10 @@ struct KnnWS {
 };
 
 void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K);
-tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int32_t* idx, double* d2,
-                    KnnWS& w, tsne_knn_info* info, cudaStream_t s);
+// Neighbours of the query rows [q0, q0 + nq) among all N points; idx / d2 are
+// nq x K (row q0 + r at row r).
+tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int64_t q0, int64_t nq,
+                    int32_t* idx, double* d2, KnnWS& w, tsne_knn_info* info, cudaStream_t s);
 
 // util (util.cu)
 tsne_status check_finite(const float* X, int64_t n, int32_t* dflag, int32_t* hflag, cudaStream_t s);

@@ -38,8 +38,8 @@ constexpr uint32_t TC_IDESC = (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) |
 constexpr size_t TC_SMEM = 1024 + TC_STAGES * TC_STAGE_BYTES + 256 + 4 * TC_CAP * 8;
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
-k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nrm, int N, int Dp,
-          int Kc, u64* __restrict__ buf, u64* __restrict__ cand, unsigned* __restrict__ sync) {
+k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nrm, int N, int q0, int nq,
+          int Dp, int Kc, u64* __restrict__ buf, u64* __restrict__ cand, unsigned* __restrict__ sync) {
   extern __shared__ unsigned char smraw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -52,7 +52,7 @@ k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nr
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = Dp / TC_BK;
-  const int nrb = (N + TC_BM - 1) / TC_BM, nct = (N + TC_BN - 1) / TC_BN;
+  const int nrb = (nq + TC_BM - 1) / TC_BM, nct = (N + TC_BN - 1) / TC_BN;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -98,7 +98,7 @@ k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nr
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_tx(&full[stage], TC_STAGE_BYTES);
             unsigned char* sa = base + stage * TC_STAGE_BYTES;
-            tma_load_2d(sa, &tmap, &full[stage], kb * TC_BK, rb * TC_BM);
+            tma_load_2d(sa, &tmap, &full[stage], kb * TC_BK, q0 + rb * TC_BM);
             tma_load_2d(sa + TC_A_BYTES, &tmap, &full[stage], kb * TC_BK, ct * TC_BN);
             tma_load_2d(sa + TC_A_BYTES + TC_A_BYTES, &tmap, &full[stage], kb * TC_BK,
                         ct * TC_BN + 128);
@@ -144,8 +144,8 @@ k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nr
     int acc = 0;
     uint32_t aphase = 0;
     for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
-      const int q = rb * TC_BM + rl;
-      const bool qok = q < N;
+      const int q = q0 + rb * TC_BM + rl;        // global query index
+      const bool qok = rb * TC_BM + rl < nq;
       int cnt = 0;
       u64 tau = kKeyMax;
       for (int ct = 0; ct < nct; ++ct) {
@@ -192,7 +192,7 @@ k_cand_tc(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ nr
       __syncwarp();
       for (int l = 0; l < 32; ++l) {
         const int ql = rb * TC_BM + e * 32 + l;
-        if (ql >= N) break;
+        if (ql >= nq) break;
         const int n = __shfl_sync(0xffffffffu, cnt, l);
         u64* rb_l = buf + ((size_t)blockIdx.x * TC_BM + e * 32 + l) * TC_CAP;
         u64 t;
@@ -236,13 +236,13 @@ bool knn_tc_available() {
 
 size_t knn_tc_cap() { return TC_CAP; }
 
-size_t knn_tc_sync_words(int64_t N) {
-  const int64_t nrb = (N + TC_BM - 1) / TC_BM, nct = (N + TC_BN - 1) / TC_BN;
+size_t knn_tc_sync_words(int64_t N, int64_t nq) {
+  const int64_t nrb = (nq + TC_BM - 1) / TC_BM, nct = (N + TC_BN - 1) / TC_BN;
   const int64_t waves = (nrb + kNumSMs - 1) / kNumSMs;
   return (size_t)(waves * ((nct + TC_SYNC_EVERY - 1) / TC_SYNC_EVERY) + 1);
 }
 
-tsne_status launch_cand_tc(const __half* Xh, const float* nrm, int N, int Dp, int Kc,
+tsne_status launch_cand_tc(const __half* Xh, const float* nrm, int N, int q0, int nq, int Dp, int Kc,
                            unsigned long long* buf, unsigned long long* cand, int slots,
                            unsigned* sync, cudaStream_t s) {
   if (!knn_tc_available()) {
@@ -274,15 +274,15 @@ tsne_status launch_cand_tc(const __half* Xh, const float* nrm, int N, int Dp, in
       set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
       return TSNE_ERR_CUDA;
     }
-    return launch_cand_tc2(map, map_b, nrm, N, Dp, Kc, buf, cand, slots, sync, s);
+    return launch_cand_tc2(map, map_b, nrm, N, q0, nq, Dp, Kc, buf, cand, slots, sync, s);
   }
   TSNE_CUDA_TRY(cudaFuncSetAttribute(k_cand_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)TC_SMEM));
-  int nrb = (N + TC_BM - 1) / TC_BM;
+  int nrb = (nq + TC_BM - 1) / TC_BM;
   int grid = nrb < kNumSMs ? nrb : kNumSMs;
   if (grid > slots) grid = slots;
-  if (sync) TSNE_CUDA_TRY(cudaMemsetAsync(sync, 0, sizeof(unsigned) * knn_tc_sync_words(N), s));
-  k_cand_tc<<<grid, TC_THREADS, TC_SMEM, s>>>(map, nrm, N, Dp, Kc, buf, cand,
+  if (sync) TSNE_CUDA_TRY(cudaMemsetAsync(sync, 0, sizeof(unsigned) * knn_tc_sync_words(N, nq), s));
+  k_cand_tc<<<grid, TC_THREADS, TC_SMEM, s>>>(map, nrm, N, q0, nq, Dp, Kc, buf, cand,
                                                grid == kNumSMs ? sync : nullptr);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;

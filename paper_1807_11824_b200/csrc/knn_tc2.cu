@@ -39,7 +39,7 @@ constexpr size_t P_SMEM = 1024 + P_STAGES * P_STAGE_BYTES + 256 + 4 * P_CAP * 8;
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_b,
-           const float* __restrict__ nrm, int N, int Dp,
+           const float* __restrict__ nrm, int N, int q0, int nq, int Dp,
            int Kc, u64* __restrict__ buf, u64* __restrict__ cand, unsigned* __restrict__ sync,
            int dbg_skip_epilogue) {
   extern __shared__ unsigned char smraw[];
@@ -57,7 +57,7 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npair_grid = gridDim.x >> 1;
   const int nkb = Dp / P_BK;
-  const int nrb = (N + P_BM - 1) / P_BM, npairs = (nrb + 1) / 2, nct = (N + P_BN - 1) / P_BN;
+  const int nrb = (nq + P_BM - 1) / P_BM, npairs = (nrb + 1) / 2, nct = (N + P_BN - 1) / P_BN;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < P_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -105,7 +105,7 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
             const uint32_t full_c = mapa_shared(smem_u32(&full[stage]), 0);
             if (leader) mbar_arrive_tx(&full[stage], 2 * P_STAGE_BYTES);
             unsigned char* sa = base + stage * P_STAGE_BYTES;
-            tma_load_2d_pair(sa, &tmap, full_c, kb * P_BK, rb * P_BM);
+            tma_load_2d_pair(sa, &tmap, full_c, kb * P_BK, q0 + rb * P_BM);
             tma_load_2d_pair(sa + P_A_BYTES, &tmap_b, full_c, kb * P_BK, ct * P_BN + (int)rank * (P_BN / 2));
             if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
           }
@@ -155,8 +155,8 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
     uint32_t aphase = 0;
     for (int pp = pair; pp < npairs; pp += npair_grid) {
       const int rb = 2 * pp + (int)rank;
-      const int q = rb * P_BM + rl;
-      const bool qok = q < N;
+      const int q = q0 + rb * P_BM + rl;         // global query index
+      const bool qok = rb * P_BM + rl < nq;
       int cnt = 0;
       u64 tau = kKeyMax;
       for (int ct = 0; ct < nct; ++ct) {
@@ -224,7 +224,7 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
       __syncwarp();
       for (int l = 0; l < 32; ++l) {
         const int ql = rb * P_BM + e * 32 + l;
-        if (ql >= N) break;
+        if (ql >= nq) break;
         const int n = __shfl_sync(0xffffffffu, cnt, l);
         u64* rb_l = buf + ((size_t)blockIdx.x * P_BM + e * 32 + l) * P_CAP;
         u64 t;
@@ -244,23 +244,23 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
 
 int knn_tc2_b_rows() { return P_BN / 2; }
 
-size_t knn_tc2_sync_words(int64_t N) {
-  const int64_t nrb = (N + P_BM - 1) / P_BM, npairs = (nrb + 1) / 2, nct = (N + P_BN - 1) / P_BN;
+size_t knn_tc2_sync_words(int64_t N, int64_t nq) {
+  const int64_t nrb = (nq + P_BM - 1) / P_BM, npairs = (nrb + 1) / 2, nct = (N + P_BN - 1) / P_BN;
   const int64_t waves = (npairs + kNumSMs / 2 - 1) / (kNumSMs / 2);
   return (size_t)(waves * ((nct + P_SYNC_EVERY - 1) / P_SYNC_EVERY) + 1);
 }
 
-tsne_status launch_cand_tc2(const CUtensorMap& map, const CUtensorMap& map_b, const float* nrm, int N, int Dp, int Kc,
+tsne_status launch_cand_tc2(const CUtensorMap& map, const CUtensorMap& map_b, const float* nrm, int N, int q0, int nq, int Dp, int Kc,
                             unsigned long long* buf, unsigned long long* cand, int slots,
                             unsigned* sync, cudaStream_t s) {
   TSNE_CUDA_TRY(cudaFuncSetAttribute(k_cand_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)P_SMEM));
-  const int nrb = (N + P_BM - 1) / P_BM, npairs = (nrb + 1) / 2;
+  const int nrb = (nq + P_BM - 1) / P_BM, npairs = (nrb + 1) / 2;
   int grid = 2 * (npairs < kNumSMs / 2 ? npairs : kNumSMs / 2);
   if (grid > slots) grid = slots & ~1;
-  if (sync) TSNE_CUDA_TRY(cudaMemsetAsync(sync, 0, sizeof(unsigned) * knn_tc2_sync_words(N), s));
+  if (sync) TSNE_CUDA_TRY(cudaMemsetAsync(sync, 0, sizeof(unsigned) * knn_tc2_sync_words(N, nq), s));
   const char* dbg = getenv("TSNE_KNN_DEBUG_NO_EPILOGUE");
-  k_cand_tc2<<<grid, P_THREADS, P_SMEM, s>>>(map, map_b, nrm, N, Dp, Kc, buf, cand,
+  k_cand_tc2<<<grid, P_THREADS, P_SMEM, s>>>(map, map_b, nrm, N, q0, nq, Dp, Kc, buf, cand,
                                               grid == kNumSMs ? sync : nullptr, dbg ? 1 : 0);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;

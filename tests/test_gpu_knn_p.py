@@ -22,12 +22,12 @@ def T():
     return T
 
 
-def check_knn(orc, X, idx_g, d2_g, idx_o, d2_o):
+def check_knn(orc, X, idx_g, d2_g, idx_o, d2_o, q0=0):
     np.testing.assert_allclose(d2_g, d2_o, rtol=1e-10, atol=0)
     bad = np.argwhere(idx_g != idx_o)
     for r, c in bad:
         # a swap is only allowed between near-tied distances (< 1e-6 relative)
-        dj = orc.sqdist(X, r, idx_g[r, c])
+        dj = orc.sqdist(X, q0 + r, idx_g[r, c])
         assert abs(dj - d2_o[r, c]) <= 1e-6 * max(d2_o[r, c], 1e-300), (r, c)
     return len(bad)
 
@@ -54,6 +54,28 @@ def test_knn_tcgen05_vs_cudacore_path(T, cfg, n, K, monkeypatch):
     assert it["gemm_path"] == "tcgen05" and is_["gemm_path"] == "cuda-core"
     assert torch.equal(d2_t, d2_s) and torch.equal(idx_t, idx_s)
     assert it["rows_uncertified"] == 0 and is_["rows_uncertified"] == 0
+
+
+@pytest.mark.parametrize("path", ["tc2", "tc1", "simt"])
+@pytest.mark.parametrize("q0,q1", [(0, 4100), (1000, 2777), (129, 130), (3967, 4100), (5, 5)])
+def test_knn_rows_equal_full(T, orc, path, q0, q1, monkeypatch):
+    """tsne_knn_rows (the multi-GPU shard of the kNN by query row) gives the
+    rows q0..q1-1 of tsne_knn, bit for bit, on every candidate path."""
+    X = torch.as_tensor(synth.make_x("C2", n=4100).numpy(), device="cuda")
+    if path != "tc2":
+        monkeypatch.setenv("TSNE_KNN_PATH", path)
+    idx, d2, _ = T.knn(X, 90)
+    il, dl, info = T.knn(X, 90, rows=(q0, q1))
+    assert il.shape == (q1 - q0, 90)
+    assert torch.equal(il, idx[q0:q1]) and torch.equal(dl, d2[q0:q1])
+    assert info["rows_uncertified"] == 0
+
+
+def test_knn_rows_vs_oracle(T, orc):
+    X = synth.make_x("C5", n=3000).numpy()
+    il, dl, _ = T.knn(torch.as_tensor(X, device="cuda"), 90, rows=(1234, 2345))
+    idx_o, d2_o = orc.knn(X, 90, rows=np.arange(1234, 2345))
+    check_knn(orc, X, il.cpu().numpy(), dl.cpu().numpy(), idx_o, d2_o, q0=1234)
 
 
 def test_knn_duplicates_tie_by_index(T, orc):
