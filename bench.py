@@ -9,7 +9,7 @@ section 7).  The supporting kNN and P stages run once before the timed loop
 (tsne_run from pinned host X to host Y).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C5] [--n N_override] [--no-e2e] [--no-cpu]
+                    [--config C5] [--npoints N_override] [--no-e2e] [--no-cpu]
 
 `--impl reference` times the fp64 CPU oracle (oracle/) on the host cores, one
 full-size oracle iteration per step.  Rank 0 prints one JSON line.
@@ -185,7 +185,7 @@ def run_e2e_sharded(Xh_local, cfg, N, args, rank, world, dev):
 
 def run_ours(args, rank, world):
     import paper_1807_11824_b200 as T
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     cfg = synth.CONFIGS[args.config]
     N = args.n or cfg.N
@@ -359,7 +359,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--npoints", "--n", dest="n", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=2)
@@ -373,7 +373,9 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if world > 1:
-        torch.distributed.init_process_group("nccl")
+        # TSNE_BENCH_BACKEND=gloo: exercise the N>1 code path with several
+        # ranks on one GPU (functional check only; NCCL is the measured path)
+        torch.distributed.init_process_group(os.environ.get("TSNE_BENCH_BACKEND", "nccl"))
     run_ours(args, rank, world)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -47,8 +47,13 @@ def local_csr(row_ptr: torch.Tensor, col: torch.Tensor, val: torch.Tensor, row0:
 def _all_gather_flat(out: torch.Tensor, inp: torch.Tensor, group=None):
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, inp, group=group)
-    else:
+    else:                       # gloo (CPU tests; CUDA tensors staged through the host)
         world = dist.get_world_size(group)
+        if inp.is_cuda:
+            host = torch.empty(out.shape, dtype=out.dtype)
+            _all_gather_flat(host, inp.cpu(), group)
+            out.copy_(host)
+            return
         parts = list(out.chunk(world))
         dist.all_gather(parts, inp, group=group)
 
