@@ -18,6 +18,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "knn.cuh"
 #include "knn_select.cuh"
 #include "knn_tc.cuh"
@@ -56,6 +58,15 @@ void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K) {
   w.rows_bad = c.take<int32_t>(N);
   w.sync = c.take<unsigned>(knn_tc_sync_words(N, N) > knn_tc2_sync_words(N, N) ? knn_tc_sync_words(N, N)
                                                                            : knn_tc2_sync_words(N, N));
+  w.sd = c.take<double>((size_t)kScanRows * N);
+  w.sd_alt = c.take<double>(N);
+  w.si = c.take<int32_t>(N);
+  w.si_alt = c.take<int32_t>(N);
+  cub::DoubleBuffer<double> dk(nullptr, nullptr);
+  cub::DoubleBuffer<int32_t> dv(nullptr, nullptr);
+  w.sort_tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, w.sort_tmp_bytes, dk, dv, (int)N);
+  w.sort_tmp = c.take<unsigned char>(w.sort_tmp_bytes);
 }
 
 // ---------------------------------------------------------------- prep
@@ -257,7 +268,7 @@ k_rerank(const float* __restrict__ X, int N, int qs, int nq, int D, int K, int K
          const u64* __restrict__ cand,
          const float* __restrict__ nrm, const float* __restrict__ scale,
          int32_t* __restrict__ idx, double* __restrict__ d2, u64* __restrict__ uncert,
-         int32_t* __restrict__ rows_bad) {
+         int32_t* __restrict__ rows_bad, int force_mod) {
   __shared__ double s_d[kRR_Threads / 32][256];
   __shared__ int s_j[kRR_Threads / 32][256];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -314,12 +325,74 @@ k_rerank(const float* __restrict__ X, int N, int qs, int nq, int D, int K, int K
   }
   if (lane == 0) {
     const bool all = (Kc >= N - 1);
-    const bool cert = all || (sd[K - 1] < tau_approx - 2.0 * emax);
+    bool cert = all || (sd[K - 1] < tau_approx - 2.0 * emax);
+    if (force_mod > 0 && i % force_mod == 0) cert = false;   // test hook (fallback coverage)
     if (!cert) {
       const u64 pos = atomicAdd(uncert, 1ull);
       rows_bad[pos] = i;
     }
   }
+}
+
+// ---------------------------------------------------------------- exact fallback (D26)
+// Rows whose candidate margin could not be certified: fp64 distances to all N
+// points, in the re-rank's own arithmetic (lane-strided fma, fixed butterfly),
+// so a row gets the same d2 values either way; then a stable radix sort of
+// (d2, index) -- ties by the lower index (D18).  Self -> +inf (sorted last).
+__global__ void __launch_bounds__(256)
+k_scan_dist(const float* __restrict__ X, int N, int D, const int32_t* __restrict__ rows, int nr,
+            double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < N; j += nw) {
+    const float* xj = X + (size_t)j * D;
+    for (int r = 0; r < nr; ++r) {
+      const int i = rows[r];
+      const float* xi = X + (size_t)i * D;
+      double acc = 0.0;
+      for (int d = lane; d < D; d += 32) {
+        const double t = (double)__ldg(xi + d) - (double)xj[d];
+        acc = fma(t, t, acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) out[(size_t)r * N + j] = (j == i) ? (double)INFINITY : acc;
+    }
+  }
+}
+
+__global__ void k_iota(int32_t* __restrict__ v, int n) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) v[k] = k;
+}
+
+__global__ void k_scan_emit(const double* __restrict__ dk, const int32_t* __restrict__ dv, int K,
+                            int32_t* __restrict__ idx, double* __restrict__ d2) {
+  for (int c = threadIdx.x; c < K; c += blockDim.x) { idx[c] = dv[c]; d2[c] = dk[c]; }
+}
+
+static tsne_status exact_fallback(const float* X, int64_t N, int32_t D, int32_t K, int64_t q0,
+                                  const int32_t* rows_host, int64_t nbad, int32_t* idx, double* d2,
+                                  KnnWS& w, cudaStream_t s) {
+  for (int64_t r0 = 0; r0 < nbad; r0 += kScanRows) {
+    const int nr = (int)((nbad - r0 < kScanRows) ? nbad - r0 : kScanRows);
+    TSNE_CUDA_TRY(cudaMemcpyAsync(w.si_alt, rows_host + r0, nr * sizeof(int32_t),
+                                  cudaMemcpyHostToDevice, s));
+    k_scan_dist<<<8 * kNumSMs, 256, 0, s>>>(X, (int)N, D, w.si_alt, nr, w.sd);
+    TSNE_LAUNCH_CHECK();
+    TSNE_CUDA_TRY(cudaStreamSynchronize(s));   // si_alt is reused as a sort buffer below
+    for (int r = 0; r < nr; ++r) {
+      k_iota<<<2 * kNumSMs, 256, 0, s>>>(w.si, (int)N);
+      TSNE_LAUNCH_CHECK();
+      cub::DoubleBuffer<double> dk(w.sd + (size_t)r * N, w.sd_alt);
+      cub::DoubleBuffer<int32_t> dv(w.si, w.si_alt);
+      size_t tb = w.sort_tmp_bytes;
+      TSNE_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, dk, dv, (int)N, 0, 64, s));
+      const int64_t il = rows_host[r0 + r] - q0;
+      k_scan_emit<<<1, 256, 0, s>>>(dk.Current(), dv.Current(), K, idx + (size_t)il * K,
+                                   d2 + (size_t)il * K);
+      TSNE_LAUNCH_CHECK();
+    }
+  }
+  return TSNE_OK;
 }
 
 // ---------------------------------------------------------------- host
@@ -357,14 +430,35 @@ tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int64_t q0,
     TSNE_LAUNCH_CHECK();
   }
   w.path = tc ? 1 : 0;
+  const char* fm = getenv("TSNE_KNN_FORCE_FALLBACK");      // test hook: every fm-th row
+  const int force_mod = fm ? atoi(fm) : 0;
   k_rerank<<<(int)((nq + 7) / 8), kRR_Threads, 0, s>>>(X, (int)N, (int)q0, (int)nq, D, K, Kc,
                                                       w.cand, w.nrm, w.scale,
-                                                     idx, d2, w.uncert, w.rows_bad);
+                                                     idx, d2, w.uncert, w.rows_bad, force_mod);
   TSNE_LAUNCH_CHECK();
+  // uncertified rows (D26): exact fp64 scan of the whole data set
+  u64 h = 0;
+  TSNE_CUDA_TRY(cudaMemcpyAsync(&h, w.uncert, sizeof(h), cudaMemcpyDeviceToHost, s));
+  TSNE_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h > 0) {
+    int32_t* rows = (int32_t*)malloc(h * sizeof(int32_t));
+    if (!rows) {
+      set_error("host allocation failed");
+      return TSNE_ERR_CUDA;
+    }
+    cudaError_t e = cudaMemcpy(rows, w.rows_bad, h * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    tsne_status st = (e == cudaSuccess) ? exact_fallback(X, N, D, K, q0, rows, (int64_t)h, idx,
+                                                          d2, w, s)
+                                        : TSNE_ERR_CUDA;
+    if (e != cudaSuccess) set_error("cudaMemcpy: %s", cudaGetErrorString(e));
+    if (st == TSNE_OK) {
+      e = cudaStreamSynchronize(s);     // `rows` is read by the async H2D copies above
+      if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); st = TSNE_ERR_CUDA; }
+    }
+    free(rows);
+    if (st != TSNE_OK) return st;
+  }
   if (info) {
-    u64 h = 0;
-    TSNE_CUDA_TRY(cudaMemcpyAsync(&h, w.uncert, sizeof(h), cudaMemcpyDeviceToHost, s));
-    TSNE_CUDA_TRY(cudaStreamSynchronize(s));
     info->rows_uncertified = (int64_t)h;
     info->candidates = Kc;
     info->gemm_path = w.path;

@@ -26,8 +26,16 @@ struct KnnWS {
   unsigned long long* uncert = nullptr;  // [0] count of uncertified rows
   int32_t* rows_bad = nullptr;    // list of uncertified rows (N)
   unsigned* sync = nullptr;       // CTA checkpoint counters of the tcgen05 sweep
+  // exact fallback scan of uncertified rows (D26): kScanRows rows at a time
+  double* sd = nullptr;           // kScanRows x N fp64 distances
+  double* sd_alt = nullptr;       // N (radix-sort double buffer)
+  int32_t* si = nullptr;          // N point indices
+  int32_t* si_alt = nullptr;      // N
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
   int32_t path = 0;
 };
+constexpr int kScanRows = 8;
 
 void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K);
 // Neighbours of the query rows [q0, q0 + nq) among all N points; idx / d2 are

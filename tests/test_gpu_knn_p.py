@@ -71,6 +71,25 @@ def test_knn_rows_equal_full(T, orc, path, q0, q1, monkeypatch):
     assert info["rows_uncertified"] == 0
 
 
+@pytest.mark.parametrize("rows", [None, (1000, 2777)])
+def test_knn_exact_fallback_scan(T, orc, rows, monkeypatch):
+    """D26: rows that fail the candidate certificate are redone by the exact
+    fp64 scan of all N points -- forced here on every 7th row; the result is
+    the same kNN, bit for bit (same fp64 arithmetic), and the oracle's."""
+    Xn = synth.make_x("C2", n=4100).numpy()
+    X = torch.as_tensor(Xn, device="cuda")
+    idx, d2, info = T.knn(X, 90, rows=rows)
+    assert info["rows_uncertified"] == 0
+    monkeypatch.setenv("TSNE_KNN_FORCE_FALLBACK", "7")
+    idx_f, d2_f, info_f = T.knn(X, 90, rows=rows)
+    q0, q1 = rows if rows else (0, 4100)
+    assert info_f["rows_uncertified"] == len(range((q0 + 6) // 7 * 7, q1, 7))
+    assert torch.equal(idx, idx_f) and torch.equal(d2, d2_f)
+    sel = np.arange((q0 + 6) // 7 * 7, q1, 7)[:40]
+    idx_o, d2_o = orc.knn(Xn, 90, rows=sel)
+    check_knn(orc, Xn, idx_f.cpu().numpy()[sel - q0], d2_f.cpu().numpy()[sel - q0], idx_o, d2_o)
+
+
 def test_knn_rows_vs_oracle(T, orc):
     X = synth.make_x("C5", n=3000).numpy()
     il, dl, _ = T.knn(torch.as_tensor(X, device="cuda"), 90, rows=(1234, 2345))
