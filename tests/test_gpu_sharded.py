@@ -97,3 +97,28 @@ def test_nccl_world1_sharded_optimizer(T, prob):
         assert rel(Y.cpu().numpy(), Yref.cpu().numpy().astype(np.float64)) < 1e-4
     finally:
         dist.destroy_process_group()
+
+
+def test_nccl_world1_sharded_run_end_to_end(T):
+    """sharded.run (X shard H2D + all-gather, tsne_knn_rows, gathered lists, P,
+    sharded iterations) against tsne_run_ex on the same pinned host X."""
+    from paper_1807_11824_b200 import sharded
+    X = synth.make_x("C2", n=3000)
+    Xh = torch.empty(X.shape, dtype=torch.float32, pin_memory=True)
+    Xh.copy_(X)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        Yh = torch.empty(3000, 2, dtype=torch.float32, pin_memory=True)
+        Y, info = sharded.run(Xh, 3000, perplexity=30.0, theta=0.5, n_iter=5, Y_out=Yh,
+                              device=torch.device("cuda"))
+        torch.cuda.synchronize()
+        assert info["K"] == 90 and info["knn_rows_uncertified"] == 0
+        Yr, rinfo = T.run(Xh, perplexity=30.0, theta=0.5, n_iter=5, relabel_every=0,
+                          use_graphs=False)
+        assert rinfo["nnz"] == info["nnz"]
+        assert torch.equal(Yh, Y.cpu())
+        assert rel(Yh.numpy(), Yr.numpy().astype(np.float64)) < 1e-4
+    finally:
+        dist.destroy_process_group()
