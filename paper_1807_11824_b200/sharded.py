@@ -115,7 +115,7 @@ class ShardedOptimizer:
 
     def __init__(self, row_ptr_local, col_local, val_local, Y0: torch.Tensor, theta=0.5,
                  learning_rate=200.0, exaggeration=12.0, exag_iters=250, mom0=0.5, mom1=0.8,
-                 min_gain=0.01, group=None, ops=None, cfg=None):
+                 min_gain=0.01, group=None, ops=None, cfg=None, use_graphs=True):
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -144,16 +144,36 @@ class ShardedOptimizer:
         self.theta, self.lr, self.exag = theta, learning_rate, exaggeration
         self.t = 0
         self.pending_recentre = False
+        self.exag_iters = int(cfg.exag_iters)
+        # CUDA graphs of the steady-state iteration (kernels + both NCCL
+        # exchanges), one per schedule phase: t < exag_iters and after (the
+        # iteration number only selects alpha and the momentum, D13)
+        self.use_graphs = (use_graphs and dev.type == "cuda" and ops is None
+                           and dist.get_backend(group) == "nccl")
+        self._graphs = {}
+
+    def _iteration(self):
+        self.ops.forces(self.Y, self.N, self.row0, self.row1, self.theta,
+                        self.pending_recentre, self.rep, self.zpart)
+        _all_gather_flat(self.zparts, self.zpart, self.group)
+        self.ops.update(self.rp, self.col, self.val, self.N, self.row0, self.row1, self.Y,
+                        self.rep, self.zparts, self.world, self.t, self.lr, self.exag,
+                        self.cfg, self.v, self.g, self.Yloc)
+        _all_gather_flat(self.Yfull, self.Yloc, self.group)
 
     def step(self, n_iter: int = 1):
         for _ in range(n_iter):
-            self.ops.forces(self.Y, self.N, self.row0, self.row1, self.theta,
-                            self.pending_recentre, self.rep, self.zpart)
-            _all_gather_flat(self.zparts, self.zpart, self.group)
-            self.ops.update(self.rp, self.col, self.val, self.N, self.row0, self.row1, self.Y,
-                            self.rep, self.zparts, self.world, self.t, self.lr, self.exag,
-                            self.cfg, self.v, self.g, self.Yloc)
-            _all_gather_flat(self.Yfull, self.Yloc, self.group)
+            if self.use_graphs and self.pending_recentre:
+                phase = int(self.t >= self.exag_iters)
+                g = self._graphs.get(phase)
+                if g is None:
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                        self._iteration()          # captured, not run
+                    self._graphs[phase] = g
+                g.replay()
+            else:
+                self._iteration()
             self.t += 1
             self.pending_recentre = True
 

@@ -95,6 +95,16 @@ def test_nccl_world1_sharded_optimizer(T, prob):
         Yref = ref.step(3)
         assert torch.isfinite(Y).all()
         assert rel(Y.cpu().numpy(), Yref.cpu().numpy().astype(np.float64)) < 1e-4
+        # graph-replayed iterations (both schedule phases) == eager, bitwise
+        cfg = T.default_config(exag_iters=4)
+        a = ShardedOptimizer(*local_csr(rp_d, col_d, val_d, 0, N), Y0, theta=0.5, cfg=cfg)
+        b = ShardedOptimizer(*local_csr(rp_d, col_d, val_d, 0, N), Y0, theta=0.5, cfg=cfg,
+                             use_graphs=False)
+        assert a.use_graphs and not b.use_graphs
+        a.step(7)
+        b.step(7)
+        assert len(a._graphs) == 2
+        assert torch.equal(a.embedding(), b.embedding())
     finally:
         dist.destroy_process_group()
 
