@@ -15,11 +15,20 @@
 // Per-point sums: z_i += N_c w, f_i += N_c w^2 (y_i - y_c), w = 1/(1+D^2)
 // (P:L132 cell formula; P:L134 simultaneous Z).  Z = sum z_i in fp64 with a
 // fixed reduction order (deterministic).
+#include <cstdio>
+#include <cstdlib>
+
 #include "tree.cuh"
 
 namespace tsne {
 
 constexpr int kTravThreads = 256;
+
+// diagnostics (TSNE_TRAV_STATS=1): [0] sum of node visits, [1] sum over warps
+// of the warp's max visits, [2] accepted cells + exact pairs, [3] fp64 re-tests
+__device__ unsigned long long g_trav_stats[4];
+
+static int trav_stats_on() { return getenv("TSNE_TRAV_STATS") ? 1 : 0; }
 
 int traverse_blocks(int64_t N) { return (int)((N + kTravThreads - 1) / kTravThreads); }
 
@@ -46,7 +55,8 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            const int32_t* __restrict__ nnodes_p, int N, const BoxInfo* __restrict__ box,
            float theta, float2* __restrict__ rep, double* __restrict__ zpart,
            unsigned* __restrict__ counter, double* __restrict__ Zout,
-           const int32_t* __restrict__ list, const int32_t* __restrict__ nlist, int row0) {
+           const int32_t* __restrict__ list, const int32_t* __restrict__ nlist, int row0,
+           int stats) {
   // list (multi-GPU): the sorted positions of the points this rank owns
   // (original indices [row0, ...)); rep is then indexed by perm[k] - row0.
   // per level l: {r^2 (fp32), margin constant A_l, margin slope B_l}, r^2 (fp64)
@@ -84,7 +94,9 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   double z = 0.0;   // fp64: Z sums up to N^2 terms of very different size
 
   const uint32_t lv_base = (uint32_t)__cvta_generic_to_shared(s_lv);
+  unsigned n_visit = 0, n_take = 0, n_f64 = 0;
   while (cur < nnodes) {
+    if (stats) ++n_visit;
     const float4 nd = __ldg(nodes + cur);
     const uint32_t sw = __float_as_uint(nd.w);
     const int lvl = (int)(sw >> 27);
@@ -102,8 +114,10 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
     const float diff = lhs - lv.x;
     const float marg = fmaf(lv.z, lhs, lv.y);
     bool acc = diff > marg;
-    if (!leaf && !self_in && fabsf(diff) <= marg)     // inside the band: decide in fp64
+    if (!leaf && !self_in && fabsf(diff) <= marg) {   // inside the band: decide in fp64
       acc = accept_fp64(com64 + cur, yi, s_r2d[lvl], theta2d);
+      if (stats) ++n_f64;
+    }
     // exact leaf of one point: the exact pair; internal cell: the criterion;
     // a cell containing i is opened (D11)
     const bool take = !self_in && (leaf ? cntf == 1.f : acc);
@@ -112,6 +126,7 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
     cur = (take || leaf || bucket) ? skip : cur + 1;
     const float w = rcp_approx(1.f + D2);
     const float nw = take ? cntf * w : 0.f;
+    if (stats && take) ++n_take;
     z += (double)nw;
     const float nww = nw * w;
     fx = fmaf(nww, dx, fx);
@@ -132,6 +147,22 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
     }
   }
   if (active) rep[perm[k] - row0] = make_float2(fx, fy);
+  if (stats) {
+    unsigned long long sv = n_visit, st = n_take, sf = n_f64;
+    unsigned mv = n_visit;
+    for (int o = 16; o > 0; o >>= 1) {
+      sv += __shfl_xor_sync(0xffffffffu, sv, o);
+      st += __shfl_xor_sync(0xffffffffu, st, o);
+      sf += __shfl_xor_sync(0xffffffffu, sf, o);
+      mv = max(mv, __shfl_xor_sync(0xffffffffu, mv, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&g_trav_stats[0], sv);
+      atomicAdd(&g_trav_stats[1], (unsigned long long)mv * 32ull);
+      atomicAdd(&g_trav_stats[2], st);
+      atomicAdd(&g_trav_stats[3], sf);
+    }
+  }
 
   // Z: fixed-order fp64 reduction without a block barrier: the last warp of
   // the block to finish sums the block, the last block sums the blocks.
@@ -170,8 +201,17 @@ tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s) {
   const int N = (int)w.N;
   k_traverse<<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
-      w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0);
+      w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0, trav_stats_on());
   TSNE_LAUNCH_CHECK();
+  if (trav_stats_on()) {
+    unsigned long long h[4];
+    TSNE_CUDA_TRY(cudaMemcpyFromSymbolAsync(h, g_trav_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, s));
+    TSNE_CUDA_TRY(cudaStreamSynchronize(s));
+    fprintf(stderr, "traverse stats: visits/pt %.1f  warp-max visits/pt %.1f  interactions/pt %.1f  fp64/pt %.3f\n",
+            h[0] / (double)N, h[1] / (double)N, h[2] / (double)N, h[3] / (double)N);
+    const unsigned long long zero[4] = {0, 0, 0, 0};
+    TSNE_CUDA_TRY(cudaMemcpyToSymbolAsync(g_trav_stats, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s));
+  }
   return TSNE_OK;
 }
 
@@ -181,7 +221,7 @@ tsne_status launch_traverse_list(TreeWS& w, float theta, const int32_t* list, co
   const int N = (int)w.N;
   k_traverse<<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta,
-      rep_local, w.zpart, w.counter + 1, z_partial, list, nlist, row0);
+      rep_local, w.zpart, w.counter + 1, z_partial, list, nlist, row0, 0);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }
