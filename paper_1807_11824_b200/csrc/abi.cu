@@ -1,6 +1,7 @@
 // abi.cu -- extern "C" entry points of include/tsne.h: argument validation,
 // workspace carving, stream plumbing.  All compute is in the kernels of
 // tree.cu, traverse.cu, attract.cu, optimize.cu, knn.cu, affinity.cu.
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -510,11 +511,21 @@ tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, 
   ws_need = ws_need > ob ? ws_need : ob;
   plan.take<char>(ws_need);
   void* mem = nullptr;
-  cudaError_t e = cudaMallocAsync(&mem, plan.bytes(), s);
+  const bool timing = getenv("TSNE_RUN_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t0 = now();
+  // plain cudaMalloc: for tens of GB it maps in milliseconds, where the
+  // stream-ordered pool took 0.3-1 s to map and 0.3-5 s to release (measured)
+  cudaError_t e = cudaMalloc(&mem, plan.bytes());
+  if (timing) {
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "tsne_run: alloc %.1f GB %.1f ms\n", plan.bytes() / 1e9,
+            std::chrono::duration<double, std::milli>(now() - t0).count());
+  }
   if (e != cudaSuccess) {
     for (auto& x : ev) cudaEventDestroy(x);
     cudaStreamDestroy(s);
-    set_error("cudaMallocAsync(%zu): %s", plan.bytes(), cudaGetErrorString(e));
+    set_error("cudaMalloc(%zu): %s", plan.bytes(), cudaGetErrorString(e));
     return TSNE_ERR_CUDA;
   }
   Carver c(mem);
@@ -587,8 +598,15 @@ tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, 
     if (e != cudaSuccess) { set_error("Y_out copy: %s", cudaGetErrorString(e)); st = TSNE_ERR_CUDA; }
   }
   cudaEventRecord(ev[5], s);
-  cudaFreeAsync(mem, s);
+  auto t1 = now();
+  if (timing) cudaStreamSynchronize(s);
+  auto t2 = now();
   e = cudaStreamSynchronize(s);
+  cudaFree(mem);
+  if (timing)
+    fprintf(stderr, "tsne_run: tail sync %.1f ms, free %.1f ms\n",
+            std::chrono::duration<double, std::milli>(t2 - t1).count(),
+            std::chrono::duration<double, std::milli>(now() - t2).count());
   if (st == TSNE_OK && e != cudaSuccess) {
     set_error("tsne_run: %s", cudaGetErrorString(e));
     st = TSNE_ERR_CUDA;

@@ -17,6 +17,7 @@
 #include <cfloat>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -66,7 +67,34 @@ void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K) {
   cub::DoubleBuffer<int32_t> dv(nullptr, nullptr);
   w.sort_tmp_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, w.sort_tmp_bytes, dk, dv, (int)N);
+  {
+    cub::DoubleBuffer<uint32_t> ck(nullptr, nullptr);
+    size_t b2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b2, ck, dv, (int)N);
+    if (b2 > w.sort_tmp_bytes) w.sort_tmp_bytes = b2;
+  }
   w.sort_tmp = c.take<unsigned char>(w.sort_tmp_bytes);
+  // symmetric search buffers (used by full-N calls with enough super-blocks)
+  w.sym = N >= 4 * 256;
+  if (w.sym) {
+    w.C = (int32_t)(N / 64 < kSymCells ? N / 64 : kSymCells);
+    w.Xs = c.take<__half>((size_t)(w.C + 256) * w.Dp);
+    w.nrm_s = c.take<float>(w.C + 256);
+    w.cand32 = c.take<u64>((size_t)N * 32);
+    w.cell = c.take<uint32_t>(2 * (size_t)N);
+    w.perm = c.take<int32_t>(2 * (size_t)N);
+    w.inv = c.take<int32_t>(N);
+    w.Xp = c.take<__half>((size_t)(N + 256) * w.Dp);
+    w.nrm_p = c.take<float>(N + 256);
+    w.tau = c.take<float>(N + 256);
+    w.ntau = c.take<float>(N + 256);
+    w.cnt = c.take<unsigned>(N);
+    w.list = c.take<u64>((size_t)N * kSymCap);
+    w.fb = c.take<int32_t>(N);
+    w.Xq = c.take<__half>((size_t)(kFbRows + 256) * w.Dp);
+    w.candfb = c.take<u64>((size_t)kFbRows * w.Kc);
+    w.misc = c.take<unsigned>(4);
+  }
 }
 
 // ---------------------------------------------------------------- prep
@@ -268,7 +296,10 @@ k_rerank(const float* __restrict__ X, int N, int qs, int nq, int D, int K, int K
          const u64* __restrict__ cand,
          const float* __restrict__ nrm, const float* __restrict__ scale,
          int32_t* __restrict__ idx, double* __restrict__ d2, u64* __restrict__ uncert,
-         int32_t* __restrict__ rows_bad, int force_mod) {
+         int32_t* __restrict__ rows_bad, int force_mod, const int32_t* __restrict__ perm,
+         const int32_t* __restrict__ inv) {
+  // perm / inv (nullable): the candidates are stored by locality position
+  // (symmetric search) with locality-position indices in their keys
   __shared__ double s_d[kRR_Threads / 32][256];
   __shared__ int s_j[kRR_Threads / 32][256];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -278,13 +309,13 @@ k_rerank(const float* __restrict__ X, int N, int qs, int nq, int D, int K, int K
   double* sd = s_d[wid];
   int* sj = s_j[wid];
   const float* xi = X + (size_t)i * D;
-  const u64* ci = cand + (size_t)il * Kc;
+  const u64* ci = cand + (size_t)(inv ? inv[i] : il) * Kc;
   const double inv2 = (double)scale[1];
   const double nrm_i = (double)nrm[i];
   double emax = 0.0;
   for (int c = 0; c < Kc; ++c) {
     const u64 key = ci[c];
-    const int j = key_idx(key);
+    const int j = perm ? perm[key_idx(key)] : key_idx(key);
     const float* xj = X + (size_t)j * D;
     double acc = 0.0;
     for (int d = lane; d < D; d += 32) {
@@ -395,6 +426,234 @@ static tsne_status exact_fallback(const float* X, int64_t N, int32_t D, int32_t 
   return TSNE_OK;
 }
 
+// ---------------------------------------------------------------- symmetric search (knn_sym.cu)
+__global__ void k_gather_rows(const __half* __restrict__ src, const float* __restrict__ nsrc,
+                              const int32_t* __restrict__ idx, int64_t n, int64_t n_pad, int Dp,
+                              __half* __restrict__ dst, float* __restrict__ ndst) {
+  // warp per destination row; rows n .. n_pad-1 are zero (tile overrun)
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= n_pad) return;
+  const uint4* s4 = r < n ? reinterpret_cast<const uint4*>(src + (size_t)idx[r] * Dp) : nullptr;
+  uint4* d4 = reinterpret_cast<uint4*>(dst + (size_t)r * Dp);
+  for (int k = lane; k < Dp / 8; k += 32) d4[k] = s4 ? s4[k] : make_uint4(0, 0, 0, 0);
+  if (lane == 0) ndst[r] = r < n ? nsrc[idx[r]] : 0.f;
+}
+
+__global__ void k_sample_idx(int32_t* __restrict__ idx, int C, int64_t N) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < C) idx[k] = (int32_t)((int64_t)k * N / C);
+}
+
+// sort key of point i: the tour rank of its cell (nearest sample)
+__global__ void k_cells(const u64* __restrict__ cand32, int64_t N, int cbits,
+                        const int32_t* __restrict__ group, uint32_t* __restrict__ cell,
+                        int32_t* __restrict__ ids, const float* __restrict__ nrm,
+                        unsigned* __restrict__ misc) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t cl = (uint32_t)key_idx(cand32[(size_t)i * 32]);
+    cell[i] = ((uint32_t)group[cl] << cbits);   // the cell's rank in the tour
+    ids[i] = (int32_t)i;
+    m = fmaxf(m, nrm[i]);
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(misc, __float_as_uint(m));   // non-negative
+}
+
+__global__ void k_inv(const int32_t* __restrict__ perm, int64_t N, int32_t* __restrict__ inv) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N;
+       p += (int64_t)gridDim.x * blockDim.x)
+    inv[perm[p]] = (int32_t)p;
+}
+
+// tau = the pilot's K'-th key + slack1 (rounding of the same pair in another
+// tile orientation), ntau = -(tau + slack2) (the column-side fast filter)
+__global__ void k_tau(const u64* __restrict__ cand, int64_t N, int Kc,
+                      const unsigned* __restrict__ misc, float* __restrict__ tau,
+                      float* __restrict__ ntau, unsigned* __restrict__ cnt) {
+  const float mx = __uint_as_float(misc[0]);
+  const float slack1 = ldexpf(mx, -11), slack2 = ldexpf(mx, -16);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N + 256;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < N) {
+      const u64 k = cand[(size_t)i * Kc + Kc - 1];
+      const float t = (k == kKeyMax) ? INFINITY : key_val(k) + slack1;
+      tau[i] = t;
+      ntau[i] = -(t + slack2);
+      cnt[i] = 0u;
+    } else {
+      tau[i] = -INFINITY;
+      ntau[i] = INFINITY;
+    }
+  }
+}
+
+// per point: the K' smallest keys of its list (or a fallback entry)
+constexpr int kSelWarps = 4;
+__global__ void __launch_bounds__(kSelWarps * 32)
+k_select(const unsigned* __restrict__ cnt, u64* __restrict__ list, int64_t N, int Kc,
+         u64* __restrict__ cand, int32_t* __restrict__ fb, unsigned* __restrict__ nfb) {
+  __shared__ u64 scratch[kSelWarps][kSymCap];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * kSelWarps + wid;
+  if (i >= N) return;
+  const unsigned n = cnt[i];
+  if (n > (unsigned)kSymCap || n < (unsigned)Kc) {
+    if (lane == 0) fb[atomicAdd(nfb, 1u)] = (int32_t)i;
+    return;
+  }
+  u64 t;
+  compact_keys(list + (size_t)i * kSymCap, (int)n, Kc, scratch[wid], lane, cand + (size_t)i * Kc, t);
+}
+
+__global__ void k_scatter_cand(const u64* __restrict__ src, const int32_t* __restrict__ rows,
+                               int n, int Kc, u64* __restrict__ cand) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)n * Kc;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / Kc, c = e % Kc;
+    cand[(size_t)rows[r] * Kc + c] = src[e];
+  }
+}
+
+// candidates of all N points by the symmetric search; w.cand / w.perm / w.inv
+// hold the result (cand rows and key indices in locality positions)
+struct StageTimer {   // TSNE_KNN_TIMING=1: per-stage times of the symmetric search (stderr)
+  bool on;
+  cudaStream_t s;
+  cudaEvent_t ev[8];
+  int n = 0;
+  StageTimer(cudaStream_t st) : on(getenv("TSNE_KNN_TIMING") != nullptr), s(st) {
+    if (on) for (auto& e : ev) cudaEventCreate(&e);
+  }
+  void mark() { if (on && n < 8) cudaEventRecord(ev[n++], s); }
+  void report(const char* const* names, int64_t N, const unsigned* cnt) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    for (int k = 1; k < n; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[k - 1], ev[k]);
+      fprintf(stderr, "  sym %-10s %9.2f ms\n", names[k - 1], ms);
+    }
+    if (cnt) {
+      unsigned* h = (unsigned*)malloc(N * sizeof(unsigned));
+      cudaMemcpy(h, cnt, N * sizeof(unsigned), cudaMemcpyDeviceToHost);
+      double sum = 0; unsigned mx = 0; int64_t over = 0;
+      for (int64_t i = 0; i < N; ++i) { sum += h[i]; mx = h[i] > mx ? h[i] : mx; over += h[i] > kSymCap; }
+      fprintf(stderr, "  sym lists: mean %.1f max %u overflow %lld\n", sum / N, mx, (long long)over);
+      free(h);
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
+static tsne_status sym_candidates(int64_t N, KnnWS& w, cudaStream_t s) {
+  const int Dp = w.Dp, Kc = w.Kc, C = w.C;
+  StageTimer tm(s);
+  tm.mark();
+  // 1. locality order: nearest of C sampled points (tensor-core pair kernel,
+  //    K' = 32), points sorted by that cell
+  k_sample_idx<<<(C + 255) / 256, 256, 0, s>>>(w.fb, C, N);
+  TSNE_LAUNCH_CHECK();
+  k_gather_rows<<<(int)(((int64_t)(C + 256) * 32 + 255) / 256), 256, 0, s>>>(
+      w.Xh, w.nrm, w.fb, C, C + 256, Dp, w.Xs, w.nrm_s);
+  TSNE_LAUNCH_CHECK();
+  // cell order: a greedy nearest-neighbour tour over the samples (host, C
+  // nodes, from their 32 nearest samples), so that neighbouring cells --
+  // e.g. the cells of one cluster -- are adjacent in the locality order
+  tsne_status st = launch_cand_pair(w.Xs, C + 256, w.Xs, C + 256, w.nrm_s, C, 0, C, Dp, 32, w.buf,
+                                    w.cand32, w.slots, nullptr, s, 1, 0, nullptr);
+  if (st != TSNE_OK) return st;
+  {
+    std::vector<u64> nb((size_t)C * 32);
+    TSNE_CUDA_TRY(cudaMemcpyAsync(nb.data(), w.cand32, nb.size() * sizeof(u64),
+                                  cudaMemcpyDeviceToHost, s));
+    TSNE_CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<int32_t> rank(C, -1);
+    int next_unvisited = 0, cur = 0, r = 0;
+    while (r < C) {
+      rank[cur] = r++;
+      int nxt = -1;
+      for (int k = 0; k < 32 && k < C - 1; ++k) {           // nearest unvisited sample
+        const int j = (int)(unsigned)(nb[(size_t)cur * 32 + k] & 0xffffffffull);
+        if (j >= 0 && j < C && rank[j] < 0) { nxt = j; break; }
+      }
+      if (nxt < 0) {                                        // jump: lowest unvisited
+        while (next_unvisited < C && rank[next_unvisited] >= 0) ++next_unvisited;
+        nxt = next_unvisited;
+      }
+      cur = nxt;
+      if (cur >= C) break;
+    }
+    TSNE_CUDA_TRY(cudaMemcpyAsync(w.inv, rank.data(), C * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                  s));
+    TSNE_CUDA_TRY(cudaStreamSynchronize(s));   // `rank` is a host temporary
+  }
+  const int32_t* group = w.inv;                // cell -> tour rank (scratch until k_inv)
+  st = launch_cand_pair(w.Xh, N + 256, w.Xs, C + 256, w.nrm_s, C, 0, (int)N, Dp, 32, w.buf,
+                        w.cand32, w.slots, nullptr, s, 0, 0, nullptr);
+  if (st != TSNE_OK) return st;
+  TSNE_CUDA_TRY(cudaMemsetAsync(w.misc, 0, 4 * sizeof(unsigned), s));
+  int cb = 1;
+  while ((1 << cb) < C) ++cb;
+  k_cells<<<4 * kNumSMs, 256, 0, s>>>(w.cand32, N, 0, group, w.cell, w.perm + N, w.nrm, w.misc);
+  TSNE_LAUNCH_CHECK();
+  {
+    cub::DoubleBuffer<uint32_t> dk(w.cell, w.cell + N);
+    cub::DoubleBuffer<int32_t> dv(w.perm + N, w.perm);
+    size_t tb = w.sort_tmp_bytes;
+    const int eb = cb;
+    TSNE_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, tb, dk, dv, (int)N, 0, eb, s));
+    if (dv.Current() != w.perm)
+      TSNE_CUDA_TRY(cudaMemcpyAsync(w.perm, dv.Current(), N * sizeof(int32_t),
+                                    cudaMemcpyDeviceToDevice, s));
+  }
+  k_inv<<<4 * kNumSMs, 256, 0, s>>>(w.perm, N, w.inv);
+  TSNE_LAUNCH_CHECK();
+  k_gather_rows<<<(int)(((N + 256) * 32 + 255) / 256), 256, 0, s>>>(w.Xh, w.nrm, w.perm, N, N + 256,
+                                                                   Dp, w.Xp, w.nrm_p);
+  TSNE_LAUNCH_CHECK();
+  tm.mark();
+  // 2. pilot: the K' best within kSymWindow column tiles around each point
+  st = launch_cand_pair(w.Xp, N + 256, w.Xp, N + 256, w.nrm_p, (int)N, 0, (int)N, Dp, Kc, w.buf,
+                        w.cand, w.slots, nullptr, s, 1, kSymWindow, nullptr);
+  if (st != TSNE_OK) return st;
+  k_tau<<<4 * kNumSMs, 256, 0, s>>>(w.cand, N, Kc, w.misc, w.tau, w.ntau, w.cnt);
+  TSNE_LAUNCH_CHECK();
+  tm.mark();
+  // 3. the symmetric sweep
+  st = launch_sym(w.Xp, N + 256, w.nrm_p, w.tau, w.ntau, w.cnt, w.list, kSymCap, (int)N, Dp,
+                  w.sync, s);
+  if (st != TSNE_OK) return st;
+  tm.mark();
+  // 4. selection; overflowing / underfilled points redone by the row sweep
+  k_select<<<(int)((N + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, s>>>(
+      w.cnt, w.list, N, Kc, w.cand, w.fb, w.misc + 1);
+  TSNE_LAUNCH_CHECK();
+  unsigned nfb = 0;
+  TSNE_CUDA_TRY(cudaMemcpyAsync(&nfb, w.misc + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  TSNE_CUDA_TRY(cudaStreamSynchronize(s));
+  tm.mark();
+  w.sym_fallback = nfb;
+  if (tm.on) fprintf(stderr, "  sym fallback points %u\n", nfb);
+  for (unsigned r0 = 0; r0 < nfb; r0 += kFbRows) {
+    const int n = (int)((nfb - r0) < (unsigned)kFbRows ? nfb - r0 : kFbRows);
+    k_gather_rows<<<(int)(((int64_t)(n + 256) * 32 + 255) / 256), 256, 0, s>>>(
+        w.Xp, w.nrm_p, w.fb + r0, n, n + 256, Dp, w.Xq, w.ntau);   // ntau: dead scratch now
+    TSNE_LAUNCH_CHECK();
+    st = launch_cand_pair(w.Xq, n + 256, w.Xp, N + 256, w.nrm_p, (int)N, 0, n, Dp, Kc, w.buf,
+                          w.candfb, w.slots, nullptr, s, 1, 0, w.fb + r0);
+    if (st != TSNE_OK) return st;
+    k_scatter_cand<<<4 * kNumSMs, 256, 0, s>>>(w.candfb, w.fb + r0, n, Kc, w.cand);
+    TSNE_LAUNCH_CHECK();
+  }
+  tm.mark();
+  static const char* names[] = {"order", "pilot", "sweep", "select", "fallback"};
+  tm.report(names, N, w.cnt);
+  return TSNE_OK;
+}
+
 // ---------------------------------------------------------------- host
 tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int64_t q0, int64_t nq,
                     int32_t* idx, double* d2, KnnWS& w, tsne_knn_info* info, cudaStream_t s) {
@@ -415,10 +674,16 @@ tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int64_t q0,
     TSNE_LAUNCH_CHECK();
   }
   TSNE_CUDA_TRY(cudaMemsetAsync(w.uncert, 0, 2 * sizeof(u64), s));
-  // TSNE_KNN_PATH=simt forces the CUDA-core candidate stage (cross-checks)
+  // TSNE_KNN_PATH=simt forces the CUDA-core candidate stage, =tc2 / =tc1 the
+  // row-by-row tensor-core sweeps (cross-checks); by default a full-N call
+  // uses the symmetric search (knn_sym.cu)
   const char* force = getenv("TSNE_KNN_PATH");
   bool tc = knn_tc_available() && Dp % 64 == 0 && !(force && strcmp(force, "simt") == 0);
-  if (tc) {
+  const bool sym = tc && w.sym && q0 == 0 && nq == N && !force;
+  if (sym) {
+    tsne_status st = sym_candidates(N, w, s);
+    if (st != TSNE_OK) return st;
+  } else if (tc) {
     tsne_status st = launch_cand_tc(w.Xh, w.nrm, (int)N, (int)q0, (int)nq, Dp, Kc, w.buf, w.cand, w.slots, w.sync, s);
     if (st != TSNE_OK) return st;
   } else {
@@ -429,12 +694,13 @@ tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int64_t q0,
                                                    w.buf, w.cand);
     TSNE_LAUNCH_CHECK();
   }
-  w.path = tc ? 1 : 0;
+  w.path = sym ? 2 : (tc ? 1 : 0);
   const char* fm = getenv("TSNE_KNN_FORCE_FALLBACK");      // test hook: every fm-th row
   const int force_mod = fm ? atoi(fm) : 0;
   k_rerank<<<(int)((nq + 7) / 8), kRR_Threads, 0, s>>>(X, (int)N, (int)q0, (int)nq, D, K, Kc,
                                                       w.cand, w.nrm, w.scale,
-                                                     idx, d2, w.uncert, w.rows_bad, force_mod);
+                                                     idx, d2, w.uncert, w.rows_bad, force_mod,
+                                                     sym ? w.perm : nullptr, sym ? w.inv : nullptr);
   TSNE_LAUNCH_CHECK();
   // uncertified rows (D26): exact fp64 scan of the whole data set
   u64 h = 0;

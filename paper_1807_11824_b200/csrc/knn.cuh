@@ -33,9 +33,33 @@ struct KnnWS {
   int32_t* si_alt = nullptr;      // N
   void* sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
+  // symmetric candidate search (knn_sym.cu), full-N calls only
+  bool sym = false;
+  int32_t C = 0;                  // locality cells (sampled points)
+  __half* Xs = nullptr;           // (C + 256) x Dp sampled rows
+  float* nrm_s = nullptr;         // C + 256
+  unsigned long long* cand32 = nullptr;          // N x 32: nearest samples
+  uint32_t* cell = nullptr;       // N   cell of each point   (+ N alt)
+  int32_t* perm = nullptr;        // N   locality order -> point (+ N alt)
+  int32_t* inv = nullptr;         // N   point -> locality position
+  __half* Xp = nullptr;           // (N + 256) x Dp rows in locality order
+  float* nrm_p = nullptr;         // N + 256
+  float* tau = nullptr;           // N + 256 per point thresholds
+  float* ntau = nullptr;          // N + 256
+  unsigned* cnt = nullptr;        // N list lengths
+  unsigned long long* list = nullptr;            // N x kSymCap
+  int32_t* fb = nullptr;          // N fallback points (locality positions)
+  __half* Xq = nullptr;           // (kFbRows + 256) x Dp gathered fallback rows
+  unsigned long long* candfb = nullptr;          // kFbRows x Kc
+  unsigned* misc = nullptr;       // [0] max |x_h|^2 bits, [1] fallback count
+  int64_t sym_fallback = 0;       // points redone by the row sweep (last call)
   int32_t path = 0;
 };
 constexpr int kScanRows = 8;
+constexpr int kSymCap = 1024;     // list capacity per point
+constexpr int kSymCells = 8192;   // locality cells (sampled points)
+constexpr int kSymWindow = 12;    // pilot window, column tiles of 256
+constexpr int kFbRows = 16384;    // fallback rows per asymmetric sweep
 
 void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K);
 // Neighbours of the query rows [q0, q0 + nq) among all N points; idx / d2 are

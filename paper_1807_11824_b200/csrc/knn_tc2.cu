@@ -44,7 +44,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_b,
            const float* __restrict__ nrm, int N, int q0, int nq, int Dp,
            int Kc, u64* __restrict__ buf, u64* __restrict__ cand, unsigned* __restrict__ sync,
-           int dbg_skip_epilogue) {
+           int dbg_skip_epilogue, int self_excl, int win_tiles, const int32_t* __restrict__ qid) {
+  // rows: queries q0 .. q0+nq-1 of the A map; columns: the N points of the B
+  // map with norms nrm (the same point set as the rows when self_excl != 0);
+  // win_tiles > 0 restricts each CTA pair to win_tiles column tiles around
+  // its own rows (the pilot of the symmetric search, knn_sym.cu)
   extern __shared__ unsigned char smraw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -60,7 +64,15 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npair_grid = gridDim.x >> 1;
   const int nkb = Dp / P_BK;
-  const int nrb = (nq + P_BM - 1) / P_BM, npairs = (nrb + 1) / 2, nct = (N + P_BN - 1) / P_BN;
+  const int nrb = (nq + P_BM - 1) / P_BM, npairs = (nrb + 1) / 2;
+  const int nct_all = (N + P_BN - 1) / P_BN;
+  const int nct = (win_tiles > 0 && win_tiles < nct_all) ? win_tiles : nct_all;
+  // first column tile of pair pp: the window is centred on the pair's rows
+  auto ct_first = [&](int pp) {
+    if (nct == nct_all) return 0;
+    const int c = (q0 + pp * 2 * P_BM) / P_BN - nct / 2;
+    return c < 0 ? 0 : (c > nct_all - nct ? nct_all - nct : c);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < P_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -87,7 +99,9 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
       int wave = 0;
       for (int pp = pair; pp < npairs; pp += npair_grid, ++wave) {
         const int rb = 2 * pp + (int)rank;
-        for (int ct = 0; ct < nct; ++ct) {
+        const int ctf = ct_first(pp);
+        for (int cs = 0; cs < nct; ++cs) {
+          const int ct = ctf + cs;
           if (sync && ct % P_SYNC_EVERY == 0) {      // CTA lockstep for L2 reuse (knn_tc.cu)
             const int members = 2 * min(npair_grid, npairs - wave * npair_grid);
             const int cp = ct / P_SYNC_EVERY;
@@ -125,7 +139,7 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
       uint32_t phase = 0, aphase = 0;
       int acc = 0;
       for (int pp = pair; pp < npairs; pp += npair_grid)
-        for (int ct = 0; ct < nct; ++ct) {
+        for (int cs = 0; cs < nct; ++cs) {
           mbar_wait(&tempty[acc], aphase ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(acc * P_BN);
@@ -158,11 +172,14 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
     uint32_t aphase = 0;
     for (int pp = pair; pp < npairs; pp += npair_grid) {
       const int rb = 2 * pp + (int)rank;
-      const int q = q0 + rb * P_BM + rl;         // global query index
       const bool qok = rb * P_BM + rl < nq;
+      const int q = qid ? (qok ? __ldg(qid + q0 + rb * P_BM + rl) : -1)
+                        : q0 + rb * P_BM + rl;   // the query's point id
       int cnt = 0;
       u64 tau = kKeyMax;
-      for (int ct = 0; ct < nct; ++ct) {
+      const int ctf = ct_first(pp);
+      for (int cs = 0; cs < nct; ++cs) {
+        const int ct = ctf + cs;
         mbar_wait(&tfull[acc], aphase);
         tc_fence_after();
         const int c0 = ct * P_BN;
@@ -211,7 +228,7 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
             if ((m >> t) & 1) {
               const u64 key = mkkey(dist, j);
               if (dbg_skip_epilogue == 3) { if (key == 0) rowbuf[0] = 0; }
-              else if (j < N && j != q && key < tau) rowbuf[cnt++] = key;
+              else if (j < N && (j != q || !self_excl) && key < tau) rowbuf[cnt++] = key;
             }
           }
         }
@@ -261,7 +278,8 @@ size_t knn_tc2_sync_words(int64_t N, int64_t nq) {
 
 tsne_status launch_cand_tc2(const CUtensorMap& map, const CUtensorMap& map_b, const float* nrm, int N, int q0, int nq, int Dp, int Kc,
                             unsigned long long* buf, unsigned long long* cand, int slots,
-                            unsigned* sync, cudaStream_t s) {
+                            unsigned* sync, cudaStream_t s, int self_excl, int win_tiles,
+                            const int32_t* qid) {
   TSNE_CUDA_TRY(cudaFuncSetAttribute(k_cand_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)P_SMEM));
   const int nrb = (nq + P_BM - 1) / P_BM, npairs = (nrb + 1) / 2;
@@ -269,8 +287,10 @@ tsne_status launch_cand_tc2(const CUtensorMap& map, const CUtensorMap& map_b, co
   if (grid > slots) grid = slots & ~1;
   if (sync) TSNE_CUDA_TRY(cudaMemsetAsync(sync, 0, sizeof(unsigned) * knn_tc2_sync_words(N, nq), s));
   const char* dbg = getenv("TSNE_KNN_DEBUG_NO_EPILOGUE");
+  if (win_tiles > 0) sync = nullptr;          // pairs stream different tiles: no lockstep
   k_cand_tc2<<<grid, P_THREADS, P_SMEM, s>>>(map, map_b, nrm, N, q0, nq, Dp, Kc, buf, cand,
-                                              grid == kNumSMs ? sync : nullptr, dbg ? atoi(dbg) : 0);
+                                              grid == kNumSMs ? sync : nullptr, dbg ? atoi(dbg) : 0,
+                                              self_excl, win_tiles, qid);
   TSNE_LAUNCH_CHECK();
   if (dbg && atoi(dbg) == 5) {
     unsigned long long h[4];

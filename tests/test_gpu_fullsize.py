@@ -33,7 +33,7 @@ def c5(T):
 
 def test_c5_knn_sampled_rows(orc, c5):
     Xh, idx, d2, info, *_ = c5
-    assert info["gemm_path"] == "tcgen05" and info["rows_uncertified"] == 0
+    assert info["gemm_path"].startswith("tcgen05") and info["rows_uncertified"] == 0
     rows = np.random.default_rng(5).choice(N5, 6, replace=False)
     rows = np.append(rows, [0, N5 - 1])          # first and last (ragged tail)
     io, do = orc.knn(Xh, 90, rows=rows)

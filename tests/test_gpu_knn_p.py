@@ -41,7 +41,7 @@ def test_knn_vs_oracle(T, orc, cfg, n, K):
     idx_o, d2_o = orc.knn(X, K)
     check_knn(orc, X, idx.cpu().numpy(), d2.cpu().numpy(), idx_o, d2_o)
     assert info["rows_uncertified"] == 0
-    assert info["gemm_path"] == "tcgen05"
+    assert info["gemm_path"].startswith("tcgen05")
 
 
 @pytest.mark.parametrize("cfg,n,K", [("C5", 5000, 90), ("C2", 4100, 90), ("C4", 3000, 150)])
@@ -51,7 +51,7 @@ def test_knn_tcgen05_vs_cudacore_path(T, cfg, n, K, monkeypatch):
     idx_t, d2_t, it = T.knn(X, K)
     monkeypatch.setenv("TSNE_KNN_PATH", "simt")
     idx_s, d2_s, is_ = T.knn(X, K)
-    assert it["gemm_path"] == "tcgen05" and is_["gemm_path"] == "cuda-core"
+    assert it["gemm_path"].startswith("tcgen05") and is_["gemm_path"] == "cuda-core"
     assert torch.equal(d2_t, d2_s) and torch.equal(idx_t, idx_s)
     assert it["rows_uncertified"] == 0 and is_["rows_uncertified"] == 0
 
