@@ -675,11 +675,15 @@ tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int64_t q0,
   }
   TSNE_CUDA_TRY(cudaMemsetAsync(w.uncert, 0, 2 * sizeof(u64), s));
   // TSNE_KNN_PATH=simt forces the CUDA-core candidate stage, =tc2 / =tc1 the
-  // row-by-row tensor-core sweeps (cross-checks); by default a full-N call
-  // uses the symmetric search (knn_sym.cu)
+  // row-by-row tensor-core sweeps, =sym the symmetric search (cross-checks).
+  // By default a full-N call uses the symmetric search (knn_sym.cu) where the
+  // tensor work dominates its list appends -- large N and D (measured: C5
+  // 1.28M x 2048 5.8 s -> 3.2 s; C2/C4 (D <= 784) are faster row by row)
   const char* force = getenv("TSNE_KNN_PATH");
   bool tc = knn_tc_available() && Dp % 64 == 0 && !(force && strcmp(force, "simt") == 0);
-  const bool sym = tc && w.sym && q0 == 0 && nq == N && !force;
+  const bool sym_default = N >= (int64_t(1) << 18) && Dp >= 1024;
+  const bool sym = tc && w.sym && q0 == 0 && nq == N &&
+                   (force ? strcmp(force, "sym") == 0 : sym_default);
   if (sym) {
     tsne_status st = sym_candidates(N, w, s);
     if (st != TSNE_OK) return st;

@@ -57,8 +57,8 @@ constexpr size_t S_SMEM = 1024 + S_STAGES * S_STAGE_BYTES + 256;
 
 struct SymArgs {
   const float* nrm;     // |x_h|^2 per point (padded with zeros)
-  const float* tau;     // per point threshold (inf = no filter; unusable)
-  const float* ntau;    // -(tau + slack2): the column-side fast filter
+  float* tau;           // per point threshold; -inf once the list overflowed
+  float* ntau;          // -(tau + slack2): the column-side fast filter (+inf: off)
   unsigned* cnt;        // per point list length (atomic)
   u64* list;            // per point list, cap keys each
   int N, Dp, cap;
@@ -196,7 +196,7 @@ k_cand_sym(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
     for (int b = pair; b < S; b += npair_grid) {
       const int i = b * S_BN + (int)rank * S_BM + rl;            // this lane's row point
       const bool iok = i < a.N;
-      const float tau_i = iok ? __ldg(a.tau + i) : -INFINITY;    // row side: key <= tau_i
+      float tau_i = -INFINITY;                                    // row side: key <= tau_i
       const float nrm_i = iok ? __ldg(a.nrm + i) : 0.f;
       const float nnrm_i = -nrm_i;                               // column side fast filter
       u64* list_i = a.list + (size_t)(iok ? i : 0) * a.cap;
@@ -204,6 +204,8 @@ k_cand_sym(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
         const int c = sym_col(b, s, S, npair_grid);
         if (c < 0) continue;
         const bool col_side = c != b;
+        // re-read per tile: an overflowing list switches its point off (-inf)
+        tau_i = iok ? __ldcg(a.tau + i) : -INFINITY;
         mbar_wait(&tfull[acc], aphase);
         tc_fence_after();
         const uint32_t tbase = tmem + ((uint32_t)(e * 32) << 16) + (uint32_t)(acc * S_BN);
@@ -220,7 +222,7 @@ k_cand_sym(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
           for (int u = 0; u < 16; ++u) {
             const float4 v = __ldg(n4 + u);
             nv[4 * u] = v.x; nv[4 * u + 1] = v.y; nv[4 * u + 2] = v.z; nv[4 * u + 3] = v.w;
-            const float4 w = __ldg(t4 + u);
+            const float4 w = __ldcg(t4 + u);
             nt[4 * u] = w.x; nt[4 * u + 1] = w.y; nt[4 * u + 2] = w.z; nt[4 * u + 3] = w.w;
           }
           tmem_wait_ld();
@@ -259,13 +261,15 @@ k_cand_sym(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
               if (d <= tau_i) {
                 const unsigned pos = atomicAdd(a.cnt + i, 1u);
                 if (pos < (unsigned)a.cap) list_i[pos] = mkkey(d, j);
+                else if (pos == (unsigned)a.cap) { a.tau[i] = -INFINITY; a.ntau[i] = INFINITY; }
               }
             }
             if ((mcol >> t) & 1) {                               // i is a candidate of j
               const float d = fmaf(-2.f, rv, nrm_i);
-              if (d <= __ldg(a.tau + j)) {
+              if (d <= __ldcg(a.tau + j)) {
                 const unsigned pos = atomicAdd(a.cnt + j, 1u);
                 if (pos < (unsigned)a.cap) a.list[(size_t)j * a.cap + pos] = mkkey(d, i);
+                else if (pos == (unsigned)a.cap) { a.tau[j] = -INFINITY; a.ntau[j] = INFINITY; }
               }
             }
           }
@@ -291,7 +295,7 @@ size_t knn_sym_sync_words(int64_t N) {
 }
 
 tsne_status launch_cand_sym(const CUtensorMap& map, const CUtensorMap& map_b, const float* nrm,
-                            const float* tau, const float* ntau, unsigned* cnt,
+                            float* tau, float* ntau, unsigned* cnt,
                             unsigned long long* list, int cap, int N, int Dp, unsigned* sync,
                             cudaStream_t s) {
   TSNE_CUDA_TRY(cudaFuncSetAttribute(k_cand_sym, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -277,8 +277,8 @@ tsne_status launch_cand_pair(const __half* A, int64_t rowsA, const __half* B, in
                          win_tiles, qid);
 }
 
-tsne_status launch_sym(const __half* Xp, int64_t rows, const float* nrm, const float* tau,
-                       const float* ntau, unsigned* cnt, unsigned long long* list, int cap, int N,
+tsne_status launch_sym(const __half* Xp, int64_t rows, const float* nrm, float* tau,
+                       float* ntau, unsigned* cnt, unsigned long long* list, int cap, int N,
                        int Dp, unsigned* sync, cudaStream_t s) {
   CUtensorMap ma, mb;
   tsne_status st = make_map(ma, Xp, rows, Dp, 128);

@@ -27,10 +27,10 @@ tsne_status launch_cand_pair(const __half* A, int64_t rowsA, const __half* B, in
                              const int32_t* qid);
 size_t knn_sym_sync_words(int64_t N);
 tsne_status launch_cand_sym(const CUtensorMap& map, const CUtensorMap& map_b, const float* nrm,
-                            const float* tau, const float* ntau, unsigned* cnt,
+                            float* tau, float* ntau, unsigned* cnt,
                             unsigned long long* list, int cap, int N, int Dp, unsigned* sync,
                             cudaStream_t s);
-tsne_status launch_sym(const __half* Xp, int64_t rows, const float* nrm, const float* tau,
-                       const float* ntau, unsigned* cnt, unsigned long long* list, int cap, int N,
+tsne_status launch_sym(const __half* Xp, int64_t rows, const float* nrm, float* tau,
+                       float* ntau, unsigned* cnt, unsigned long long* list, int cap, int N,
                        int Dp, unsigned* sync, cudaStream_t s);
 }  // namespace tsne

@@ -97,6 +97,24 @@ def test_knn_rows_vs_oracle(T, orc):
     check_knn(orc, X, il.cpu().numpy(), dl.cpu().numpy(), idx_o, d2_o, q0=1234)
 
 
+@pytest.mark.parametrize("cfg,n,K", [("C5", 5000, 90), ("C2", 4100, 90), ("C4", 3000, 150),
+                                     ("C3", 1500, 90), ("C1", 1030, 90)])
+def test_knn_symmetric_search(T, orc, cfg, n, K, monkeypatch):
+    """The symmetric candidate search (each super-block pair multiplied once,
+    pilot thresholds, atomic lists, row-sweep fallback) gives the same exact
+    kNN as the row sweep, bit for bit, and the oracle's."""
+    Xn = synth.make_x(cfg, n=n).numpy()
+    X = torch.as_tensor(Xn, device="cuda")
+    monkeypatch.setenv("TSNE_KNN_PATH", "tc2")
+    idx_r, d2_r, _ = T.knn(X, K)
+    monkeypatch.setenv("TSNE_KNN_PATH", "sym")
+    idx_s, d2_s, info = T.knn(X, K)
+    assert info["gemm_path"] == "tcgen05-sym" and info["rows_uncertified"] == 0
+    assert torch.equal(idx_s, idx_r) and torch.equal(d2_s, d2_r)
+    idx_o, d2_o = orc.knn(Xn, K)
+    check_knn(orc, Xn, idx_s.cpu().numpy(), d2_s.cpu().numpy(), idx_o, d2_o)
+
+
 def test_knn_duplicates_tie_by_index(T, orc):
     X = synth.make_x("C1", n=500).numpy()
     X[100:140] = X[7]                        # 41 identical rows
