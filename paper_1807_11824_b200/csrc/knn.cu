@@ -303,13 +303,16 @@ k_rerank(const float* __restrict__ X, int N, int qs, int nq, int D, int K, int K
   __shared__ double s_d[kRR_Threads / 32][256];
   __shared__ int s_j[kRR_Threads / 32][256];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int il = blockIdx.x * (kRR_Threads / 32) + wid;   // local query row
-  if (il >= nq) return;
+  const int w = blockIdx.x * (kRR_Threads / 32) + wid;
+  if (w >= nq) return;
+  // with a locality order (symmetric search) warps take the rows in that
+  // order: consecutive rows share most candidates, which then hit in L2
+  const int il = perm ? perm[w] : w;                       // local query row
   const int i = qs + il;
   double* sd = s_d[wid];
   int* sj = s_j[wid];
   const float* xi = X + (size_t)i * D;
-  const u64* ci = cand + (size_t)(inv ? inv[i] : il) * Kc;
+  const u64* ci = cand + (size_t)(perm ? w : il) * Kc;
   const double inv2 = (double)scale[1];
   const double nrm_i = (double)nrm[i];
   double emax = 0.0;
