@@ -63,6 +63,10 @@ int32_t tsne_abi_version(void);
  * accumulate) distance GEMM selects K' >= K candidates per row by the
  * expanded form |x|^2 + |y|^2 - 2 x.y on column-mean-centred data, then an
  * fp64 re-rank of exact differences sum_d (x_d - y_d)^2 picks the K best.
+ * For N >= 2^18 and D >= 1024 the candidate GEMM exploits the symmetry of the
+ * distance matrix (each pair of 256-point blocks multiplied once, DESIGN.md
+ * 6.6); the result is identical.  The call synchronises `stream` internally
+ * (the host orders the locality tour and reads the fallback counts).
  *
  *   X    [N x D] float32, row-major, finite.
  *   idx  [N x K] int32 out: neighbours of row i, self excluded, ascending by
@@ -76,7 +80,8 @@ int32_t tsne_abi_version(void);
 typedef struct {
   int64_t rows_uncertified;  /* rows re-done by the exact fallback scan      */
   int32_t candidates;        /* K' used                                       */
-  int32_t gemm_path;         /* 1 = tcgen05 tensor-core path, 0 = CUDA-core   */
+  int32_t gemm_path;         /* 2 = tcgen05 symmetric search, 1 = tcgen05 row
+                                sweep, 0 = CUDA-core                         */
 } tsne_knn_info;
 
 size_t tsne_knn_workspace_size(int64_t N, int32_t D, int32_t K);
