@@ -214,31 +214,38 @@ tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, 
  * Multi-GPU building blocks (the paper is single-GPU).
  * One process per GPU.  Every rank holds the full embedding Y [N x 2] and the
  * CSR rows [row0, row1) of P it owns (row_ptr_local: n_local + 1 offsets into
- * col_local / val_local; columns are global point indices).  Per iteration:
- *   1. tsne_shard_forces: (recentre Y in place if `recentre`: Y -= mean, D15)
- *      -> quadtree over the whole Y (built redundantly on every rank) -> the
- *      theta traversal for the owned points only: rep_local[i - row0] = f_i,
- *      z_partial[0] = sum over owned i of z_i (z_partial: 2 doubles, DEVICE).
+ * col_local / val_local, 16-byte aligned; columns are global point indices).
+ * Per iteration:
+ *   1. tsne_shard_forces: quadtree over the whole Y (built redundantly on
+ *      every rank; if `recentre`, over Y - mean(Y), D15, the shift being kept
+ *      in the workspace) -> the theta traversal for the owned points only:
+ *      rep_local[i - row0] = f_i, z_partial[0] = sum over owned i of z_i
+ *      (z_partial: 2 doubles, DEVICE).  Y is NOT modified.
+ *   1'. tsne_shard_attract (may run concurrently with 1 on another stream:
+ *      it only reads Y): A_local[i - row0] = sum_j P_ij (y_i - y_j) q_ij Z.
  *   2. caller: all-gather the ranks' z_partial pairs (NCCL) -> z_partials
  *      [world x 2] DEVICE, in rank order.
- *   3. tsne_shard_update: attractive pass for the owned rows against the full
- *      Y, Eq. 7 with Z = sum_r z_partials[2r] (added in rank order, so every
- *      rank uses the identical Z), D12 update of v_local, gains_local, and
- *      Y_local_out [n_local x 2] = the owned rows of the updated Y.
+ *   3. tsne_shard_update (same workspace as 1): Eq. 7 with Z = sum_r
+ *      z_partials[2r] (added in rank order, so every rank uses the identical
+ *      Z), D12 update of v_local, gains_local, and Y_local_out [n_local x 2] =
+ *      the owned rows of the updated, recentred Y.
  *   4. caller: all-gather Y_local_out shards into Y (NCCL).
  * After the last iteration, tsne_recentre(Y) applies the final recentring.
  * `flag` (DEVICE int, nullable) is set to 1 on a non-finite result.
  * ------------------------------------------------------------------------ */
 size_t tsne_shard_workspace_size(int64_t N);
-tsne_status tsne_shard_forces(float* Y, int64_t N, int64_t row0, int64_t row1, float theta,
+tsne_status tsne_shard_forces(const float* Y, int64_t N, int64_t row0, int64_t row1, float theta,
                               int32_t recentre, float* rep_local, double* z_partial, void* ws,
                               size_t ws_bytes, tsne_stream_t stream);
-tsne_status tsne_shard_update(const int64_t* row_ptr_local, const int32_t* col_local,
-                              const float* val_local, int64_t N, int64_t row0, int64_t row1,
+tsne_status tsne_shard_attract(const int64_t* row_ptr_local, const int32_t* col_local,
+                               const float* val_local, int64_t N, int64_t row0, int64_t row1,
+                               const float* Y, float* A_local, tsne_stream_t stream);
+tsne_status tsne_shard_update(const float* A_local, int64_t N, int64_t row0, int64_t row1,
                               const float* Y, const float* rep_local, const double* z_partials,
                               int32_t world, int32_t t, float learning_rate, float exaggeration,
                               const tsne_config* cfg, float* v_local, float* gains_local,
-                              float* Y_local_out, int32_t* flag, tsne_stream_t stream);
+                              float* Y_local_out, int32_t* flag, void* ws, size_t ws_bytes,
+                              tsne_stream_t stream);
 tsne_status tsne_recentre(float* Y, int64_t N, void* ws, size_t ws_bytes, tsne_stream_t stream);
 
 /* Y0 = 1e-4 N(0,1) from Philox4x32-10 (key = seed, counter = (i,0,0,0)),

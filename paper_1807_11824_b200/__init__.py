@@ -51,7 +51,7 @@ EXPORTS = ["tsne_last_error", "tsne_abi_version", "tsne_config_default",
            "tsne_compute_p", "tsne_gradient_workspace_size", "tsne_gradient",
            "tsne_optimize_workspace_size", "tsne_optimize", "tsne_init_y", "tsne_run",
            "tsne_run_ex", "tsne_profile_iterations", "tsne_shard_workspace_size",
-           "tsne_shard_forces", "tsne_shard_update", "tsne_recentre"]
+           "tsne_shard_forces", "tsne_shard_attract", "tsne_shard_update", "tsne_recentre"]
 
 
 def lib():
@@ -92,12 +92,13 @@ def lib():
     L.tsne_shard_workspace_size.argtypes = [i64]
     L.tsne_shard_workspace_size.restype = sz
     L.tsne_shard_forces.argtypes = [vp, i64, i64, i64, f32, i32, vp, vp, vp, sz, vp]
-    L.tsne_shard_update.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, vp, i32, i32, f32, f32,
-                                    C.POINTER(Config), vp, vp, vp, vp, vp]
+    L.tsne_shard_attract.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, vp]
+    L.tsne_shard_update.argtypes = [vp, i64, i64, i64, vp, vp, vp, i32, i32, f32, f32,
+                                    C.POINTER(Config), vp, vp, vp, vp, vp, sz, vp]
     L.tsne_recentre.argtypes = [vp, i64, vp, sz, vp]
     for name in ["tsne_knn", "tsne_knn_rows", "tsne_compute_p", "tsne_gradient", "tsne_optimize", "tsne_init_y",
                  "tsne_run", "tsne_run_ex", "tsne_profile_iterations", "tsne_shard_forces",
-                 "tsne_shard_update", "tsne_recentre"]:
+                 "tsne_shard_attract", "tsne_shard_update", "tsne_recentre"]:
         getattr(L, name).restype = C.c_int
     _lib = L
     return L

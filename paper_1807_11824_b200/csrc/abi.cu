@@ -277,7 +277,7 @@ size_t tsne_shard_workspace_size(int64_t N) {
   return c.bytes();
 }
 
-tsne_status tsne_shard_forces(float* Y, int64_t N, int64_t row0, int64_t row1, float theta,
+tsne_status tsne_shard_forces(const float* Y, int64_t N, int64_t row0, int64_t row1, float theta,
                               int32_t recentre, float* rep_local, double* z_partial, void* ws,
                               size_t ws_bytes, tsne_stream_t stream) {
   clear_error();
@@ -298,16 +298,32 @@ tsne_status tsne_shard_forces(float* Y, int64_t N, int64_t row0, int64_t row1, f
   if (st != TSNE_OK) return st;
   Carver c(ws);
   carve_shard(c, w, N);
-  return shard_forces(w, reinterpret_cast<float2*>(Y), N, row0, row1, theta, recentre != 0,
+  return shard_forces(w, reinterpret_cast<const float2*>(Y), N, row0, row1, theta, recentre != 0,
                       reinterpret_cast<float2*>(rep_local), z_partial, (cudaStream_t)stream);
 }
 
-tsne_status tsne_shard_update(const int64_t* row_ptr_local, const int32_t* col_local,
-                              const float* val_local, int64_t N, int64_t row0, int64_t row1,
+tsne_status tsne_shard_attract(const int64_t* row_ptr_local, const int32_t* col_local,
+                               const float* val_local, int64_t N, int64_t row0, int64_t row1,
+                               const float* Y, float* A_local, tsne_stream_t stream) {
+  clear_error();
+  TSNE_ARG_CHECK(N >= 2 && 0 <= row0 && row0 <= row1 && row1 <= N, "bad row range");
+  TSNE_ARG_CHECK(Y && (row1 == row0 || (row_ptr_local && col_local && val_local && A_local)),
+                 "null pointer argument");
+  TSNE_ARG_CHECK(row1 == row0 || (aligned(col_local, 16) && aligned(val_local, 16)),
+                 "col and val must be 16-byte aligned");
+  tsne_status st = check_device();
+  if (st != TSNE_OK) return st;
+  return launch_attract_sum_shard(row_ptr_local, col_local, val_local,
+                                  reinterpret_cast<const float2*>(Y), row0, row1 - row0,
+                                  reinterpret_cast<float2*>(A_local), (cudaStream_t)stream);
+}
+
+tsne_status tsne_shard_update(const float* A_local, int64_t N, int64_t row0, int64_t row1,
                               const float* Y, const float* rep_local, const double* z_partials,
                               int32_t world, int32_t t, float learning_rate, float exaggeration,
                               const tsne_config* cfg_in, float* v_local, float* gains_local,
-                              float* Y_local_out, int32_t* flag, tsne_stream_t stream) {
+                              float* Y_local_out, int32_t* flag, void* ws, size_t ws_bytes,
+                              tsne_stream_t stream) {
   clear_error();
   tsne_config cfg;
   tsne_config_default(&cfg);
@@ -315,19 +331,25 @@ tsne_status tsne_shard_update(const int64_t* row_ptr_local, const int32_t* col_l
   TSNE_ARG_CHECK(N >= 2 && 0 <= row0 && row0 <= row1 && row1 <= N, "bad row range");
   TSNE_ARG_CHECK(world >= 1 && t >= 0, "world must be >= 1, t >= 0");
   TSNE_ARG_CHECK(learning_rate > 0.f && exaggeration > 0.f, "learning_rate, exaggeration > 0");
-  TSNE_ARG_CHECK(Y && z_partials && (row1 == row0 || (row_ptr_local && col_local && val_local &&
-                                                     rep_local && v_local && gains_local &&
-                                                     Y_local_out)),
+  TSNE_ARG_CHECK(Y && z_partials && (row1 == row0 || (A_local && rep_local && v_local &&
+                                                     gains_local && Y_local_out)),
                  "null pointer argument");
-  TSNE_ARG_CHECK(row1 == row0 || (aligned(col_local, 16) && aligned(val_local, 16)),
-                 "col and val must be 16-byte aligned");
+  ShardWS w;
+  Carver c0(nullptr);
+  carve_shard(c0, w, N);
+  if (!ws || ws_bytes < c0.bytes()) {
+    set_error("workspace too small: need %zu bytes, got %zu", c0.bytes(), ws_bytes);
+    return TSNE_ERR_WORKSPACE;
+  }
   tsne_status st = check_device();
   if (st != TSNE_OK) return st;
+  Carver c(ws);
+  carve_shard(c, w, N);
   Sched sc{cfg.exag_iters, exaggeration, cfg.mom0, cfg.mom1, learning_rate, cfg.min_gain};
-  return launch_attract_update_shard(
-      row_ptr_local, col_local, val_local, reinterpret_cast<const float2*>(Y), row0, row1 - row0,
-      reinterpret_cast<const float2*>(rep_local), z_partials, world, t, sc,
-      reinterpret_cast<float2*>(v_local), reinterpret_cast<float2*>(gains_local),
+  return launch_update_shard(
+      reinterpret_cast<const float2*>(A_local), reinterpret_cast<const float2*>(Y), row0,
+      row1 - row0, reinterpret_cast<const float2*>(rep_local), z_partials, world, t, sc,
+      w.tree.box, reinterpret_cast<float2*>(v_local), reinterpret_cast<float2*>(gains_local),
       reinterpret_cast<float2*>(Y_local_out), flag, (cudaStream_t)stream);
 }
 

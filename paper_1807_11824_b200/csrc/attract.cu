@@ -270,47 +270,69 @@ namespace tsne {
 // replicated embedding, Eq. 7 with Z = the ranks' partial sums added in rank
 // order (deterministic), and the D12 update into the local shard.
 __global__ void __launch_bounds__(kAttrThreads)
-k_attract_update_shard(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                       const float* __restrict__ val, const float2* __restrict__ Y, int row0,
-                       int n_local, const float2* __restrict__ rep, const double* __restrict__ zp,
-                       int world, int t, Sched sc, float2* __restrict__ V, float2* __restrict__ G,
-                       float2* __restrict__ Yout, int32_t* __restrict__ flag) {
+k_attract_sum_shard(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                    const float* __restrict__ val, const float2* __restrict__ Y, int row0,
+                    int n_local, float2* __restrict__ A) {
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * kAttrThreads + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * kAttrThreads) >> 5;
+  const int64_t nnz = row_ptr[n_local];
+  for (int l = warp; l < n_local; l += nwarps) {
+    const int i = row0 + l;
+    const float2 a = row_attractive(row_ptr[l], row_ptr[l + 1], nnz, col, val, Y, i, Y[i], lane);
+    if (lane == 0) A[l] = a;
+  }
+}
+
+// Eq. 7 + D12 for the owned rows, Z = the ranks' partials added in rank
+// order; the pending recentring shift of this iteration (box->shift, D15) is
+// applied to the owned rows on the way out, so Y itself is never modified in
+// place (the attractive pass reads it concurrently)
+__global__ void __launch_bounds__(kAttrThreads)
+k_update_shard(const float2* __restrict__ A, const float2* __restrict__ Y, int row0, int n_local,
+               const float2* __restrict__ rep, const double* __restrict__ zp, int world, int t,
+               Sched sc, const BoxInfo* __restrict__ box, float2* __restrict__ V,
+               float2* __restrict__ G, float2* __restrict__ Yout, int32_t* __restrict__ flag) {
   double Z = 0.0;
   for (int r = 0; r < world; ++r) Z += zp[2 * r];
   const float invZ = (float)(1.0 / Z);
   const float alpha = (t < sc.exag_iters) ? sc.exag : 1.f;
   const float mu = (t < sc.exag_iters) ? sc.mom0 : sc.mom1;
-  const int64_t nnz = row_ptr[n_local];
-  for (int l = warp; l < n_local; l += nwarps) {
-    const int i = row0 + l;
-    const float2 yi = Y[i];
-    const float2 a = row_attractive(row_ptr[l], row_ptr[l + 1], nnz, col, val, Y, i, yi, lane);
-    if (lane == 0) {
-      const float2 f = rep[l];
-      const float gx = 4.f * (alpha * a.x - f.x * invZ);
-      const float gy = 4.f * (alpha * a.y - f.y * invZ);
-      float2 v = V[l], gn = G[l], y = yi;
-      update_coord(gx, v.x, gn.x, y.x, mu, sc.eta, sc.min_gain);
-      update_coord(gy, v.y, gn.y, y.y, mu, sc.eta, sc.min_gain);
-      V[l] = v;
-      G[l] = gn;
-      Yout[l] = y;
-      if (flag && !(isfinite(y.x) && isfinite(y.y))) *flag = 1;
-    }
+  const float shx = box->shift_x, shy = box->shift_y;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n_local; l += gridDim.x * blockDim.x) {
+    const float2 a = A[l], f = rep[l];
+    const float gx = 4.f * (alpha * a.x - f.x * invZ);
+    const float gy = 4.f * (alpha * a.y - f.y * invZ);
+    float2 v = V[l], gn = G[l], y = Y[row0 + l];
+    y.x = y.x - shx;
+    y.y = y.y - shy;
+    update_coord(gx, v.x, gn.x, y.x, mu, sc.eta, sc.min_gain);
+    update_coord(gy, v.y, gn.y, y.y, mu, sc.eta, sc.min_gain);
+    V[l] = v;
+    G[l] = gn;
+    Yout[l] = y;
+    if (flag && !(isfinite(y.x) && isfinite(y.y))) *flag = 1;
   }
 }
 
-tsne_status launch_attract_update_shard(const int64_t* row_ptr, const int32_t* col,
-                                        const float* val, const float2* Y, int64_t row0,
-                                        int64_t n_local, const float2* rep, const double* zp,
-                                        int world, int t, const Sched& sc, float2* V, float2* G,
-                                        float2* Yout, int32_t* flag, cudaStream_t s) {
+tsne_status launch_attract_sum_shard(const int64_t* row_ptr, const int32_t* col, const float* val,
+                                     const float2* Y, int64_t row0, int64_t n_local, float2* A,
+                                     cudaStream_t s) {
   if (n_local <= 0) return TSNE_OK;
-  k_attract_update_shard<<<attract_blocks(n_local), kAttrThreads, 0, s>>>(
-      row_ptr, col, val, Y, (int)row0, (int)n_local, rep, zp, world, t, sc, V, G, Yout, flag);
+  k_attract_sum_shard<<<attract_blocks(n_local), kAttrThreads, 0, s>>>(row_ptr, col, val, Y,
+                                                                       (int)row0, (int)n_local, A);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
+tsne_status launch_update_shard(const float2* A, const float2* Y, int64_t row0, int64_t n_local,
+                                const float2* rep, const double* zp, int world, int t,
+                                const Sched& sc, const BoxInfo* box, float2* V, float2* G,
+                                float2* Yout, int32_t* flag, cudaStream_t s) {
+  if (n_local <= 0) return TSNE_OK;
+  k_update_shard<<<update_blocks(n_local), kAttrThreads, 0, s>>>(A, Y, (int)row0, (int)n_local,
+                                                                 rep, zp, world, t, sc, box, V, G,
+                                                                 Yout, flag);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }

@@ -46,18 +46,17 @@ __global__ void k_recentre(float2* Y, int N, const BoxInfo* box) {
   Y[i] = y;
 }
 
-tsne_status shard_forces(ShardWS& w, float2* Y, int64_t N, int64_t row0, int64_t row1,
+tsne_status shard_forces(ShardWS& w, const float2* Y, int64_t N, int64_t row0, int64_t row1,
                          float theta, bool recentre, float2* rep_local, double* z_partial,
                          cudaStream_t s) {
+  // Y is read-only: the recentring shift (D15) is computed here (box->shift)
+  // and applied on the fly by the tree build and by the update of the owned
+  // rows (tsne_shard_update), so the attractive pass may read Y concurrently
   TreeWS& t = w.tree;
   TSNE_CUDA_TRY(cudaMemsetAsync(t.counter, 0, 8 * sizeof(unsigned), s));
   tsne_status st = recentre ? launch_bbox_mean(t, Y, s) : launch_bbox(t, Y, s);
   if (st != TSNE_OK) return st;
-  if (recentre) {            // the replicated embedding is recentred in place (D15)
-    k_recentre<<<(int)((N + 255) / 256), 256, 0, s>>>(Y, (int)N, t.box);
-    TSNE_LAUNCH_CHECK();
-  }
-  if ((st = build_tree(t, Y, /*apply_shift=*/false, s)) != TSNE_OK) return st;
+  if ((st = build_tree(t, Y, /*apply_shift=*/true, s)) != TSNE_OK) return st;
   const int n = (int)N;
   k_owned_flags<<<(n + 256) / 256, 256, 0, s>>>(t.perm, n, (int)row0, (int)row1, w.flags);
   TSNE_LAUNCH_CHECK();

@@ -3,9 +3,11 @@
 //  k_bbox        step 1: exact min/max, root box (D8)         [H1]
 //  k_keys        fp64 quantisation -> 32-bit Morton key (D8)  [H2]
 //  radix sort    (key, point id) pairs                         [H2]
-//  k_gather      Y in Morton order + fixed-point coordinates
-//  scan          exclusive prefix sums (integers: exact, deterministic)
-//  k_karras      binary radix tree over the sorted keys        [H3]
+//  k_gather      Y in Morton order + fixed-point coordinates + block sums
+//  k_bscan       exclusive scan of the block sums (one block)
+//  k_karras      binary radix tree over the sorted keys        [H3], and the
+//                exclusive prefix sums of the fixed-point coordinates
+//                (integers: exact, deterministic)
 //  k_quad_rank   which binary nodes are quad cells; chain rank [H3]
 //  scan          quad-node count per start position -> pre-order index
 //  k_quad_emit   pre-order node records, counts, centres of mass [H3, H4]
@@ -35,8 +37,6 @@ size_t tree_cub_bytes(int64_t N, size_t* sort_b, size_t* scan_b, size_t* scan2_b
   cub::DoubleBuffer<uint32_t> dk(nullptr, nullptr);
   cub::DoubleBuffer<int32_t> dv(nullptr, nullptr);
   cub::DeviceRadixSort::SortPairs(nullptr, a, dk, dv, (int)N, 0, 32);
-  cub::DeviceScan::ExclusiveScan(nullptr, b, (longlong2*)nullptr, (longlong2*)nullptr, LL2Sum(),
-                                 make_longlong2(0, 0), (int)(N + 1));
   cub::DeviceScan::ExclusiveSum(nullptr, c, (int32_t*)nullptr, (int32_t*)nullptr, (int)(N + 1));
   if (sort_b) *sort_b = a;
   if (scan_b) *scan_b = b;
@@ -57,8 +57,8 @@ void carve_tree(Carver& c, TreeWS& w, int64_t N) {
   w.ys = c.take<float2>(N);
   w.fq = c.take<longlong2>(N + 1);
   w.S = c.take<longlong2>(N + 1);
-  w.scan_tmp = c.take<char>(cb);
-  w.scan_tmp_bytes = cb;
+  w.bsum = c.take<longlong2>((N + 1 + 255) / 256 + 1);
+  (void)cb;
   w.bfirst = c.take<int32_t>(N);
   w.blast = c.take<int32_t>(N);
   w.bdelta = c.take<int32_t>(N);
@@ -245,22 +245,71 @@ __global__ void k_keys(const float2* __restrict__ Y, int N, const BoxInfo* __res
 }
 
 // ---------------------------------------------------------------- gather
-__global__ void k_gather(const float2* __restrict__ Y, const int32_t* __restrict__ perm, int N,
-                         const BoxInfo* __restrict__ box, int apply_shift, float2* __restrict__ ys,
-                         longlong2* __restrict__ fq) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k > N) return;
-  if (k == N) { fq[N] = make_longlong2(0, 0); return; }
-  float2 y = Y[perm[k]];
-  if (apply_shift) {
-    y.x = y.x - box->shift_x;
-    y.y = y.y - box->shift_y;
+constexpr int kScanBlock = 256;   // k_gather / k_karras block = prefix-sum block
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(kScanBlock)
+k_gather(const float2* __restrict__ Y, const int32_t* __restrict__ perm, int N,
+         const BoxInfo* __restrict__ box, int apply_shift, float2* __restrict__ ys,
+         longlong2* __restrict__ fq, longlong2* __restrict__ bsum) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  long long qx = 0, qy = 0;
+  if (k < N) {
+    float2 y = Y[perm[k]];
+    if (apply_shift) {
+      y.x = y.x - box->shift_x;
+      y.y = y.y - box->shift_y;
+    }
+    ys[k] = y;
+    const double cx = box->cx, cy = box->cy, inv = kFixScale / box->r0;
+    qx = __double2ll_rn(__dmul_rn(__dsub_rn((double)y.x, cx), inv));
+    qy = __double2ll_rn(__dmul_rn(__dsub_rn((double)y.y, cy), inv));
   }
-  ys[k] = y;
-  const double cx = box->cx, cy = box->cy, inv = kFixScale / box->r0;
-  long long qx = __double2ll_rn(__dmul_rn(__dsub_rn((double)y.x, cx), inv));
-  long long qy = __double2ll_rn(__dmul_rn(__dsub_rn((double)y.y, cy), inv));
-  fq[k] = make_longlong2(qx, qy);
+  if (k <= N) fq[k] = make_longlong2(qx, qy);      // fq[N] = 0
+  // block sum (exact integer arithmetic: the order does not matter)
+  __shared__ long long sx[kScanBlock / 32], sy[kScanBlock / 32];
+  qx = warp_sum_ll(qx);
+  qy = warp_sum_ll(qy);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { sx[wid] = qx; sy[wid] = qy; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long tx = 0, ty = 0;
+    for (int q = 0; q < kScanBlock / 32; ++q) { tx += sx[q]; ty += sy[q]; }
+    bsum[blockIdx.x] = make_longlong2(tx, ty);
+  }
+}
+
+// exclusive scan of the nb block sums, in place (one block)
+__global__ void __launch_bounds__(1024) k_bscan(longlong2* __restrict__ bsum, int nb) {
+  __shared__ long long sx[1024], sy[1024];
+  const int t = threadIdx.x;
+  const int per = (nb + 1023) / 1024;
+  const int b0 = t * per, b1 = min(nb, b0 + per);
+  long long tx = 0, ty = 0;
+  for (int b = b0; b < b1; ++b) { tx += bsum[b].x; ty += bsum[b].y; }
+  sx[t] = tx;
+  sy[t] = ty;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {               // Hillis-Steele inclusive scan
+    const long long ax = t >= o ? sx[t - o] : 0, ay = t >= o ? sy[t - o] : 0;
+    __syncthreads();
+    sx[t] += ax;
+    sy[t] += ay;
+    __syncthreads();
+  }
+  long long ox = sx[t] - tx, oy = sy[t] - ty;          // exclusive offset of this thread
+  for (int b = b0; b < b1; ++b) {
+    const longlong2 v = bsum[b];
+    bsum[b] = make_longlong2(ox, oy);
+    ox += v.x;
+    oy += v.y;
+  }
 }
 
 // ---------------------------------------------------------------- H3 Karras
@@ -271,10 +320,30 @@ __device__ __forceinline__ int kdelta(const uint32_t* __restrict__ k, int N, int
   return 32 + __clz((uint32_t)a ^ (uint32_t)b);
 }
 
-__global__ void k_karras(const uint32_t* __restrict__ keys, int N, int32_t* __restrict__ bfirst,
-                         int32_t* __restrict__ blast, int32_t* __restrict__ bdelta,
-                         int32_t* __restrict__ bparent, int32_t* __restrict__ lparent) {
+__global__ void __launch_bounds__(kScanBlock)
+k_karras(const uint32_t* __restrict__ keys, int N, int32_t* __restrict__ bfirst,
+         int32_t* __restrict__ blast, int32_t* __restrict__ bdelta, int32_t* __restrict__ bparent,
+         int32_t* __restrict__ lparent, const longlong2* __restrict__ fq,
+         const longlong2* __restrict__ boff, longlong2* __restrict__ S) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
+  {
+    // S[i] = boff[block] + exclusive scan of fq within the block (i <= N)
+    const longlong2 v = i <= N ? fq[i] : make_longlong2(0, 0);
+    long long ix = v.x, iy = v.y;                    // inclusive warp scan
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long ax = __shfl_up_sync(0xffffffffu, ix, o);
+      const long long ay = __shfl_up_sync(0xffffffffu, iy, o);
+      if (lane >= o) { ix += ax; iy += ay; }
+    }
+    __shared__ long long wx[kScanBlock / 32], wy[kScanBlock / 32];
+    if (lane == 31) { wx[wid] = ix; wy[wid] = iy; }
+    __syncthreads();
+    long long ox = boff[blockIdx.x].x, oy = boff[blockIdx.x].y;
+    for (int q = 0; q < wid; ++q) { ox += wx[q]; oy += wy[q]; }
+    if (i <= N) S[i] = make_longlong2(ox + ix - v.x, oy + iy - v.y);
+  }
   if (i >= N - 1) return;
   int d = (kdelta(keys, N, i, i + 1) - kdelta(keys, N, i, i - 1)) >= 0 ? 1 : -1;
   int dmin = kdelta(keys, N, i, i - d);
@@ -403,13 +472,13 @@ tsne_status build_tree(TreeWS& w, const float2* Y, bool apply_shift, cudaStream_
   TSNE_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, sb, dk, dv, N, 0, 32, s));
   w.keys_sorted = dk.Current();
   w.perm = dv.Current();
-  k_gather<<<cdiv(N + 1, T), T, 0, s>>>(Y, w.perm, N, w.box, apply_shift ? 1 : 0, w.ys, w.fq);
+  const int nb = cdiv(N + 1, kScanBlock);
+  k_gather<<<nb, kScanBlock, 0, s>>>(Y, w.perm, N, w.box, apply_shift ? 1 : 0, w.ys, w.fq, w.bsum);
   TSNE_LAUNCH_CHECK();
-  size_t cb = w.scan_tmp_bytes;
-  TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveScan(w.scan_tmp, cb, w.fq, w.S, LL2Sum(),
-                                               make_longlong2(0, 0), N + 1, s));
-  k_karras<<<cdiv(N - 1, T), T, 0, s>>>(w.keys_sorted, N, w.bfirst, w.blast, w.bdelta, w.bparent,
-                                         w.lparent);
+  k_bscan<<<1, 1024, 0, s>>>(w.bsum, nb);
+  TSNE_LAUNCH_CHECK();
+  k_karras<<<nb, kScanBlock, 0, s>>>(w.keys_sorted, N, w.bfirst, w.blast, w.bdelta, w.bparent,
+                                      w.lparent, w.fq, w.bsum, w.S);
   TSNE_LAUNCH_CHECK();
   k_quad_rank<<<cdiv(2 * N - 1, T), T, 0, s>>>(N, w.bfirst, w.bdelta, w.bparent, w.lparent,
                                                 w.rank, w.cnt);

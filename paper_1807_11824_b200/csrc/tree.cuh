@@ -44,8 +44,7 @@ struct TreeWS {
   float2* ys = nullptr;        // Y in Morton order
   longlong2* fq = nullptr;     // fixed-point coordinates (N+1)
   longlong2* S = nullptr;      // exclusive prefix sums of fq (N+1)
-  void* scan_tmp = nullptr;
-  size_t scan_tmp_bytes = 0;
+  longlong2* bsum = nullptr;   // per 256-point block sums of fq, then their exclusive scan
   int32_t *bfirst = nullptr, *blast = nullptr, *bdelta = nullptr;
   int32_t *bparent = nullptr, *lparent = nullptr;
   int32_t* rank = nullptr;     // 2N-1 binary nodes

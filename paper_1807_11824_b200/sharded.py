@@ -5,8 +5,10 @@ is single-GPU, P:L173).
 Per iteration, on every rank:
   1. forces   -- quadtree over the full replicated embedding (redundant, small),
                  theta traversal for the owned points, partial Z   [C ABI]
+  1'. attract -- attractive sums of the owned rows, on a side stream
+                 concurrently with 1 (it only reads Y)              [C ABI]
   2. exchange -- all-gather the partial Z of every rank (rank order)  [NCCL]
-  3. update   -- attractive pass + Eq. 7 + D12 update of the owned rows [C ABI]
+  3. update   -- Eq. 7 + D12 update of the owned rows (recentred)    [C ABI]
   4. exchange -- all-gather the updated Y shards                      [NCCL]
 The host logic (ranges, exchange order, padding) lives here; all arithmetic
 runs in the library's kernels (`GpuShardOps`).  The ops object is injectable
@@ -90,14 +92,19 @@ class GpuShardOps:
                                                P(rep_local), P(zpart), P(self.ws), self.ws.numel(),
                                                self._stream()), "tsne_shard_forces")
 
-    def update(self, rp, col, val, N, row0, row1, Y, rep_local, zparts, world, t, lr, exag, cfg,
+    def attract(self, rp, col, val, N, row0, row1, Y, A_local):
+        P = self._ptr
+        self._check(self.lib.tsne_shard_attract(P(rp), P(col), P(val), N, row0, row1, P(Y),
+                                                P(A_local), self._stream()), "tsne_shard_attract")
+
+    def update(self, A_local, N, row0, row1, Y, rep_local, zparts, world, t, lr, exag, cfg,
                v_local, g_local, Y_out):
         P = self._ptr
-        self._check(self.lib.tsne_shard_update(P(rp), P(col), P(val), N, row0, row1, P(Y),
-                                               P(rep_local), P(zparts), world, int(t), float(lr),
-                                               float(exag), C.byref(cfg), P(v_local), P(g_local),
-                                               P(Y_out), P(self.flag), self._stream()),
-                    "tsne_shard_update")
+        self._check(self.lib.tsne_shard_update(P(A_local), N, row0, row1, P(Y), P(rep_local),
+                                               P(zparts), world, int(t), float(lr), float(exag),
+                                               C.byref(cfg), P(v_local), P(g_local), P(Y_out),
+                                               P(self.flag), P(self.ws), self.ws.numel(),
+                                               self._stream()), "tsne_shard_update")
 
     def recentre(self, Y, N):
         P = self._ptr
@@ -134,6 +141,8 @@ class ShardedOptimizer:
         self.v = torch.zeros(max(n_local, 1), 2, dtype=torch.float32, device=dev)
         self.g = torch.ones(max(n_local, 1), 2, dtype=torch.float32, device=dev)
         self.rep = torch.zeros(max(n_local, 1), 2, dtype=torch.float32, device=dev)
+        self.A = torch.zeros(max(n_local, 1), 2, dtype=torch.float32, device=dev)
+        self.side = torch.cuda.Stream(device=dev) if dev.type == "cuda" else None
         self.zpart = torch.zeros(2, dtype=torch.float64, device=dev)
         self.zparts = torch.zeros(self.world * 2, dtype=torch.float64, device=dev)
         self.ops = ops if ops is not None else GpuShardOps(N, dev)
@@ -153,12 +162,23 @@ class ShardedOptimizer:
         self._graphs = {}
 
     def _iteration(self):
+        if self.side is not None:          # attractive pass concurrently with the tree work
+            main = torch.cuda.current_stream()
+            self.side.wait_stream(main)
+            with torch.cuda.stream(self.side):
+                self.ops.attract(self.rp, self.col, self.val, self.N, self.row0, self.row1,
+                                 self.Y, self.A)
+        else:
+            self.ops.attract(self.rp, self.col, self.val, self.N, self.row0, self.row1, self.Y,
+                             self.A)
         self.ops.forces(self.Y, self.N, self.row0, self.row1, self.theta,
                         self.pending_recentre, self.rep, self.zpart)
+        if self.side is not None:
+            torch.cuda.current_stream().wait_stream(self.side)
         _all_gather_flat(self.zparts, self.zpart, self.group)
-        self.ops.update(self.rp, self.col, self.val, self.N, self.row0, self.row1, self.Y,
-                        self.rep, self.zparts, self.world, self.t, self.lr, self.exag,
-                        self.cfg, self.v, self.g, self.Yloc)
+        self.ops.update(self.A, self.N, self.row0, self.row1, self.Y, self.rep, self.zparts,
+                        self.world, self.t, self.lr, self.exag, self.cfg, self.v, self.g,
+                        self.Yloc)
         _all_gather_flat(self.Yfull, self.Yloc, self.group)
 
     def step(self, n_iter: int = 1):

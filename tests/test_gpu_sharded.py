@@ -48,17 +48,19 @@ def test_virtual_shards_match_single_gpu(T, orc, prob, G):
         a, b, S = shard_range(N, G, r)
         shards.append((a, b, *local_csr(rp_d, col_d, val_d, a, b),
                        torch.zeros(b - a, 2, device=dev), torch.ones(b - a, 2, device=dev),
-                       torch.zeros(b - a, 2, device=dev)))
+                       torch.zeros(b - a, 2, device=dev), torch.zeros(b - a, 2, device=dev),
+                       GpuShardOps(N, dev)))       # one workspace (tree, shift) per rank
     Y = Y0.clone()
     zp = torch.zeros(G * 2, dtype=torch.float64, device=dev)
     n_iter = 3        # trajectories diverge chaotically; compare a few iterations
     for t in range(n_iter):
-        for r, (a, b, rpl, cl, vl, v, g, rep) in enumerate(shards):
-            ops.forces(Y, N, a, b, 0.5, t > 0, rep, zp[2 * r:2 * r + 2])
+        for r, (a, b, rpl, cl, vl, v, g, rep, A, o) in enumerate(shards):
+            o.attract(rpl, cl, vl, N, a, b, Y, A)
+            o.forces(Y, N, a, b, 0.5, t > 0, rep, zp[2 * r:2 * r + 2])
         Ynew = torch.empty_like(Y)
-        for r, (a, b, rpl, cl, vl, v, g, rep) in enumerate(shards):
+        for r, (a, b, rpl, cl, vl, v, g, rep, A, o) in enumerate(shards):
             out = torch.empty(b - a, 2, device=dev)
-            ops.update(rpl, cl, vl, N, a, b, Y, rep, zp, G, t, 200.0, 12.0, cfg, v, g, out)
+            o.update(A, N, a, b, Y, rep, zp, G, t, 200.0, 12.0, cfg, v, g, out)
             Ynew[a:b] = out
         Y = Ynew
     ops.recentre(Y, N)

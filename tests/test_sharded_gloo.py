@@ -21,36 +21,42 @@ class Cfg:
 
 
 class OracleShardOps:
-    """Per-rank compute from the oracle (fp64 inside, fp32 state like the GPU)."""
+    """Per-rank compute from the oracle (fp64 inside, fp32 state like the GPU),
+    with the C ABI's contract: forces leaves Y untouched and records the
+    recentring shift; update applies it to the owned rows."""
 
     def __init__(self, rp, col, val):
         self.rp, self.col, self.val = rp, col, val
+        self.shift = np.zeros(2, np.float32)
 
     def forces(self, Y, N, row0, row1, theta, recentre, rep_local, zpart):
         import oracle
-        if recentre:
-            self.recentre(Y, N)
-        f, z, _, _ = oracle.repulsive_bh(Y.numpy(), theta, pts=np.arange(row0, row1))
+        self.shift = (Y.double().mean(0).float().numpy() if recentre
+                      else np.zeros(2, np.float32))
+        Ys = (Y - torch.as_tensor(self.shift)).numpy()
+        f, z, _, _ = oracle.repulsive_bh(Ys, theta, pts=np.arange(row0, row1))
         rep_local[: row1 - row0] = torch.as_tensor(f, dtype=torch.float32)
         zpart[0] = float(z.sum())
 
-    def update(self, rp, col, val, N, row0, row1, Y, rep, zparts, world, t, lr, exag, cfg,
-               v, g, Yout):
+    def attract(self, rp, col, val, N, row0, row1, Y, A_local):
         import oracle
+        A = oracle.attractive(self.rp, self.col, self.val, Y.numpy())[row0:row1]
+        A_local[: row1 - row0] = torch.as_tensor(A, dtype=torch.float32)
+
+    def update(self, A_local, N, row0, row1, Y, rep, zparts, world, t, lr, exag, cfg, v, g, Yout):
         Z = 0.0
         for r in range(world):
             Z += float(zparts[2 * r])
-        A = oracle.attractive(self.rp, self.col, self.val, Y.numpy())[row0:row1]
         alpha = exag if t < cfg.exag_iters else 1.0
         mu = cfg.mom0 if t < cfg.exag_iters else cfg.mom1
         n = row1 - row0
-        gr = 4.0 * (alpha * A - rep[:n].double().numpy() / Z)
+        gr = 4.0 * (alpha * A_local[:n].double().numpy() - rep[:n].double().numpy() / Z)
         vv = v[:n].double().numpy()
         gg = g[:n].double().numpy()
         gg = np.where(np.sign(gr) != np.sign(vv), gg + 0.2, gg * 0.8)
         gg = np.maximum(gg, cfg.min_gain)
         vv = mu * vv - lr * gg * gr
-        y = Y[row0:row1].double().numpy() + vv
+        y = (Y[row0:row1] - torch.as_tensor(self.shift)).double().numpy() + vv
         v[:n] = torch.as_tensor(vv, dtype=torch.float32)
         g[:n] = torch.as_tensor(gg, dtype=torch.float32)
         Yout[:n] = torch.as_tensor(y, dtype=torch.float32)
@@ -144,11 +150,13 @@ def test_gloo_sharded_equals_unsharded(tmp_path, world):
     v = torch.zeros(N, 2)
     g = torch.ones(N, 2)
     rep = torch.zeros(N, 2)
+    A = torch.zeros(N, 2)
     zp = torch.zeros(2, dtype=torch.float64)
     Yn = torch.zeros(N, 2)
     for t in range(n_iter):
+        ops.attract(None, None, None, N, 0, N, Y, A)
         ops.forces(Y, N, 0, N, 0.5, t > 0, rep, zp)
-        ops.update(None, None, None, N, 0, N, Y, rep, zp, 1, t, 200.0, 12.0, Cfg(), v, g, Yn)
+        ops.update(A, N, 0, N, Y, rep, zp, 1, t, 200.0, 12.0, Cfg(), v, g, Yn)
         Y = Yn.clone()
     ops.recentre(Y, N)
     Y1 = Y.double().numpy()
