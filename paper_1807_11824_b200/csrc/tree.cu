@@ -285,25 +285,37 @@ k_gather(const float2* __restrict__ Y, const int32_t* __restrict__ perm, int N,
   }
 }
 
-// exclusive scan of the nb block sums, in place (one block)
+// exclusive scan of the nb block sums, in place (one block): per-thread
+// serial sums, warp shuffle scans, one warp over the 32 warp totals
 __global__ void __launch_bounds__(1024) k_bscan(longlong2* __restrict__ bsum, int nb) {
-  __shared__ long long sx[1024], sy[1024];
-  const int t = threadIdx.x;
+  __shared__ long long wx[32], wy[32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int per = (nb + 1023) / 1024;
   const int b0 = t * per, b1 = min(nb, b0 + per);
   long long tx = 0, ty = 0;
-  for (int b = b0; b < b1; ++b) { tx += bsum[b].x; ty += bsum[b].y; }
-  sx[t] = tx;
-  sy[t] = ty;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {               // Hillis-Steele inclusive scan
-    const long long ax = t >= o ? sx[t - o] : 0, ay = t >= o ? sy[t - o] : 0;
-    __syncthreads();
-    sx[t] += ax;
-    sy[t] += ay;
-    __syncthreads();
+  for (int b = b0; b < b1; ++b) { const longlong2 v = bsum[b]; tx += v.x; ty += v.y; }
+  long long ix = tx, iy = ty;                          // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long ax = __shfl_up_sync(0xffffffffu, ix, o);
+    const long long ay = __shfl_up_sync(0xffffffffu, iy, o);
+    if (lane >= o) { ix += ax; iy += ay; }
   }
-  long long ox = sx[t] - tx, oy = sy[t] - ty;          // exclusive offset of this thread
+  if (lane == 31) { wx[wid] = ix; wy[wid] = iy; }
+  __syncthreads();
+  if (wid == 0) {
+    long long vx = wx[lane], vy = wy[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long ax = __shfl_up_sync(0xffffffffu, vx, o);
+      const long long ay = __shfl_up_sync(0xffffffffu, vy, o);
+      if (lane >= o) { vx += ax; vy += ay; }
+    }
+    wx[lane] = vx;                                     // inclusive over warps
+    wy[lane] = vy;
+  }
+  __syncthreads();
+  long long ox = (wid ? wx[wid - 1] : 0) + ix - tx, oy = (wid ? wy[wid - 1] : 0) + iy - ty;
   for (int b = b0; b < b1; ++b) {
     const longlong2 v = bsum[b];
     bsum[b] = make_longlong2(ox, oy);
