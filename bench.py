@@ -302,11 +302,11 @@ def run_ours(args, rank, world):
 
     # roofline of the dominant kernel
     hbm, which = peaks()
-    # k_attract_sum, algorithmic bytes per launch: col + val (8 B/nnz), row_ptr
+    # k_attract_tma, algorithmic bytes per launch: col + val (8 B/nnz), row_ptr
     # (8 B/row), y_i (8 B/row), A out (8 B/row); the y_j gathers hit L2 (Y = 10 MB)
     bytes_attr = 8 * nnz + 8 * (N + 1) + 16 * N
     bytes_upd = 64 * N             # k_update: A, f, y, v, gains in; y', v, gains out
-    stage_kern = {"attract_ms": "k_attract_sum", "traverse_ms": "k_traverse",
+    stage_kern = {"attract_ms": "k_attract_tma", "traverse_ms": "k_traverse",
                   "tree_ms": "tree build (10 kernels)", "update_ms": "k_update"}
     kern = max(stage_kern, key=lambda k: prof[k])
     traffic = None

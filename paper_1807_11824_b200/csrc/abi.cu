@@ -314,7 +314,7 @@ tsne_status tsne_shard_attract(const int64_t* row_ptr_local, const int32_t* col_
   tsne_status st = check_device();
   if (st != TSNE_OK) return st;
   return launch_attract_sum_shard(row_ptr_local, col_local, val_local,
-                                  reinterpret_cast<const float2*>(Y), row0, row1 - row0,
+                                  reinterpret_cast<const float2*>(Y), N, row0, row1 - row0,
                                   reinterpret_cast<float2*>(A_local), (cudaStream_t)stream);
 }
 

@@ -13,78 +13,258 @@
 // bounding box (fixed-order last-block reduction), so the tree build of the
 // next iteration needs no separate bbox pass.
 #include "optimize.cuh"
+#include "tc_ptx.cuh"
 
 namespace tsne {
 
 constexpr int kAttrThreads = 256;
 constexpr int kAttrWarps = kAttrThreads / 32;
-constexpr int kAttrBlocksPerSM = 4;
 
-// One warp per row.  The row's nonzeros are read as 16-byte vectors from the
-// 16-byte-aligned window around [e0, e1) (lanes masked outside the row), so
-// each lane has 4 independent y_j gathers in flight per vector; the row sum is
-// reduced with a fixed butterfly (deterministic).
-__device__ __forceinline__ float2 row_attractive(const int64_t e0, const int64_t e1,
-                                                 const int64_t nnz,
-                                                 const int32_t* __restrict__ col,
-                                                 const float* __restrict__ val,
-                                                 const float2* __restrict__ Y, int i, float2 yi,
-                                                 int lane) {
-  float ax = 0.f, ay = 0.f;
-  for (int64_t b = (e0 & ~int64_t(3)) + 4 * lane; b < e1; b += 128) {
-    int c[4];
-    float p[4];
-    if (b + 3 < nnz) {
-      const int4 cv = __ldcs(reinterpret_cast<const int4*>(col + b));
-      const float4 pv = __ldcs(reinterpret_cast<const float4*>(val + b));
-      c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
-      p[0] = pv.x; p[1] = pv.y; p[2] = pv.z; p[3] = pv.w;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool ok = b + q < nnz;
-        c[q] = ok ? __ldcs(col + b + q) : i;
-        p[q] = ok ? __ldcs(val + b + q) : 0.f;
-      }
-    }
-    float2 yj[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const bool in = (b + q >= e0) && (b + q < e1);
-      if (!in) { c[q] = i; p[q] = 0.f; }
-      yj[q] = Y[c[q]];
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float dx = yi.x - yj[q].x, dy = yi.y - yj[q].y;
-      const float w = __frcp_rn(1.f + dx * dx + dy * dy);
-      const float pw = p[q] * w;
-      ax = fmaf(pw, dx, ax);
-      ay = fmaf(pw, dy, ay);
-    }
-  }
-  return make_float2(warp_sum(ax), warp_sum(ay));
+// ---------------------------------------------------------------- H7
+// Attractive pass as a persistent TMA pipeline (one CTA per SM).  The CTA
+// owns a contiguous range of rows, cut into batches of kAtRows rows.  A
+// producer warp streams each batch's col/val span (contiguous in the CSR)
+// into a kAtStages-deep shared-memory ring with cp.async.bulk + mbarriers
+// (the bulk copies keep ~3 batches of the 8-byte-per-nonzero stream in flight
+// per SM without holding registers); the embedding window
+// Y[wlo, wlo + kAtWin) around the CTA's rows is staged once the same way.
+// Two groups of kAtRows consumer warps take alternate batches (latency hiding
+// for the L2 gathers); warp w of a group computes row w of its batches: lanes take consecutive
+// nonzeros from shared memory, gather y_j from the window (columns outside it,
+// rare once the labels are in a locality order -- DESIGN.md 6.4-6.5 -- come
+// from L2), and reduce with a fixed butterfly (deterministic; the result does
+// not depend on which path an operand came from).  A batch whose span does
+// not fit a stage buffer is read from global memory directly.
+#ifndef TSNE_AT_ROWS
+#define TSNE_AT_ROWS 15
+#define TSNE_AT_GROUPS 2
+#define TSNE_AT_STAGES 4
+#define TSNE_AT_CAP 4096
+#define TSNE_AT_WIN 12288
+#endif
+constexpr int kAtRows = TSNE_AT_ROWS;          // rows per batch: one per consumer warp of a group
+constexpr int kAtGroups = TSNE_AT_GROUPS;      // consumer groups take alternate batches
+constexpr int kAtConsumers = kAtRows * kAtGroups;
+constexpr int kAtThreads = (kAtConsumers + 1) * 32;
+constexpr int kAtStages = TSNE_AT_STAGES;
+constexpr int kAtCap = TSNE_AT_CAP;            // nonzeros per stage buffer
+constexpr int kAtWin = TSNE_AT_WIN;            // window points
+constexpr int kAtLook = 4;                     // row_ptr prefetch distance (batches)
+constexpr int kAtRpSlots = kAtLook + 1;
+static_assert(kAtStages % kAtGroups == 0, "a stage always serves the same consumer group");
+constexpr size_t kAtSmem = sizeof(float2) * kAtWin + (size_t)kAtStages * kAtCap * 8;
+
+struct AtMeta {
+  int64_t rp[kAtRows + 1];   // row_ptr of the batch's rows (local CSR)
+  int64_t a_lo, a_hi;        // staged nonzeros [a_lo, a_hi) (a_hi <= a_lo when not staged)
+  int32_t r0, nrows;         // first local row, rows in the batch
+};
+
+__device__ __forceinline__ float rcp_approx_f(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
-// tsne_gradient: dY = 4 (alpha A - f / Z)
-__global__ void __launch_bounds__(kAttrThreads)
-k_attract_grad(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-               const float* __restrict__ val, const float2* __restrict__ Y, int N,
-               const float2* __restrict__ rep, const double* __restrict__ Z, float alpha,
-               float2* __restrict__ dY) {
-  const int lane = threadIdx.x & 31;
-  const int warp = (blockIdx.x * kAttrThreads + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * kAttrThreads) >> 5;
-  const float invZ = (float)Z[1];
-  const int64_t nnz = row_ptr[N];
-  for (int i = warp; i < N; i += nwarps) {
-    const float2 yi = Y[i];
-    const float2 a = row_attractive(row_ptr[i], row_ptr[i + 1], nnz, col, val, Y, i, yi, lane);
-    if (lane == 0) {
-      const float2 f = rep[i];
-      dY[i] = make_float2(4.f * (alpha * a.x - f.x * invZ), 4.f * (alpha * a.y - f.y * invZ));
+// y_j from the window when j is inside it, else from L2 (branch-free: the
+// shared load is clamped into the window, the predicated global load
+// overwrites it for columns outside)
+__device__ __forceinline__ float2 win_y(uint32_t sbase, const float2* __restrict__ Y, int j,
+                                        int wlo, int wn) {
+  const unsigned o = (unsigned)(j - wlo);
+  const unsigned oc = min(o, (unsigned)(wn - 1));
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(sbase + oc * 8u));
+  asm("{\n\t.reg .pred p;\n\tsetp.ge.u32 p, %2, %3;\n\t@p ld.global.nc.v2.f32 {%0, %1}, [%4];\n\t}"
+      : "+f"(v.x), "+f"(v.y)
+      : "r"(o), "r"((unsigned)wn), "l"(Y + j));
+  return v;
+}
+
+__device__ __forceinline__ void win_accum(float2 yi, float2 yj, float p, float& ax, float& ay) {
+  const float dx = yi.x - yj.x, dy = yi.y - yj.y;
+  const float w = rcp_approx_f(fmaf(dy, dy, fmaf(dx, dx, 1.f)));   // 1/(1+d^2), d^2 >= 0
+  const float pw = p * w;
+  ax = fmaf(pw, dx, ax);
+  ay = fmaf(pw, dy, ay);
+}
+
+// spin wait (no suspend-time hint: the pipeline's waits are short and a
+// sleeping producer would throttle the stream)
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// MODE 0: out[l] = A_l.  MODE 1 (tsne_gradient): out[l] = 4 (alpha A_l - f_l / Z).
+// Rows l in [0, n_rows) of the (local) CSR are global points row0 + l of Y.
+template <int MODE>
+__global__ void __launch_bounds__(kAtThreads, 1)
+k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+              const float* __restrict__ val, const float2* __restrict__ Y, int Ny, int row0,
+              int n_rows, float2* __restrict__ out, const float2* __restrict__ rep,
+              const double* __restrict__ Z, float alpha) {
+  extern __shared__ __align__(128) unsigned char at_smem[];
+  __shared__ AtMeta s_meta[kAtStages];
+  __shared__ __align__(16) int64_t s_rpring[kAtRpSlots][kAtRows + 1];
+  __shared__ __align__(8) uint64_t s_full[kAtStages], s_empty[kAtStages], s_win;
+  float2* s_y = reinterpret_cast<float2*>(at_smem);
+  int32_t* s_col = reinterpret_cast<int32_t*>(at_smem + sizeof(float2) * kAtWin);
+  float* s_val = reinterpret_cast<float*>(s_col + kAtStages * kAtCap);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // this CTA's batches [kb0, kb1) -> rows [kb0 * kAtRows, min(kb1 * kAtRows, n_rows))
+  const int nb = (n_rows + kAtRows - 1) / kAtRows;
+  const int kb0 = (int)((int64_t)nb * blockIdx.x / gridDim.x);
+  const int kb1 = (int)((int64_t)nb * (blockIdx.x + 1) / gridDim.x);
+  const int lr0 = kb0 * kAtRows, lr1 = min(kb1 * kAtRows, n_rows);
+  int wlo = row0 + (lr0 + lr1) / 2 - kAtWin / 2;
+  wlo = min(wlo, Ny - kAtWin);
+  wlo = max(wlo, 0) & ~1;                      // 16-byte aligned source
+  const int wn = min(kAtWin, Ny - wlo) & ~1;   // 16-byte multiple
+  const uint32_t sbase = smem_u32(s_y);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kAtStages; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_empty[s], kAtRows);
     }
+    mbar_init(&s_win, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncthreads();
+
+  if (wid == kAtConsumers) {
+    // ------------------------------------------------------------ producer
+    const int64_t nnz4 = row_ptr[n_rows] & ~int64_t(3);
+    if (lane == 0) {
+      mbar_arrive_tx(&s_win, (uint32_t)(wn * sizeof(float2)));
+      bulk_g2s(sbase, Y + wlo, (uint32_t)(wn * sizeof(float2)), &s_win);
+    }
+    // row_ptr of batch kb + kAtLook is fetched with cp.async into a small ring
+    // while batch kb is issued, so the producer never waits on a global load
+    auto fetch_rp = [&](int kb) {
+      if (kb < kb1 && lane <= kAtRows) {
+        const int r = min(kb * kAtRows + lane, n_rows);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                         smem_u32(&s_rpring[kb % kAtRpSlots][lane])),
+                     "l"(row_ptr + r)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int j = 0; j < kAtLook; ++j) fetch_rp(kb0 + j);
+    for (int kb = kb0; kb < kb1; ++kb) {
+      const int k = kb - kb0, s = k % kAtStages;
+      if (k >= kAtStages) mbar_wait_spin(&s_empty[s], ((k / kAtStages) - 1) & 1);
+      fetch_rp(kb + kAtLook);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kAtLook) : "memory");
+      __syncwarp();
+      const int r0 = kb * kAtRows, nr = min(kAtRows, n_rows - r0);
+      AtMeta& m = s_meta[s];
+      const int64_t v = (lane <= kAtRows) ? s_rpring[kb % kAtRpSlots][lane] : 0;
+      if (lane <= kAtRows) m.rp[lane] = v;
+      const int64_t e_lo = __shfl_sync(0xffffffffu, v, 0);
+      const int64_t e_hi = __shfl_sync(0xffffffffu, v, nr);
+      const int64_t a_lo = e_lo & ~int64_t(3);
+      int64_t a_hi = min((e_hi + 3) & ~int64_t(3), nnz4);
+      if (e_hi + 3 - a_lo > kAtCap) a_hi = a_lo;              // does not fit: read from global
+      if (lane == 0) {
+        m.a_lo = a_lo;
+        m.a_hi = a_hi;
+        m.r0 = r0;
+        m.nrows = nr;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t cnt = (a_hi > a_lo) ? (uint32_t)(a_hi - a_lo) : 0u;
+        mbar_arrive_tx(&s_full[s], cnt * 8u);
+        if (cnt) {
+          bulk_g2s(smem_u32(s_col + s * kAtCap), col + a_lo, cnt * 4u, &s_full[s]);
+          bulk_g2s(smem_u32(s_val + s * kAtCap), val + a_lo, cnt * 4u, &s_full[s]);
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  mbar_wait_spin(&s_win, 0);
+  const int grp = wid / kAtRows, wr = wid % kAtRows;
+  for (int kb = kb0 + grp; kb < kb1; kb += kAtGroups) {
+    const int k = kb - kb0, s = k % kAtStages;
+    mbar_wait_spin(&s_full[s], (k / kAtStages) & 1);
+    const AtMeta& m = s_meta[s];
+    if (wr < m.nrows) {
+      const int l = m.r0 + wr;
+      const int i = row0 + l;
+      const int64_t e0 = m.rp[wr], e1 = m.rp[wr + 1];
+      const int64_t a_lo = m.a_lo, a_hi = m.a_hi;
+      const int32_t* cs = s_col + s * kAtCap;
+      const float* vs = s_val + s * kAtCap;
+      const float2 yi = win_y(sbase, Y, i, wlo, wn);
+      float ax = 0.f, ay = 0.f;
+      const int n = (int)(e1 - e0);
+      if (e0 >= a_lo && e1 <= a_hi) {             // the row is staged (the common case)
+        const int32_t* cr = cs + (e0 - a_lo);
+        const float* vr = vs + (e0 - a_lo);
+#pragma unroll 4
+#pragma unroll 4
+        for (int q = lane; q < n; q += 32)
+          win_accum(yi, win_y(sbase, Y, cr[q], wlo, wn), vr[q], ax, ay);
+      } else {
+        for (int q = lane; q < n; q += 32)
+          win_accum(yi, win_y(sbase, Y, __ldcs(col + e0 + q), wlo, wn), __ldcs(val + e0 + q), ax,
+                    ay);
+      }
+      ax = warp_sum(ax);
+      ay = warp_sum(ay);
+      if (lane == 0) {
+        if (MODE == 0) {
+          out[l] = make_float2(ax, ay);
+        } else {
+          const float invZ = (float)Z[1];
+          const float2 f = rep[l];
+          out[l] = make_float2(4.f * (alpha * ax - f.x * invZ), 4.f * (alpha * ay - f.y * invZ));
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_empty[s]);
+  }
+}
+
+template <int MODE>
+static tsne_status launch_win(const int64_t* row_ptr, const int32_t* col, const float* val,
+                              const float2* Y, int64_t Ny, int64_t row0, int64_t n_rows,
+                              float2* out, const float2* rep, const double* Z, float alpha,
+                              cudaStream_t s) {
+  if (n_rows <= 0) return TSNE_OK;
+  static bool attr = false;                    // not a stream operation (graph-capture safe)
+  if (!attr) {
+    TSNE_CUDA_TRY(cudaFuncSetAttribute(k_attract_tma<MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAtSmem));
+    attr = true;
+  }
+  const int64_t nb = (n_rows + kAtRows - 1) / kAtRows;
+  const int blocks = (int)(nb < kNumSMs ? nb : kNumSMs);
+  k_attract_tma<MODE><<<blocks, kAtThreads, kAtSmem, s>>>(row_ptr, col, val, Y, (int)Ny,
+                                                           (int)row0, (int)n_rows, out, rep, Z,
+                                                           alpha);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
 }
 
 __device__ __forceinline__ float sgnf(float x) { return (float)((x > 0.f) - (x < 0.f)); }
@@ -97,24 +277,6 @@ __device__ __forceinline__ void update_coord(float g, float& v, float& gain, flo
   gain = gn;
   v = mu * v - eta * gn * g;
   y = y + v;
-}
-
-// Attractive sums only (H7): A_i for every row, written to A.  Independent of
-// the tree, the traversal and Z, so it runs concurrently with them on a side
-// stream; reads the unshifted Y (differences only).
-__global__ void __launch_bounds__(kAttrThreads)
-k_attract_sum(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-              const float* __restrict__ val, const float2* __restrict__ Y, int N,
-              float2* __restrict__ A) {
-  const int lane = threadIdx.x & 31;
-  const int warp = (blockIdx.x * kAttrThreads + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * kAttrThreads) >> 5;
-  const int64_t nnz = row_ptr[N];
-  for (int i = warp; i < N; i += nwarps) {
-    const float2 yi = Y[i];
-    const float2 a = row_attractive(row_ptr[i], row_ptr[i + 1], nnz, col, val, Y, i, yi, lane);
-    if (lane == 0) A[i] = a;
-  }
 }
 
 // The update (H8): Eq. 7 with the traversal's f and Z, the D12 step, the
@@ -224,32 +386,21 @@ k_update(const float2* __restrict__ Yin, const float2* __restrict__ A, int N,
   }
 }
 
-int attract_blocks(int64_t N) {
-  int64_t b = (N + kAttrWarps - 1) / kAttrWarps;
-  int64_t cap = (int64_t)kNumSMs * kAttrBlocksPerSM;
-  return (int)(b < cap ? (b < 1 ? 1 : b) : cap);
-}
-
-tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, const float* val,
-                                const float2* Y, int64_t N, const float2* rep, const double* Z,
-                                float alpha, float2* dY, cudaStream_t s) {
-  k_attract_grad<<<attract_blocks(N), kAttrThreads, 0, s>>>(row_ptr, col, val, Y, (int)N, rep, Z,
-                                                            alpha, dY);
-  TSNE_LAUNCH_CHECK();
-  return TSNE_OK;
-}
-
 int update_blocks(int64_t N) {
   int64_t b = (N + kAttrThreads - 1) / kAttrThreads;
   int64_t cap = (int64_t)kNumSMs * 8;
   return (int)(b < cap ? (b < 1 ? 1 : b) : cap);
 }
 
+tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, const float* val,
+                                const float2* Y, int64_t N, const float2* rep, const double* Z,
+                                float alpha, float2* dY, cudaStream_t s) {
+  return launch_win<1>(row_ptr, col, val, Y, N, 0, N, dY, rep, Z, alpha, s);
+}
+
 tsne_status launch_attract_sum(const int64_t* row_ptr, const int32_t* col, const float* val,
                                const float2* Y, int64_t N, float2* A, cudaStream_t s) {
-  k_attract_sum<<<attract_blocks(N), kAttrThreads, 0, s>>>(row_ptr, col, val, Y, (int)N, A);
-  TSNE_LAUNCH_CHECK();
-  return TSNE_OK;
+  return launch_win<0>(row_ptr, col, val, Y, N, 0, N, A, nullptr, nullptr, 1.f, s);
 }
 
 tsne_status launch_update(const float2* Yin, const float2* A, int64_t N, TreeWS& w, OptWS& o,
@@ -269,21 +420,6 @@ namespace tsne {
 // Rows [row0, row0 + n_local) of this rank: attractive pass against the full
 // replicated embedding, Eq. 7 with Z = the ranks' partial sums added in rank
 // order (deterministic), and the D12 update into the local shard.
-__global__ void __launch_bounds__(kAttrThreads)
-k_attract_sum_shard(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                    const float* __restrict__ val, const float2* __restrict__ Y, int row0,
-                    int n_local, float2* __restrict__ A) {
-  const int lane = threadIdx.x & 31;
-  const int warp = (blockIdx.x * kAttrThreads + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * kAttrThreads) >> 5;
-  const int64_t nnz = row_ptr[n_local];
-  for (int l = warp; l < n_local; l += nwarps) {
-    const int i = row0 + l;
-    const float2 a = row_attractive(row_ptr[l], row_ptr[l + 1], nnz, col, val, Y, i, Y[i], lane);
-    if (lane == 0) A[l] = a;
-  }
-}
-
 // Eq. 7 + D12 for the owned rows, Z = the ranks' partials added in rank
 // order; the pending recentring shift of this iteration (box->shift, D15) is
 // applied to the owned rows on the way out, so Y itself is never modified in
@@ -316,13 +452,9 @@ k_update_shard(const float2* __restrict__ A, const float2* __restrict__ Y, int r
 }
 
 tsne_status launch_attract_sum_shard(const int64_t* row_ptr, const int32_t* col, const float* val,
-                                     const float2* Y, int64_t row0, int64_t n_local, float2* A,
-                                     cudaStream_t s) {
-  if (n_local <= 0) return TSNE_OK;
-  k_attract_sum_shard<<<attract_blocks(n_local), kAttrThreads, 0, s>>>(row_ptr, col, val, Y,
-                                                                       (int)row0, (int)n_local, A);
-  TSNE_LAUNCH_CHECK();
-  return TSNE_OK;
+                                     const float2* Y, int64_t N, int64_t row0, int64_t n_local,
+                                     float2* A, cudaStream_t s) {
+  return launch_win<0>(row_ptr, col, val, Y, N, row0, n_local, A, nullptr, nullptr, 1.f, s);
 }
 
 tsne_status launch_update_shard(const float2* A, const float2* Y, int64_t row0, int64_t n_local,

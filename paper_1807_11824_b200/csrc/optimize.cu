@@ -151,19 +151,75 @@ static tsne_status relabel(const int32_t* perm, int N, const int64_t* rp, const 
   return TSNE_OK;
 }
 
-// Enter the internal label space: Morton order of the caller's Y.
+// ---------------------------------------------------------------- locality order
+// Before the embedding has any structure (t < kMortonFrom: Y is still the
+// 1e-4-scale random start, measured in profiles/README.md), its Morton order
+// puts a row's neighbours anywhere and the attractive pass gathers y_j at
+// random.  Instead the points are labelled by the Morton order of a graph
+// diffusion of random coordinates, u <- D^-1 P u (kDiffuseSteps steps): the
+// within-community differences decay geometrically while the communities of
+// the kNN graph keep distinct means, so rows of one community become
+// contiguous and their y_j fall inside the attractive pass's shared-memory
+// window.  Labels only reorder rows; the method's results do not depend on it.
+constexpr int kMortonFrom = 128;
+constexpr int kDiffuseSteps = 8;
+
+__global__ void __launch_bounds__(256)
+k_diffuse(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+          const float* __restrict__ val, const float2* __restrict__ u, int N,
+          float2* __restrict__ u2) {
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= N) return;
+  float sx = 0.f, sy = 0.f, sw = 0.f;
+  for (int64_t e = rp[i] + lane; e < rp[i + 1]; e += 32) {
+    const float p = __ldcs(val + e);
+    const float2 v = u[__ldcs(col + e)];
+    sx = fmaf(p, v.x, sx);
+    sy = fmaf(p, v.y, sy);
+    sw += p;
+  }
+  sx = warp_sum(sx);
+  sy = warp_sum(sy);
+  sw = warp_sum(sw);
+  if (lane == 0) u2[i] = (sw > 0.f) ? make_float2(sx / sw, sy / sw) : u[i];
+}
+
+static tsne_status diffusion_order(const int64_t* row_ptr, const int32_t* col, const float* val,
+                                   int64_t N, TreeWS& w, OptWS& o, cudaStream_t s) {
+  float2* u = o.tmp;
+  float2* u2 = o.tmp + N;
+  tsne_status st = launch_init_y(N, 0x6c6f63616c697479ull, u, s);
+  if (st != TSNE_OK) return st;
+  const int blocks = (int)((N * 32 + 255) / 256);
+  for (int k = 0; k < kDiffuseSteps; ++k) {
+    k_diffuse<<<blocks, 256, 0, s>>>(row_ptr, col, val, u, (int)N, u2);
+    TSNE_LAUNCH_CHECK();
+    float2* t = u; u = u2; u2 = t;
+  }
+  if ((st = launch_bbox(w, u, s)) != TSNE_OK) return st;
+  return build_tree(w, u, /*apply_shift=*/false, s);      // w.perm = the order
+}
+
+// Enter the internal label space: the diffusion order early in the run, the
+// Morton order of the caller's Y later (or the caller's order if !morton).
 static tsne_status enter(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t N,
                          float2* Y, float2* V, float2* G, int32_t t0, TreeWS& w, OptWS& o,
                          bool morton, cudaStream_t s) {
   k_set_state<<<1, 1, 0, s>>>(o.t_dev, t0, o.flag);
   TSNE_LAUNCH_CHECK();
-  tsne_status st = launch_bbox(w, Y, s);
-  if (st != TSNE_OK) return st;
+  tsne_status st;
   const int32_t* perm = nullptr;
   if (morton) {
-    if ((st = build_tree(w, Y, /*apply_shift=*/false, s)) != TSNE_OK) return st;
+    if (t0 < kMortonFrom) {
+      if ((st = diffusion_order(row_ptr, col, val, N, w, o, s)) != TSNE_OK) return st;
+    } else {
+      if ((st = launch_bbox(w, Y, s)) != TSNE_OK) return st;
+      if ((st = build_tree(w, Y, /*apply_shift=*/false, s)) != TSNE_OK) return st;
+    }
     perm = w.perm;
   }
+  if ((st = launch_bbox(w, Y, s)) != TSNE_OK) return st;      // root box of the caller's Y
   return relabel(perm, (int)N, row_ptr, col, val, Y, V, G, nullptr, 0, o, s);
 }
 
@@ -234,7 +290,7 @@ tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const flo
     }
     cur = (chunk % 2 == 0) ? o.Ya : o.Yb;
     done += chunk;
-    if (done < n_iter) {
+    if (done < n_iter && t0 + done >= kMortonFrom) {
       // chunks are even, so the state is in Ya; w.perm is the Morton order of
       // the last iteration's embedding (a permutation of the current labels).
       // The pending recentring shift is uniform, so it commutes with relabelling.

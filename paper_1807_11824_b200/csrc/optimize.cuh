@@ -35,7 +35,6 @@ struct OptWS {
 
 void carve_opt(Carver& c, OptWS& o, int64_t N, int64_t nnz);
 
-int attract_blocks(int64_t N);
 tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, const float* val,
                                 const float2* Y, int64_t N, const float2* rep, const double* Z,
                                 float alpha, float2* dY, cudaStream_t s);
