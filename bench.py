@@ -156,7 +156,7 @@ def run_e2e(T, Xh, cfg, N, args):
             "device_event_seconds": info["ms_total"] / 1e3, "n_iter": args.e2e_iters,
             "h2d_bytes_per_step": 4 * N * cfg.D, "d2h_bytes_per_step": 8 * N,
             "split_ms": {k: info[k] for k in ("ms_h2d", "ms_knn", "ms_p", "ms_loop", "ms_d2h")},
-            "knn_rows_uncertified": info["knn_rows_uncertified"], "nnz": info["nnz"]}
+            "knn_rows_uncertified": info["knn_rows_uncertified"], "nnz": info["nnz"], "_Y": Yh}
 
 
 def run_e2e_sharded(Xh_local, cfg, N, args, rank, world, dev):
@@ -250,6 +250,18 @@ def run_ours(args, rank, world):
     stages["p_ms"] = a.elapsed_time(b)
     nnz = int(col.numel())
     del idx, d2
+    quality = None
+    if e2e is not None and "_Y" in e2e:
+        # cost of the end-to-end embedding with the exact Z (tsne_kl),
+        # outside every timed region; P here is the e2e run's P (same X, deterministic)
+        Ye = e2e.pop("_Y").to(dev)
+        a.record()
+        kl, Z = T.kl(rp, col, val, Ye)
+        b.record()
+        torch.cuda.synchronize()
+        quality = {"kl_exact_z": kl, "Z": Z, "n_iter": args.e2e_iters, "kl_ms": a.elapsed_time(b),
+                   "api": "tsne_kl"}
+        del Ye
 
     opt = T.Optimizer(rp, col, val, T.init_y(N, 42, device=dev), theta=0.5,
                       relabel_every=args.relabel_every)
@@ -349,7 +361,10 @@ def run_ours(args, rank, world):
                                 "sample": f"{ns} full-size fp64 oracle iteration(s) at N={N} "
                                           f"(synthetic clustered Y, {round(nnz / N)} nnz/row)"}
     if e2e is not None:
+        e2e.pop("_Y", None)
         line["e2e"] = e2e
+    if quality is not None:
+        line["quality"] = quality
     if rank == 0:
         print(json.dumps(line), flush=True)
 

@@ -154,6 +154,27 @@ tsne_status tsne_gradient(const int64_t* row_ptr, const int32_t* col, const floa
                           float* dY, double* Z_out, void* ws, size_t ws_bytes,
                           tsne_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * f4  Cost of an embedding with the EXACT normaliser:
+ *   C = KL(P || Q) = sum_{P_ij > 0} P_ij ln(P_ij / q_ij),  q_ij = w_ij / Z,
+ *   w_ij = (1 + |y_i - y_j|^2)^-1,  Z = sum_{k != l} w_kl
+ * (Eq. 2 and the cost below it; Eq. 4).  Z is the exact
+ * O(N^2) sum (each unordered pair once, fp32 pair arithmetic with fp64
+ * accumulation in a fixed order: deterministic), not the Barnes-Hut
+ * estimate; the cost is then one fp64 pass over the CSR.  P is used as given
+ * (pass the non-exaggerated P of tsne_compute_p); zero entries contribute 0.
+ *
+ *   row_ptr/col/val  CSR of P (as for tsne_gradient; no alignment beyond the
+ *             element size is required here).
+ *   Y      [N x 2] float32, 8-byte aligned.
+ *   kl_out HOST out: C.   Z_out HOST out (nullable): Z.
+ * Synchronises `stream`.  Requires 2 <= N < 2^27.
+ * ------------------------------------------------------------------------ */
+size_t tsne_kl_workspace_size(int64_t N);
+tsne_status tsne_kl(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t N,
+                    const float* Y, double* kl_out, double* Z_out, void* ws, size_t ws_bytes,
+                    tsne_stream_t stream);
+
 /* Schedule / optimiser constants (the paper states none of them: D12-D16). */
 typedef struct {
   int32_t K;            /* neighbours; 0 -> min(N-1, floor(3 perplexity)) (D4) */
@@ -165,8 +186,10 @@ typedef struct {
   int32_t use_graphs;   /* 1: replay the iteration as a CUDA graph (default)    */
   int32_t relabel_every; /* period (iterations) of the internal relabelling of
                            points into the Morton order of the embedding, for
-                           gather locality; 0 = never (64).  Results differ
-                           only by floating-point summation order.              */
+                           gather locality (before iteration 128 the order of a
+                           graph diffusion of P is used instead); 0 = never
+                           (64).  Results differ only by floating-point
+                           summation order.                                     */
 } tsne_config;
 
 /* Fills the defaults listed above. */

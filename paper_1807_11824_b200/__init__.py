@@ -51,7 +51,8 @@ EXPORTS = ["tsne_last_error", "tsne_abi_version", "tsne_config_default",
            "tsne_compute_p", "tsne_gradient_workspace_size", "tsne_gradient",
            "tsne_optimize_workspace_size", "tsne_optimize", "tsne_init_y", "tsne_run",
            "tsne_run_ex", "tsne_profile_iterations", "tsne_shard_workspace_size",
-           "tsne_shard_forces", "tsne_shard_attract", "tsne_shard_update", "tsne_recentre"]
+           "tsne_shard_forces", "tsne_shard_attract", "tsne_shard_update", "tsne_recentre",
+           "tsne_kl_workspace_size", "tsne_kl"]
 
 
 def lib():
@@ -96,9 +97,13 @@ def lib():
     L.tsne_shard_update.argtypes = [vp, i64, i64, i64, vp, vp, vp, i32, i32, f32, f32,
                                     C.POINTER(Config), vp, vp, vp, vp, vp, sz, vp]
     L.tsne_recentre.argtypes = [vp, i64, vp, sz, vp]
+    L.tsne_kl_workspace_size.argtypes = [i64]
+    L.tsne_kl_workspace_size.restype = sz
+    L.tsne_kl.argtypes = [vp, vp, vp, i64, vp, C.POINTER(C.c_double), C.POINTER(C.c_double), vp,
+                          sz, vp]
     for name in ["tsne_knn", "tsne_knn_rows", "tsne_compute_p", "tsne_gradient", "tsne_optimize", "tsne_init_y",
                  "tsne_run", "tsne_run_ex", "tsne_profile_iterations", "tsne_shard_forces",
-                 "tsne_shard_attract", "tsne_shard_update", "tsne_recentre"]:
+                 "tsne_shard_attract", "tsne_shard_update", "tsne_recentre", "tsne_kl"]:
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -198,6 +203,22 @@ def gradient(row_ptr, col, val, Y: torch.Tensor, theta: float = 0.5, exaggeratio
                                float(exaggeration), _ptr(dY), C.byref(Z), _ptr(ws), ws.numel(),
                                _stream()), "tsne_gradient")
     return dY, Z.value
+
+
+# ---------------------------------------------------------------- f4
+def kl(row_ptr, col, val, Y: torch.Tensor):
+    """KL(P || Q) of the embedding Y with the exact normaliser Z (tsne_kl):
+    returns (KL, Z)."""
+    Y = _dev(Y, torch.float32, "Y")
+    row_ptr = _dev(row_ptr, torch.int64, "row_ptr")
+    col = _dev(col, torch.int32, "col")
+    val = _dev(val, torch.float32, "val")
+    N = Y.shape[0]
+    out, Z = C.c_double(), C.c_double()
+    ws = _ws(lib().tsne_kl_workspace_size(N), Y.device)
+    _check(lib().tsne_kl(_ptr(row_ptr), _ptr(col), _ptr(val), N, _ptr(Y), C.byref(out),
+                         C.byref(Z), _ptr(ws), ws.numel(), _stream()), "tsne_kl")
+    return out.value, Z.value
 
 
 # ---------------------------------------------------------------- H1-H8

@@ -14,6 +14,12 @@
 #include "shard.cuh"
 
 namespace tsne {
+size_t kl_workspace_size(int64_t N);
+tsne_status kl_run(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t N,
+                   const float2* Y, void* ws, double* kl_out, double* Z_out, cudaStream_t s);
+}  // namespace tsne
+
+namespace tsne {
 
 static thread_local char g_err[1024] = "";
 
@@ -101,7 +107,7 @@ extern "C" {
 
 const char* tsne_last_error(void) { return g_err; }
 
-int32_t tsne_abi_version(void) { return (1 << 16) | 0; }
+int32_t tsne_abi_version(void) { return (1 << 16) | 1; }
 
 void tsne_config_default(tsne_config* cfg) {
   if (!cfg) return;
@@ -159,6 +165,31 @@ tsne_status tsne_gradient(const int64_t* row_ptr, const int32_t* col, const floa
     *Z_out = z[0];
   }
   return TSNE_OK;
+}
+
+// ---------------------------------------------------------------- f4 KL
+size_t tsne_kl_workspace_size(int64_t N) {
+  if (N < 2) return 0;
+  return kl_workspace_size(N);
+}
+
+tsne_status tsne_kl(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t N,
+                    const float* Y, double* kl_out, double* Z_out, void* ws, size_t ws_bytes,
+                    tsne_stream_t stream) {
+  clear_error();
+  TSNE_ARG_CHECK(N >= 2 && N < (int64_t(1) << 27), "N must be in [2, 2^27) (got %lld)",
+                 (long long)N);
+  TSNE_ARG_CHECK(row_ptr && col && val && Y && kl_out, "null pointer argument");
+  TSNE_ARG_CHECK(aligned(Y, 8), "Y needs 8-byte alignment");
+  const size_t need = kl_workspace_size(N);
+  if (!ws || ws_bytes < need) {
+    set_error("workspace too small: need %zu bytes, got %zu", need, ws_bytes);
+    return TSNE_ERR_WORKSPACE;
+  }
+  tsne_status st = check_device();
+  if (st != TSNE_OK) return st;
+  return kl_run(row_ptr, col, val, N, reinterpret_cast<const float2*>(Y), ws, kl_out, Z_out,
+                (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------- optimise

@@ -52,6 +52,7 @@ def test_workspace_sizes_monotone(L):
     assert L.tsne_knn_workspace_size(5000, 784, 90) > 5000 * 784 * 2
     assert L.tsne_compute_p_workspace_size(5000, 90) > 2 * 5000 * 90 * 16
     assert L.tsne_optimize_workspace_size(5000, 700000) > L.tsne_gradient_workspace_size(5000)
+    assert 0 < L.tsne_kl_workspace_size(1000) < L.tsne_kl_workspace_size(1281167)
 
 
 def test_argument_validation_without_device(L):
@@ -66,6 +67,9 @@ def test_argument_validation_without_device(L):
     assert L.tsne_compute_p(v, v, 100, 30, 40.0, v, v, v, C.byref(n), None, v, 1 << 30, None) == 1
     assert b"perplexity" in L.tsne_last_error()
     assert L.tsne_run(v, 100, 5, 30.0, -0.5, 200.0, 10, 12.0, v) == 1
+    d = C.c_double()
+    assert L.tsne_kl(v, v, v, 1, v, C.byref(d), None, v, 1 << 30, None) == 1
+    assert L.tsne_kl(v, v, v, 100, v, None, None, v, 1 << 30, None) == 1
 
 
 def test_workspace_too_small(L):
