@@ -262,10 +262,12 @@ int64_t oracle_symmetrize(const int32_t* idx, const double* P_cond, int64_t N, i
  *
  * O4 root box (D8): exact min/max per axis; centre c = (min+max)/2;
  *    r0 = max(span_x, span_y)/2 * (1 + 2^-20), or 1 if both spans are 0;
- *    lo = c - r0; s = 2^16 / (2 r0).  All fp64.
- * O5 cells (D7-D9): q = min(2^16-1, max(0, floor((y - lo) s))) per axis.
- *    A cell at level l holds the points sharing q >> (16-l) on both axes;
- *    it is a leaf iff it holds exactly one point or l = 16.
+ *    lo = c - r0; s = 2^L / (2 r0) with L = OTREE_LEVELS = 24.  All fp64.
+ * O5 cells (D7-D9): q = min(2^L-1, max(0, floor((y - lo) s))) per axis.
+ *    A cell at level l holds the points sharing q >> (L-l) on both axes;
+ *    it is a leaf iff it holds exactly one point or l = L (D9: the paper
+ *    inserts until every leaf holds one body; L = 24 stops only
+ *    points closer than ~2^-23 r0, about one fp32 ulp of the coordinates).
  *    Summary: N_c, centre of mass = mean (fp64), radius r_l = r0 2^-l
  *    (half the side of the square cell).
  * O6 traversal for point i (D10, D11): DFS from the root, children in
@@ -275,12 +277,14 @@ int64_t oracle_symmetrize(const int32_t* idx, const double* P_cond, int64_t N, i
  *    w = 1/(1 + D^2)  (P:L132 cell formula, P:L134 simultaneous Z);
  *    else open.
  * ====================================================================== */
+#define OTREE_LEVELS 24
+
 typedef struct {
   int32_t level;
   int32_t leaf;
   int64_t count;
   double comx, comy;
-  uint32_t px, py;        /* cell prefix: q >> (16 - level) */
+  uint32_t px, py;        /* cell prefix: q >> (L - level) */
   int64_t child[4];       /* node ids, -1 if empty */
   int64_t first;          /* leaf: offset of its members in `members` */
 } onode_t;
@@ -314,10 +318,10 @@ static int64_t otree_build_cell(otree_t* T, const double* Y, int64_t* list, int6
   for (int64_t a = 0; a < n; ++a) { sx += Y[2 * list[a]]; sy += Y[2 * list[a] + 1]; }
   c->comx = sx / (double)n;
   c->comy = sy / (double)n;
-  c->px = T->qx[list[0]] >> (16 - level);
-  c->py = T->qy[list[0]] >> (16 - level);
+  c->px = T->qx[list[0]] >> (OTREE_LEVELS - level);
+  c->py = T->qy[list[0]] >> (OTREE_LEVELS - level);
   for (int k = 0; k < 4; ++k) c->child[k] = -1;
-  if (n == 1 || level == 16) {
+  if (n == 1 || level == OTREE_LEVELS) {
     c->leaf = 1;
     c->first = T->nmembers;
     for (int64_t a = 0; a < n; ++a) T->members[T->nmembers++] = list[a];
@@ -327,7 +331,7 @@ static int64_t otree_build_cell(otree_t* T, const double* Y, int64_t* list, int6
   c->first = -1;
   /* stable partition of the list into the 4 quadrants of level+1 */
   int64_t cnt[4] = {0, 0, 0, 0};
-  int shift = 15 - level;
+  int shift = OTREE_LEVELS - 1 - level;
   for (int64_t a = 0; a < n; ++a) {
     int q = (int)(((T->qx[list[a]] >> shift) & 1u) * 2u + ((T->qy[list[a]] >> shift) & 1u));
     cnt[q]++;
@@ -366,7 +370,7 @@ static int otree_build(otree_t* T, const double* Y, int64_t N) {
   double span = (maxx - minx) > (maxy - miny) ? (maxx - minx) : (maxy - miny);
   double r0 = (span == 0.0) ? 1.0 : (span / 2.0) * (1.0 + ldexp(1.0, -20));
   double lox = cx - r0, loy = cy - r0;
-  double s = 65536.0 / (2.0 * r0);
+  double s = ldexp(1.0, OTREE_LEVELS) / (2.0 * r0);
   T->r0 = r0; T->cx = cx; T->cy = cy;
   T->qx = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)N);
   T->qy = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)N);
@@ -381,8 +385,8 @@ static int otree_build(otree_t* T, const double* Y, int64_t N) {
     double fy = floor((Y[2 * i + 1] - loy) * s);
     if (fx < 0.0) fx = 0.0;
     if (fy < 0.0) fy = 0.0;
-    if (fx > 65535.0) fx = 65535.0;
-    if (fy > 65535.0) fy = 65535.0;
+    if (fx > ldexp(1.0, OTREE_LEVELS) - 1.0) fx = ldexp(1.0, OTREE_LEVELS) - 1.0;
+    if (fy > ldexp(1.0, OTREE_LEVELS) - 1.0) fy = ldexp(1.0, OTREE_LEVELS) - 1.0;
     T->qx[i] = (uint32_t)fx;
     T->qy[i] = (uint32_t)fy;
     list[i] = i;
@@ -393,7 +397,8 @@ static int otree_build(otree_t* T, const double* Y, int64_t N) {
 }
 
 static int otree_contains(const otree_t* T, const onode_t* c, int64_t i) {
-  return (T->qx[i] >> (16 - c->level)) == c->px && (T->qy[i] >> (16 - c->level)) == c->py;
+  return (T->qx[i] >> (OTREE_LEVELS - c->level)) == c->px &&
+         (T->qy[i] >> (OTREE_LEVELS - c->level)) == c->py;
 }
 
 typedef struct { double fx, fy, z; int64_t visits, interactions; } oacc_t;

@@ -25,8 +25,9 @@ namespace tsne {
 constexpr int kTravThreads = 256;
 
 // diagnostics (TSNE_TRAV_STATS=1): [0] sum of node visits, [1] sum over warps
-// of the warp's max visits, [2] accepted cells + exact pairs, [3] fp64 re-tests
-__device__ unsigned long long g_trav_stats[4];
+// of the warp's max visits, [2] accepted cells + exact pairs, [3] fp64 re-tests,
+// [4] bucket pairs (coincident-point cells evaluated pairwise)
+__device__ unsigned long long g_trav_stats[5];
 
 static int trav_stats_on() { return getenv("TSNE_TRAV_STATS") ? 1 : 0; }
 
@@ -48,6 +49,105 @@ __device__ __noinline__ bool accept_fp64(const double2* __restrict__ c64, float2
   return r2 < __dmul_rn(theta2d, D2d);
 }
 
+// Exact pairs inside each point's own bucket (a level-16 cell holding several
+// points, D9): every member opens its bucket (D11) and takes all pairs with
+// the other members.  Done here, before the traversal, warp-synchronously:
+// the lanes of a warp that share a bucket walk its members together (one
+// broadcast load per member, 32 useful pairs per step), and 64-thread blocks
+// spread a large bucket's members over many SMs.  (Inside the traversal each
+// lane would reach its bucket at a different step and the warp would run the
+// member loop once per lane group: measured 12-21 ms per traversal at
+// C2/C3 early in the run, where a few thousand points share a cell.)
+// Output per sorted position: the pair sums (f, z), added by k_traverse.
+struct BucketSum {
+  float2 f;
+  double z;
+};
+static_assert(sizeof(BucketSum) == sizeof(longlong2), "reuses the fixed-point scratch");
+constexpr int kBucketThreads = 64;
+
+__global__ void __launch_bounds__(kBucketThreads)
+k_bucket_pairs(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
+               const float2* __restrict__ ys, const int32_t* __restrict__ leafnode, int N,
+               const int32_t* __restrict__ list, const int32_t* __restrict__ nlist,
+               BucketSum* __restrict__ out) {
+  const int tid = blockIdx.x * kBucketThreads + threadIdx.x;
+  const bool active = tid < (list ? *nlist : N);
+  const int k = active ? (list ? list[tid] : tid) : -1;
+  int s0 = -1, cnt = 0;
+  float2 yi = make_float2(0.f, 0.f);
+  if (active) {
+    const int L = leafnode[k];
+    const int c = (int)__ldg(&nodes[L].z);
+    if (c > 1) {
+      s0 = nfirst[L];
+      cnt = c;
+    }
+    yi = ys[k];
+  }
+  float fx = 0.f, fy = 0.f;
+  double z = 0.0;
+  unsigned todo = __ballot_sync(0xffffffffu, s0 >= 0);
+  while (todo) {                                   // one shared bucket at a time
+    const int ld = __ffs(todo) - 1;
+    const int sb = __shfl_sync(0xffffffffu, s0, ld);
+    const int cb = __shfl_sync(0xffffffffu, cnt, ld);
+    const bool mine = (s0 == sb);
+    todo &= ~__ballot_sync(0xffffffffu, mine);
+    int m = sb;
+    const int me = sb + cb;
+    for (; m + 4 <= me; m += 4) {
+      float zs = 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 yj = ys[m + u];
+        const float ex = yi.x - yj.x, ey = yi.y - yj.y;
+        const float wj = (mine && m + u != k) ? rcp_approx(1.f + ex * ex + ey * ey) : 0.f;
+        zs += wj;
+        const float ww = wj * wj;
+        fx = fmaf(ww, ex, fx);
+        fy = fmaf(ww, ey, fy);
+      }
+      z += (double)zs;
+    }
+    for (; m < me; ++m) {
+      const float2 yj = ys[m];
+      const float ex = yi.x - yj.x, ey = yi.y - yj.y;
+      const float wj = (mine && m != k) ? rcp_approx(1.f + ex * ex + ey * ey) : 0.f;
+      z += (double)wj;
+      const float ww = wj * wj;
+      fx = fmaf(ww, ex, fx);
+      fy = fmaf(ww, ey, fy);
+    }
+  }
+  if (active) {
+    BucketSum b;
+    b.f = make_float2(fx, fy);
+    b.z = z;
+    out[k] = b;
+  }
+}
+
+constexpr int kPend = 4;   // deferred buckets per lane
+constexpr int kDeepFp32 = 16;   // deeper cells: fp64 criterion and offsets
+
+
+// exact pairs of point k (y_i) with the members [s0, s0 + cnt) of a bucket;
+// lanes with take == false run the loop (warp-uniform trip count) adding 0
+__device__ __forceinline__ void bucket_pairs(const float2* __restrict__ ys, int s0, int cnt, int k,
+                                             float2 yi, bool take, float& fx, float& fy,
+                                             double& z) {
+  for (int m = s0; m < s0 + cnt; ++m) {
+    const float2 yj = ys[m];
+    const float ex = yi.x - yj.x, ey = yi.y - yj.y;
+    const float wj = (take && m != k) ? rcp_approx(1.f + ex * ex + ey * ey) : 0.f;
+    z += (double)wj;
+    const float ww = wj * wj;
+    fx = fmaf(ww, ex, fx);
+    fy = fmaf(ww, ey, fy);
+  }
+}
+
 __global__ void __launch_bounds__(kTravThreads, 4)
 k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            const double2* __restrict__ com64, const float2* __restrict__ ys,
@@ -56,19 +156,19 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            float theta, float2* __restrict__ rep, double* __restrict__ zpart,
            unsigned* __restrict__ counter, double* __restrict__ Zout,
            const int32_t* __restrict__ list, const int32_t* __restrict__ nlist, int row0,
-           int stats) {
+           const BucketSum* __restrict__ bsum, int stats) {
   // list (multi-GPU): the sorted positions of the points this rank owns
   // (original indices [row0, ...)); rep is then indexed by perm[k] - row0.
   // per level l: {r^2 (fp32), margin constant A_l, margin slope B_l}, r^2 (fp64)
-  __shared__ float4 s_lv[18];
-  __shared__ double s_r2d[18];
+  __shared__ float4 s_lv[kLevels + 2];
+  __shared__ double s_r2d[kLevels + 2];
   __shared__ double s_z[kTravThreads / 32];
   __shared__ int s_done;
   const float theta2 = theta * theta;
   const double theta2d = (double)theta * (double)theta;
-  if (threadIdx.x < 18) {
+  if (threadIdx.x < kLevels + 2) {
     const int l = threadIdx.x;
-    const int le = (l == kLevelBucketTest) ? 15 : (l > 16 ? 16 : l);
+    const int le = (l == kLevelBucketTest) ? kLevels - 1 : (l > kLevels ? kLevels : l);
     const double r = ldexp(box->r0, -le);
     const double r2 = r * r;
     const double M = (double)box->mabs, th = (double)theta;
@@ -93,8 +193,12 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   float fx = 0.f, fy = 0.f;
   double z = 0.0;   // fp64: Z sums up to N^2 terms of very different size
 
+  int pq_s[kPend], pq_c[kPend];   // deferred buckets of this lane
+#pragma unroll
+  for (int q = 0; q < kPend; ++q) { pq_s[q] = -1; pq_c[q] = 0; }
+  int npend = 0;
   const uint32_t lv_base = (uint32_t)__cvta_generic_to_shared(s_lv);
-  unsigned n_visit = 0, n_take = 0, n_f64 = 0;
+  unsigned n_visit = 0, n_take = 0, n_f64 = 0, n_pair = 0;
   while (cur < nnodes) {
     if (stats) ++n_visit;
     const float4 nd = __ldg(nodes + cur);
@@ -114,7 +218,20 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
     const float diff = lhs - lv.x;
     const float marg = fmaf(lv.z, lhs, lv.y);
     bool acc = diff > marg;
-    if (!leaf && !self_in && fabsf(diff) <= marg) {   // inside the band: decide in fp64
+    // cells below level kDeepFp32 are decided, and their offset y_i - com
+    // taken, in fp64: their size approaches the fp32 spacing of the coordinates
+    const bool deep = !leaf && lvl > kDeepFp32;
+    float ddx = dx, ddy = dy, dd2 = D2;
+    if (deep && !self_in) {
+      const double2 c = com64[cur];
+      const double ex = __dsub_rn((double)yi.x, c.x), ey = __dsub_rn((double)yi.y, c.y);
+      const double D2d = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
+      acc = s_r2d[lvl] < __dmul_rn(theta2d, D2d);
+      ddx = (float)ex;
+      ddy = (float)ey;
+      dd2 = __fadd_rn(__fmul_rn(ddx, ddx), __fmul_rn(ddy, ddy));
+      if (stats) ++n_f64;
+    } else if (!leaf && !self_in && fabsf(diff) <= marg) {   // inside the band: decide in fp64
       acc = accept_fp64(com64 + cur, yi, s_r2d[lvl], theta2d);
       if (stats) ++n_f64;
     }
@@ -124,36 +241,74 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
     const bool bucket = !take && (leaf ? cntf > 1.f : lvl == kLevelBucketTest);
     const int node = cur;
     cur = (take || leaf || bucket) ? skip : cur + 1;
-    const float w = rcp_approx(1.f + D2);
+    const float w = rcp_approx(1.f + dd2);
     const float nw = take ? cntf * w : 0.f;
     if (stats && take) ++n_take;
     z += (double)nw;
     const float nww = nw * w;
-    fx = fmaf(nww, dx, fx);
-    fy = fmaf(nww, dy, fy);
-    if (bucket) {                                  // coincident points: exact pairs
+    fx = fmaf(nww, ddx, fx);
+    fy = fmaf(nww, ddy, fy);
+    if (bucket && !self_in) {   // another bucket, not accepted: exact pairs (own bucket: k_bucket_pairs)
       const int s0 = nfirst[node];
       const int cnt = (int)cntf;
-      for (int m = s0; m < s0 + cnt; ++m) {
-        if (m == k) continue;
-        const float2 yj = ys[m];
-        const float ex = yi.x - yj.x, ey = yi.y - yj.y;
-        const float wj = rcp_approx(1.f + ex * ex + ey * ey);
-        z += (double)wj;
-        const float ww = wj * wj;
-        fx = fmaf(ww, ex, fx);
-        fy = fmaf(ww, ey, fy);
+      if (stats) n_pair += (unsigned)cnt;
+      if (npend < kPend) {      // deferred: processed warp-synchronously after the walk
+#pragma unroll
+        for (int q = 0; q < kPend; ++q)
+          if (q == npend) { pq_s[q] = s0; pq_c[q] = cnt; }
+        ++npend;
+      } else {
+        bucket_pairs(ys, s0, cnt, k, yi, true, fx, fy, z);
       }
     }
   }
-  if (active) rep[perm[k] - row0] = make_float2(fx, fy);
+  // Deferred buckets: lanes of the warp that share a bucket walk its members
+  // together (a lane reaches a bucket at its own step of the walk, so doing it
+  // in place would run the member loop once per lane group).
+  while (true) {
+    const unsigned ball = __ballot_sync(0xffffffffu, npend > 0);
+    if (!ball) break;
+    const int ld = __ffs(ball) - 1;
+    const int sb = __shfl_sync(0xffffffffu, pq_s[0], ld);
+    const int cb = __shfl_sync(0xffffffffu, pq_c[0], ld);
+    bool mine = false;
+#pragma unroll
+    for (int q = 0; q < kPend; ++q) mine |= (q < npend) && (pq_s[q] == sb);
+    bucket_pairs(ys, sb, cb, k, yi, mine, fx, fy, z);
+    if (mine) {                 // drop sb from this lane's list (order kept)
+      int ns = 0;
+      int ts[kPend], tc[kPend];
+#pragma unroll
+      for (int q = 0; q < kPend; ++q) { ts[q] = 0; tc[q] = 0; }
+#pragma unroll
+      for (int q = 0; q < kPend; ++q) {
+        if (q < npend && pq_s[q] != sb) {
+#pragma unroll
+          for (int r = 0; r < kPend; ++r)
+            if (r == ns) { ts[r] = pq_s[q]; tc[r] = pq_c[q]; }
+          ++ns;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kPend; ++q) { pq_s[q] = ts[q]; pq_c[q] = tc[q]; }
+      npend = ns;
+    }
+  }
+  if (active) {
+    const BucketSum b = bsum[k];
+    fx += b.f.x;
+    fy += b.f.y;
+    z += b.z;
+    rep[perm[k] - row0] = make_float2(fx, fy);
+  }
   if (stats) {
-    unsigned long long sv = n_visit, st = n_take, sf = n_f64;
+    unsigned long long sv = n_visit, st = n_take, sf = n_f64, sp = n_pair;
     unsigned mv = n_visit;
     for (int o = 16; o > 0; o >>= 1) {
       sv += __shfl_xor_sync(0xffffffffu, sv, o);
       st += __shfl_xor_sync(0xffffffffu, st, o);
       sf += __shfl_xor_sync(0xffffffffu, sf, o);
+      sp += __shfl_xor_sync(0xffffffffu, sp, o);
       mv = max(mv, __shfl_xor_sync(0xffffffffu, mv, o));
     }
     if ((threadIdx.x & 31) == 0) {
@@ -161,6 +316,7 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
       atomicAdd(&g_trav_stats[1], (unsigned long long)mv * 32ull);
       atomicAdd(&g_trav_stats[2], st);
       atomicAdd(&g_trav_stats[3], sf);
+      atomicAdd(&g_trav_stats[4], sp);
     }
   }
 
@@ -197,19 +353,32 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   }
 }
 
+static tsne_status launch_bucket_pairs(TreeWS& w, const int32_t* list, const int32_t* nlist,
+                                       cudaStream_t s) {
+  const int N = (int)w.N;
+  // the fixed-point coordinates are dead after the tree build: reuse them
+  k_bucket_pairs<<<(N + kBucketThreads - 1) / kBucketThreads, kBucketThreads, 0, s>>>(
+      w.nodes, w.nfirst, w.ys, w.leafnode, N, list, nlist, reinterpret_cast<BucketSum*>(w.fq));
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
 tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s) {
   const int N = (int)w.N;
+  tsne_status st = launch_bucket_pairs(w, nullptr, nullptr, s);
+  if (st != TSNE_OK) return st;
   k_traverse<<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
-      w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0, trav_stats_on());
+      w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0,
+      reinterpret_cast<const BucketSum*>(w.fq), trav_stats_on());
   TSNE_LAUNCH_CHECK();
   if (trav_stats_on()) {
-    unsigned long long h[4];
+    unsigned long long h[5];
     TSNE_CUDA_TRY(cudaMemcpyFromSymbolAsync(h, g_trav_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, s));
     TSNE_CUDA_TRY(cudaStreamSynchronize(s));
-    fprintf(stderr, "traverse stats: visits/pt %.1f  warp-max visits/pt %.1f  interactions/pt %.1f  fp64/pt %.3f\n",
-            h[0] / (double)N, h[1] / (double)N, h[2] / (double)N, h[3] / (double)N);
-    const unsigned long long zero[4] = {0, 0, 0, 0};
+    fprintf(stderr, "traverse stats: visits/pt %.1f  warp-max visits/pt %.1f  interactions/pt %.1f  fp64/pt %.3f  bucket pairs/pt %.1f\n",
+            h[0] / (double)N, h[1] / (double)N, h[2] / (double)N, h[3] / (double)N, h[4] / (double)N);
+    const unsigned long long zero[5] = {0, 0, 0, 0, 0};
     TSNE_CUDA_TRY(cudaMemcpyToSymbolAsync(g_trav_stats, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s));
   }
   return TSNE_OK;
@@ -219,9 +388,12 @@ tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s) {
 tsne_status launch_traverse_list(TreeWS& w, float theta, const int32_t* list, const int32_t* nlist,
                                  int row0, float2* rep_local, double* z_partial, cudaStream_t s) {
   const int N = (int)w.N;
+  tsne_status st = launch_bucket_pairs(w, list, nlist, s);
+  if (st != TSNE_OK) return st;
   k_traverse<<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta,
-      rep_local, w.zpart, w.counter + 1, z_partial, list, nlist, row0, 0);
+      rep_local, w.zpart, w.counter + 1, z_partial, list, nlist, row0,
+      reinterpret_cast<const BucketSum*>(w.fq), 0);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }

@@ -34,9 +34,9 @@ struct LL2Sum {
 
 size_t tree_cub_bytes(int64_t N, size_t* sort_b, size_t* scan_b, size_t* scan2_b) {
   size_t a = 0, b = 0, c = 0;
-  cub::DoubleBuffer<uint32_t> dk(nullptr, nullptr);
+  cub::DoubleBuffer<uint64_t> dk(nullptr, nullptr);
   cub::DoubleBuffer<int32_t> dv(nullptr, nullptr);
-  cub::DeviceRadixSort::SortPairs(nullptr, a, dk, dv, (int)N, 0, 32);
+  cub::DeviceRadixSort::SortPairs(nullptr, a, dk, dv, (int)N, 0, kKeyBits);
   cub::DeviceScan::ExclusiveSum(nullptr, c, (int32_t*)nullptr, (int32_t*)nullptr, (int)(N + 1));
   if (sort_b) *sort_b = a;
   if (scan_b) *scan_b = b;
@@ -48,8 +48,8 @@ void carve_tree(Carver& c, TreeWS& w, int64_t N) {
   w.N = N;
   size_t sb, cb, c2b;
   tree_cub_bytes(N, &sb, &cb, &c2b);
-  w.keys_a = c.take<uint32_t>(N);
-  w.keys_b = c.take<uint32_t>(N);
+  w.keys_a = c.take<uint64_t>(N);
+  w.keys_b = c.take<uint64_t>(N);
   w.vals_a = c.take<int32_t>(N);
   w.vals_b = c.take<int32_t>(N);
   w.sort_tmp = c.take<char>(sb);
@@ -207,26 +207,29 @@ tsne_status launch_bbox_mean(TreeWS& w, const float2* Y, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- H2 keys
-__device__ __forceinline__ uint32_t spread16(uint32_t x) {
-  x = (x | (x << 8)) & 0x00FF00FFu;
-  x = (x | (x << 4)) & 0x0F0F0F0Fu;
-  x = (x | (x << 2)) & 0x33333333u;
-  x = (x | (x << 1)) & 0x55555555u;
+// spread the kLevels bits of x to the even bit positions of a 64-bit word
+__device__ __forceinline__ uint64_t spread_bits(uint32_t x32) {
+  uint64_t x = x32;
+  x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x << 2)) & 0x3333333333333333ull;
+  x = (x | (x << 1)) & 0x5555555555555555ull;
   return x;
 }
 
-// q = min(2^16-1, max(0, floor((y - lo) * s))) in fp64 without contraction (D8)
+// q = min(2^L-1, max(0, floor((y - lo) * s))) in fp64 without contraction (D8, D9)
 __device__ __forceinline__ uint32_t quantise(float y, double lo, double s) {
   double f = floor(__dmul_rn(__dsub_rn((double)y, lo), s));
   f = f < 0.0 ? 0.0 : f;
-  f = f > 65535.0 ? 65535.0 : f;
+  f = f > (double)((1u << kLevels) - 1u) ? (double)((1u << kLevels) - 1u) : f;
   return (uint32_t)f;
 }
 
 // Y is read-only: the pending recentring shift (D15) is applied on the fly,
 // so the attractive pass may read Y concurrently.
 __global__ void k_keys(const float2* __restrict__ Y, int N, const BoxInfo* __restrict__ box,
-                       int apply_shift, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                       int apply_shift, uint64_t* __restrict__ keys, int32_t* __restrict__ vals,
                        int32_t* __restrict__ cnt) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i > N) return;
@@ -240,7 +243,7 @@ __global__ void k_keys(const float2* __restrict__ Y, int N, const BoxInfo* __res
   }
   uint32_t qx = quantise(y.x, b.lox, b.s);
   uint32_t qy = quantise(y.y, b.loy, b.s);
-  keys[i] = (spread16(qx) << 1) | spread16(qy);   // quadrant digit = 2 bx + by
+  keys[i] = (spread_bits(qx) << 1) | spread_bits(qy);   // quadrant digit = 2 bx + by
   vals[i] = i;
 }
 
@@ -325,15 +328,17 @@ __global__ void __launch_bounds__(1024) k_bscan(longlong2* __restrict__ bsum, in
 }
 
 // ---------------------------------------------------------------- H3 Karras
-__device__ __forceinline__ int kdelta(const uint32_t* __restrict__ k, int N, int a, int b) {
+// common-prefix length of sorted keys a, b within the kKeyBits-bit keys;
+// equal keys are told apart by their index (kKeyBits + prefix of a ^ b)
+__device__ __forceinline__ int kdelta(const uint64_t* __restrict__ k, int N, int a, int b) {
   if (b < 0 || b >= N) return -1;
-  uint32_t ka = k[a], kb = k[b];
-  if (ka != kb) return __clz(ka ^ kb);
-  return 32 + __clz((uint32_t)a ^ (uint32_t)b);
+  uint64_t ka = k[a], kb = k[b];
+  if (ka != kb) return __clzll(ka ^ kb) - (64 - kKeyBits);
+  return kKeyBits + __clz((uint32_t)a ^ (uint32_t)b);
 }
 
 __global__ void __launch_bounds__(kScanBlock)
-k_karras(const uint32_t* __restrict__ keys, int N, int32_t* __restrict__ bfirst,
+k_karras(const uint64_t* __restrict__ keys, int N, int32_t* __restrict__ bfirst,
          int32_t* __restrict__ blast, int32_t* __restrict__ bdelta, int32_t* __restrict__ bparent,
          int32_t* __restrict__ lparent, const longlong2* __restrict__ fq,
          const longlong2* __restrict__ boff, longlong2* __restrict__ S) {
@@ -381,7 +386,9 @@ k_karras(const uint32_t* __restrict__ keys, int N, int32_t* __restrict__ bfirst,
   if (i == 0) bparent[0] = -1;
 }
 
-__device__ __forceinline__ int qlevel(int delta) { return (delta < 32 ? delta : 32) >> 1; }
+__device__ __forceinline__ int qlevel(int delta) {
+  return (delta < kKeyBits ? delta : kKeyBits) >> 1;
+}
 
 // binary node ids: [0, N-1) internal, [N-1, 2N-1) leaves (sorted position id-(N-1))
 __device__ __forceinline__ bool internal_is_quad(const int32_t* bdelta, const int32_t* bparent,
@@ -402,12 +409,12 @@ __global__ void k_quad_rank(int N, const int32_t* __restrict__ bfirst,
     s = bfirst[id];
     p = bparent[id];
     quad = internal_is_quad(bdelta, bparent, id);
-    deepest = bdelta[id] >= 32;                       // bucket top
+    deepest = bdelta[id] >= kKeyBits;                 // bucket top
   } else {
     int k = id - (N - 1);
     s = k;
     p = lparent[k];
-    quad = qlevel(bdelta[p]) < 16;                    // not inside a bucket
+    quad = qlevel(bdelta[p]) < kLevels;               // not inside a bucket
     deepest = true;
   }
   if (!quad) { rank[id] = -1; return; }
@@ -434,11 +441,11 @@ __global__ void k_quad_emit(int N, const int32_t* __restrict__ bfirst,
     s = bfirst[id];
     e = blast[id];
     int dl = bdelta[id];
-    if (dl < 32) {
+    if (dl < kKeyBits) {
       level = qlevel(dl);
     } else {                                          // bucket top
       int p = bparent[id];
-      level = (p < 0 || bdelta[p] <= 29) ? kLevelBucketTest : kLevelLeaf;
+      level = (p < 0 || bdelta[p] <= kKeyBits - 3) ? kLevelBucketTest : kLevelLeaf;
     }
   } else {
     s = e = id - (N - 1);
@@ -478,10 +485,10 @@ tsne_status build_tree(TreeWS& w, const float2* Y, bool apply_shift, cudaStream_
   const int T = 256;
   k_keys<<<cdiv(N + 1, T), T, 0, s>>>(Y, N, w.box, apply_shift ? 1 : 0, w.keys_a, w.vals_a, w.cnt);
   TSNE_LAUNCH_CHECK();
-  cub::DoubleBuffer<uint32_t> dk(w.keys_a, w.keys_b);
+  cub::DoubleBuffer<uint64_t> dk(w.keys_a, w.keys_b);
   cub::DoubleBuffer<int32_t> dv(w.vals_a, w.vals_b);
   size_t sb = w.sort_tmp_bytes;
-  TSNE_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, sb, dk, dv, N, 0, 32, s));
+  TSNE_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.sort_tmp, sb, dk, dv, N, 0, kKeyBits, s));
   w.keys_sorted = dk.Current();
   w.perm = dv.Current();
   const int nb = cdiv(N + 1, kScanBlock);

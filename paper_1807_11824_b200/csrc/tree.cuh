@@ -10,12 +10,12 @@
 // bucket leaves) and the fp64 centre of mass (`com64`, read only inside the
 // fp64 decision band, D25).
 //
-// level field: 0..15  internal cell whose point set branches at that level
+// level field: 0..23  internal cell whose point set branches at that level
 //                     (single-child chains are compressed away, D9)
-//              16     leaf evaluated exactly (one point, or a level-16 bucket
-//                     directly below a level-15 branching cell)
-//              17     bucket whose chain reaches level <= 15: the criterion
-//                     is tested with r_15; accept -> summary, else exact pairs
+//              24     leaf evaluated exactly (one point, or a level-24 bucket
+//                     directly below a level-23 branching cell)
+//              25     bucket whose chain reaches level <= 23: the criterion
+//                     is tested with r_23; accept -> summary, else exact pairs
 #pragma once
 #include "common.cuh"
 
@@ -29,15 +29,18 @@ struct BoxInfo {
   double cx, cy, r0, lox, loy, s;  // root box (D8), fp64
 };
 
-constexpr int kLevelLeaf = 16;
-constexpr int kLevelBucketTest = 17;
+constexpr int kLevels = 24;                   // quadtree depth (D9): 2^24 cells per axis
+constexpr int kKeyBits = 2 * kLevels;          // Morton key bits (48, in a 64-bit word)
+constexpr int kLevelLeaf = kLevels;            // 24
+constexpr int kLevelBucketTest = kLevels + 1;  // 25 (level field is 5 bits)
+static_assert(kLevelBucketTest < 32, "level field");
 constexpr uint32_t kSkipMask = (1u << 27) - 1u;
 constexpr int kMaxParts = 4096;
 constexpr double kFixScale = 274877906944.0;  // 2^38: fixed-point COM sums
 
 struct TreeWS {
   int64_t N = 0;
-  uint32_t *keys_a = nullptr, *keys_b = nullptr;
+  uint64_t *keys_a = nullptr, *keys_b = nullptr;
   int32_t *vals_a = nullptr, *vals_b = nullptr;
   void* sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
@@ -64,7 +67,7 @@ struct TreeWS {
   float4* part4 = nullptr;     // per-block min/max partials (kMaxParts)
   double2* part2 = nullptr;    // per-block fp64 sum partials (kMaxParts)
   // set by build(): which double-buffer half holds the sorted result
-  uint32_t* keys_sorted = nullptr;
+  uint64_t* keys_sorted = nullptr;
   int32_t* perm = nullptr;
 };
 
@@ -134,7 +137,7 @@ __host__ __device__ inline void make_root_box(float minx, float maxx, float miny
   b->cx = cx; b->cy = cy; b->r0 = r0;
   b->lox = dsub(cx, r0);
   b->loy = dsub(cy, r0);
-  b->s = ddiv(65536.0, dmul(2.0, r0));
+  b->s = ddiv(16777216.0 /* 2^kLevels */, dmul(2.0, r0));
   float m = fmaxf(fmaxf(fabsf(minx), fabsf(maxx)), fmaxf(fabsf(miny), fabsf(maxy)));
   b->mabs = m;
 }

@@ -78,7 +78,7 @@ def test_tree_counts_and_com(orc):
     n = len(lvl)
     for k in range(0, n, 7):
         if leaf[k]:
-            assert cnt[k] == 1 or lvl[k] == 16
+            assert cnt[k] == 1 or lvl[k] == 24
             continue
         s, m = 0, k + 1
         while m < n and lvl[m] > lvl[k]:
