@@ -22,7 +22,8 @@ constexpr int kAttrWarps = kAttrThreads / 32;
 
 // ---------------------------------------------------------------- H7
 // Attractive pass as a persistent TMA pipeline (one CTA per SM).  The CTA
-// owns a contiguous range of rows, cut into batches of kAtRows rows.  A
+// owns a contiguous range of rows, cut into batches of at most kAtRows rows
+// whose nonzeros fit a stage buffer.  A
 // producer warp streams each batch's col/val span (contiguous in the CSR)
 // into a kAtStages-deep shared-memory ring with cp.async.bulk + mbarriers
 // (the bulk copies keep ~3 batches of the 8-byte-per-nonzero stream in flight
@@ -49,7 +50,9 @@ constexpr int kAtThreads = (kAtConsumers + 1) * 32;
 constexpr int kAtStages = TSNE_AT_STAGES;
 constexpr int kAtCap = TSNE_AT_CAP;            // nonzeros per stage buffer
 constexpr int kAtWin = TSNE_AT_WIN;            // window points
-constexpr int kAtLook = 4;                     // row_ptr prefetch distance (batches)
+constexpr int kAtLong = 2048;                  // longer rows: k_attract_long
+constexpr int kAtChunk = 30;                   // rows per row_ptr prefetch chunk (2 batches)
+constexpr int kAtLook = 4;                     // row_ptr prefetch distance (chunks)
 constexpr int kAtRpSlots = kAtLook + 1;
 static_assert(kAtStages % kAtGroups == 0, "a stage always serves the same consumer group");
 constexpr size_t kAtSmem = sizeof(float2) * kAtWin + (size_t)kAtStages * kAtCap * 8;
@@ -119,17 +122,17 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
               const double* __restrict__ Z, float alpha) {
   extern __shared__ __align__(128) unsigned char at_smem[];
   __shared__ AtMeta s_meta[kAtStages];
-  __shared__ __align__(16) int64_t s_rpring[kAtRpSlots][kAtRows + 1];
+  __shared__ __align__(16) int64_t s_rpring[kAtRpSlots][kAtChunk + 1];
   __shared__ __align__(8) uint64_t s_full[kAtStages], s_empty[kAtStages], s_win;
   float2* s_y = reinterpret_cast<float2*>(at_smem);
   int32_t* s_col = reinterpret_cast<int32_t*>(at_smem + sizeof(float2) * kAtWin);
   float* s_val = reinterpret_cast<float*>(s_col + kAtStages * kAtCap);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // this CTA's batches [kb0, kb1) -> rows [kb0 * kAtRows, min(kb1 * kAtRows, n_rows))
-  const int nb = (n_rows + kAtRows - 1) / kAtRows;
-  const int kb0 = (int)((int64_t)nb * blockIdx.x / gridDim.x);
-  const int kb1 = (int)((int64_t)nb * (blockIdx.x + 1) / gridDim.x);
-  const int lr0 = kb0 * kAtRows, lr1 = min(kb1 * kAtRows, n_rows);
+  // this CTA's rows [lr0, lr1): whole chunks of kAtChunk rows
+  const int nch_all = (n_rows + kAtChunk - 1) / kAtChunk;
+  const int c0 = (int)((int64_t)nch_all * blockIdx.x / gridDim.x);
+  const int c1 = (int)((int64_t)nch_all * (blockIdx.x + 1) / gridDim.x);
+  const int lr0 = c0 * kAtChunk, lr1 = min(c1 * kAtChunk, n_rows);
   int wlo = row0 + (lr0 + lr1) / 2 - kAtWin / 2;
   wlo = min(wlo, Ny - kAtWin);
   wlo = max(wlo, 0) & ~1;                      // 16-byte aligned source
@@ -152,39 +155,38 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
       mbar_arrive_tx(&s_win, (uint32_t)(wn * sizeof(float2)));
       bulk_g2s(sbase, Y + wlo, (uint32_t)(wn * sizeof(float2)), &s_win);
     }
-    // row_ptr of batch kb + kAtLook is fetched with cp.async into a small ring
-    // while batch kb is issued, so the producer never waits on a global load
-    auto fetch_rp = [&](int kb) {
-      if (kb < kb1 && lane <= kAtRows) {
-        const int r = min(kb * kAtRows + lane, n_rows);
+    // row_ptr of chunk c + kAtLook is fetched with cp.async into a small ring
+    // while chunk c is cut into batches, so the producer never waits on a
+    // global load.  A batch is at most kAtRows rows whose nonzeros fit a stage
+    // (a longer single row is read from global memory by its consumer).
+    auto fetch_rp = [&](int c) {
+      if (c < c1 && lane <= kAtChunk) {
+        const int r = min(c * kAtChunk + lane, n_rows);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                         smem_u32(&s_rpring[kb % kAtRpSlots][lane])),
+                         smem_u32(&s_rpring[c % kAtRpSlots][lane])),
                      "l"(row_ptr + r)
                      : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    for (int j = 0; j < kAtLook; ++j) fetch_rp(kb0 + j);
-    for (int kb = kb0; kb < kb1; ++kb) {
-      const int k = kb - kb0, s = k % kAtStages;
+    int k = 0;                                  // batch sequence number
+    auto issue = [&](int r0, int nr, const int64_t* rpb, bool sentinel) {
+      const int s = k % kAtStages;
       if (k >= kAtStages) mbar_wait_spin(&s_empty[s], ((k / kAtStages) - 1) & 1);
-      fetch_rp(kb + kAtLook);
-      asm volatile("cp.async.wait_group %0;" ::"n"(kAtLook) : "memory");
-      __syncwarp();
-      const int r0 = kb * kAtRows, nr = min(kAtRows, n_rows - r0);
       AtMeta& m = s_meta[s];
-      const int64_t v = (lane <= kAtRows) ? s_rpring[kb % kAtRpSlots][lane] : 0;
-      if (lane <= kAtRows) m.rp[lane] = v;
-      const int64_t e_lo = __shfl_sync(0xffffffffu, v, 0);
-      const int64_t e_hi = __shfl_sync(0xffffffffu, v, nr);
-      const int64_t a_lo = e_lo & ~int64_t(3);
-      int64_t a_hi = min((e_hi + 3) & ~int64_t(3), nnz4);
-      if (e_hi + 3 - a_lo > kAtCap) a_hi = a_lo;              // does not fit: read from global
+      int64_t a_lo = 0, a_hi = 0;
+      if (!sentinel) {
+        if (lane <= nr) m.rp[lane] = rpb[lane];
+        const int64_t e_lo = rpb[0], e_hi = rpb[nr];
+        a_lo = e_lo & ~int64_t(3);
+        a_hi = min((e_hi + 3) & ~int64_t(3), nnz4);
+        if (e_hi + 3 - a_lo > kAtCap) a_hi = a_lo;            // does not fit: read from global
+      }
       if (lane == 0) {
         m.a_lo = a_lo;
         m.a_hi = a_hi;
         m.r0 = r0;
-        m.nrows = nr;
+        m.nrows = sentinel ? -1 : nr;
       }
       __syncwarp();
       if (lane == 0) {
@@ -195,7 +197,27 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
           bulk_g2s(smem_u32(s_val + s * kAtCap), val + a_lo, cnt * 4u, &s_full[s]);
         }
       }
+      ++k;
+    };
+    for (int j = 0; j < kAtLook; ++j) fetch_rp(c0 + j);
+    for (int c = c0; c < c1; ++c) {
+      fetch_rp(c + kAtLook);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kAtLook) : "memory");
+      __syncwarp();
+      const int64_t* rpc = s_rpring[c % kAtRpSlots];
+      const int cr0 = c * kAtChunk, cn = min(kAtChunk, n_rows - cr0);
+      for (int b0 = 0; b0 < cn;) {
+        // largest nr <= kAtRows with rows [b0, b0 + nr) fitting a stage (a prefix: rp grows)
+        const int l = lane + 1;
+        const bool ok = l <= kAtRows && b0 + l <= cn &&
+                        rpc[b0 + l] + 3 - (rpc[b0] & ~int64_t(3)) <= kAtCap;
+        int nr = __popc(__ballot_sync(0xffffffffu, ok));
+        nr = nr > 0 ? nr : 1;
+        issue(cr0 + b0, nr, rpc + b0, false);
+        b0 += nr;
+      }
     }
+    for (int g = 0; g < kAtGroups; ++g) issue(0, 0, nullptr, true);   // one end marker per group
     asm volatile("cp.async.wait_all;" ::: "memory");
     return;
   }
@@ -203,10 +225,11 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
   // -------------------------------------------------------------- consumers
   mbar_wait_spin(&s_win, 0);
   const int grp = wid / kAtRows, wr = wid % kAtRows;
-  for (int kb = kb0 + grp; kb < kb1; kb += kAtGroups) {
-    const int k = kb - kb0, s = k % kAtStages;
+  for (int k = grp;; k += kAtGroups) {
+    const int s = k % kAtStages;
     mbar_wait_spin(&s_full[s], (k / kAtStages) & 1);
     const AtMeta& m = s_meta[s];
+    if (m.nrows < 0) break;                     // end marker
     if (wr < m.nrows) {
       const int l = m.r0 + wr;
       const int i = row0 + l;
@@ -224,14 +247,14 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
 #pragma unroll 4
         for (int q = lane; q < n; q += 32)
           win_accum(yi, win_y(sbase, Y, cr[q], wlo, wn), vr[q], ax, ay);
-      } else {
+      } else if (n <= kAtLong) {
         for (int q = lane; q < n; q += 32)
           win_accum(yi, win_y(sbase, Y, __ldcs(col + e0 + q), wlo, wn), __ldcs(val + e0 + q), ax,
                     ay);
       }
       ax = warp_sum(ax);
       ay = warp_sum(ay);
-      if (lane == 0) {
+      if (lane == 0 && n <= kAtLong) {          // longer rows: k_attract_long
         if (MODE == 0) {
           out[l] = make_float2(ax, ay);
         } else {
@@ -243,6 +266,61 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&s_empty[s]);
+  }
+}
+
+// Rows longer than kAtLong nonzeros (hubs of the kNN graph: a point that is a
+// neighbour of thousands of others) would serialise one warp of the
+// pipeline; a whole CTA takes each of them instead.  CTA b scans rows
+// [b*n/G, (b+1)*n/G) and processes the long ones: threads stride the row, the
+// sum is reduced in a fixed order (deterministic).
+constexpr int kLongThreads = 512;
+
+template <int MODE>
+__global__ void __launch_bounds__(kLongThreads)
+k_attract_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+               const float* __restrict__ val, const float2* __restrict__ Y, int row0, int n_rows,
+               float2* __restrict__ out, const float2* __restrict__ rep,
+               const double* __restrict__ Z, float alpha) {
+  __shared__ float2 s_red[kLongThreads / 32];
+  __shared__ unsigned s_ball[kLongThreads / 32];
+  const int r0 = (int)((int64_t)n_rows * blockIdx.x / gridDim.x);
+  const int r1 = (int)((int64_t)n_rows * (blockIdx.x + 1) / gridDim.x);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = r0; base < r1; base += kLongThreads) {
+    const int r = base + (int)threadIdx.x;
+    const bool lng = r < r1 && row_ptr[r + 1] - row_ptr[r] > kAtLong;
+    const unsigned ball = __ballot_sync(0xffffffffu, lng);
+    if (lane == 0) s_ball[wid] = ball;
+    __syncthreads();
+    for (int w = 0; w < kLongThreads / 32; ++w) {
+      unsigned b = s_ball[w];
+      while (b) {                                       // block-uniform loop
+        const int l = base + w * 32 + __ffs(b) - 1;
+        b &= b - 1;
+        const float2 yi = Y[row0 + l];
+        float ax = 0.f, ay = 0.f;
+        for (int64_t e = row_ptr[l] + threadIdx.x; e < row_ptr[l + 1]; e += kLongThreads)
+          win_accum(yi, __ldg(Y + __ldcs(col + e)), __ldcs(val + e), ax, ay);
+        ax = warp_sum(ax);
+        ay = warp_sum(ay);
+        if (lane == 0) s_red[wid] = make_float2(ax, ay);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          float sx = 0.f, sy = 0.f;
+          for (int q = 0; q < kLongThreads / 32; ++q) { sx += s_red[q].x; sy += s_red[q].y; }
+          if (MODE == 0) {
+            out[l] = make_float2(sx, sy);
+          } else {
+            const float invZ = (float)Z[1];
+            const float2 f = rep[l];
+            out[l] = make_float2(4.f * (alpha * sx - f.x * invZ), 4.f * (alpha * sy - f.y * invZ));
+          }
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -258,11 +336,16 @@ static tsne_status launch_win(const int64_t* row_ptr, const int32_t* col, const 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAtSmem));
     attr = true;
   }
-  const int64_t nb = (n_rows + kAtRows - 1) / kAtRows;
-  const int blocks = (int)(nb < kNumSMs ? nb : kNumSMs);
+  const int64_t nch = (n_rows + kAtChunk - 1) / kAtChunk;
+  const int blocks = (int)(nch < kNumSMs ? nch : kNumSMs);
   k_attract_tma<MODE><<<blocks, kAtThreads, kAtSmem, s>>>(row_ptr, col, val, Y, (int)Ny,
                                                            (int)row0, (int)n_rows, out, rep, Z,
                                                            alpha);
+  TSNE_LAUNCH_CHECK();
+  const int64_t lb = (n_rows + kLongThreads - 1) / kLongThreads;
+  const int lblocks = (int)(lb < 2 * kNumSMs ? lb : 2 * kNumSMs);
+  k_attract_long<MODE><<<lblocks, kLongThreads, 0, s>>>(row_ptr, col, val, Y, (int)row0,
+                                                        (int)n_rows, out, rep, Z, alpha);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }
