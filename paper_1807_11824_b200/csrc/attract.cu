@@ -243,10 +243,18 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
       if (e0 >= a_lo && e1 <= a_hi) {             // the row is staged (the common case)
         const int32_t* cr = cs + (e0 - a_lo);
         const float* vr = vs + (e0 - a_lo);
+        int q = lane;
+        // long rows (K = 150 workloads): 8 gathers in flight per lane -- their
+        // neighbours are spread and many gathers go to L2
+        for (; q + 7 * 32 < n; q += 8 * 32) {
+          float2 yj[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) yj[u] = win_y(sbase, Y, cr[q + 32 * u], wlo, wn);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) win_accum(yi, yj[u], vr[q + 32 * u], ax, ay);
+        }
 #pragma unroll 4
-#pragma unroll 4
-        for (int q = lane; q < n; q += 32)
-          win_accum(yi, win_y(sbase, Y, cr[q], wlo, wn), vr[q], ax, ay);
+        for (; q < n; q += 32) win_accum(yi, win_y(sbase, Y, cr[q], wlo, wn), vr[q], ax, ay);
       } else if (n <= kAtLong) {
         for (int q = lane; q < n; q += 32)
           win_accum(yi, win_y(sbase, Y, __ldcs(col + e0 + q), wlo, wn), __ldcs(val + e0 + q), ax,
