@@ -345,10 +345,24 @@ def run_ours(args, rank, world):
                      "frac": ach / hbm, "traffic": traffic, "peak_source": which,
                      "algorithmic_bytes": bytes_attr})
     else:
+        # k_traverse is issue bound: its roofline is the SM issue rate,
+        # 148 SMs x 4 schedulers x 1 warp-instruction per clock at the measured SM clock;
+        # achieved = the kernel's warp instructions per launch (ncu, profiles/traffic.json)
+        # / its CUDA-event time.  The HBM-bound attractive pass is reported beside it.
+        tj = json.load(open(tf)) if os.path.exists(tf) else {}
+        inst = tj.get("k_traverse_warp_inst")
+        clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+        peak_issue = 148 * 4 * clk_mhz * 1e6 / 1e9            # G warp-instructions / s
+        ach = inst / (prof[kern] / 1e3) / 1e9 if inst else None
+        roof.update({"bound": "alu", "achieved": ach, "peak": peak_issue,
+                     "unit": "G warp-instructions/s", "frac": ach / peak_issue if ach else None,
+                     "traffic": traffic, "peak_source": "148 SMs x 4 issue/clk x measured SM clock",
+                     "warp_instructions_per_launch": inst})
         ach_attr = bytes_attr / (prof["attract_ms"] / 1e3) / 1e9
-        roof.update({"bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None,
-                     "traffic": traffic, "note": "traversal is issue/latency bound; DESIGN.md 7",
-                     "attract_hbm_gbs": ach_attr, "attract_frac": ach_attr / hbm})
+        roof["hbm_kernel"] = {"kernel": "k_attract_tma", "kernel_ms": prof["attract_ms"],
+                              "bound": "hbm", "achieved": ach_attr, "peak": hbm, "unit": "GB/s",
+                              "frac": ach_attr / hbm, "traffic": tj.get("k_attract_tma"),
+                              "algorithmic_bytes": bytes_attr}
     roof["update_hbm_gbs"] = bytes_upd / (prof["update_ms"] / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
