@@ -148,6 +148,7 @@ __device__ __forceinline__ void bucket_pairs(const float2* __restrict__ ys, int 
   }
 }
 
+template <bool STATS>
 __global__ void __launch_bounds__(kTravThreads, 4)
 k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            const double2* __restrict__ com64, const float2* __restrict__ ys,
@@ -156,7 +157,8 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            float theta, float2* __restrict__ rep, double* __restrict__ zpart,
            unsigned* __restrict__ counter, double* __restrict__ Zout,
            const int32_t* __restrict__ list, const int32_t* __restrict__ nlist, int row0,
-           const BucketSum* __restrict__ bsum, int stats) {
+           const BucketSum* __restrict__ bsum) {
+  constexpr bool stats = STATS;
   // list (multi-GPU): the sorted positions of the points this rank owns
   // (original indices [row0, ...)); rep is then indexed by perm[k] - row0.
   // per level l: {r^2 (fp32), margin constant A_l, margin slope B_l}, r^2 (fp64)
@@ -367,10 +369,15 @@ tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s) {
   const int N = (int)w.N;
   tsne_status st = launch_bucket_pairs(w, nullptr, nullptr, s);
   if (st != TSNE_OK) return st;
-  k_traverse<<<traverse_blocks(N), kTravThreads, 0, s>>>(
-      w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
-      w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0,
-      reinterpret_cast<const BucketSum*>(w.fq), trav_stats_on());
+  const BucketSum* bs = reinterpret_cast<const BucketSum*>(w.fq);
+  if (trav_stats_on())
+    k_traverse<true><<<traverse_blocks(N), kTravThreads, 0, s>>>(
+        w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
+        w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0, bs);
+  else
+    k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
+        w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
+        w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0, bs);
   TSNE_LAUNCH_CHECK();
   if (trav_stats_on()) {
     unsigned long long h[5];
@@ -390,10 +397,10 @@ tsne_status launch_traverse_list(TreeWS& w, float theta, const int32_t* list, co
   const int N = (int)w.N;
   tsne_status st = launch_bucket_pairs(w, list, nlist, s);
   if (st != TSNE_OK) return st;
-  k_traverse<<<traverse_blocks(N), kTravThreads, 0, s>>>(
+  k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta,
       rep_local, w.zpart, w.counter + 1, z_partial, list, nlist, row0,
-      reinterpret_cast<const BucketSum*>(w.fq), 0);
+      reinterpret_cast<const BucketSum*>(w.fq));
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }
