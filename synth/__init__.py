@@ -178,3 +178,31 @@ def random_rows_csr(N: int, k: int = 126, seed: int = 11):
     val = rng.random(N * k).astype(np.float32)
     val /= np.float32(val.sum(dtype=np.float64))
     return rp, cols.ravel(), val
+
+
+def hub_csr(N: int, k: int = 8, hub_degrees=(2500, 5000, 9000, 15000), seed: int = 13):
+    """random_csr plus a few hub points joined to many others (rows far longer
+    than a kNN row: the attractive pass's long-row path), symmetric, sum 1;
+    drawn, not computed by the method."""
+    rng = np.random.default_rng(seed)
+    rows = np.repeat(np.arange(N), k)
+    cols = rng.integers(0, N, size=N * k)
+    hubs = rng.choice(N, size=len(hub_degrees), replace=False)
+    hr = [np.full(d, h) for h, d in zip(hubs, hub_degrees)]
+    hc = [rng.choice(N, size=d, replace=False) for d in hub_degrees]
+    rows = np.concatenate([rows] + hr)
+    cols = np.concatenate([cols] + hc)
+    keep = rows != cols
+    r = np.concatenate([rows[keep], cols[keep]])
+    c = np.concatenate([cols[keep], rows[keep]])
+    key = np.unique(r.astype(np.int64) * N + c)
+    r = (key // N).astype(np.int64)
+    c = (key % N).astype(np.int32)
+    lo = np.minimum(r, c).astype(np.int64) * N + np.maximum(r, c)
+    uniq, inv = np.unique(lo, return_inverse=True)
+    sym = rng.random(len(uniq))[inv]
+    sym = sym / sym.sum()
+    row_ptr = np.zeros(N + 1, np.int64)
+    np.add.at(row_ptr, r + 1, 1)
+    row_ptr = np.cumsum(row_ptr)
+    return row_ptr, c, sym.astype(np.float32), sym

@@ -131,3 +131,35 @@ def test_real_p_from_oracle(T, orc):
         g, Z = gpu_grad(T, rp, col, v32, Y, theta, 1.0)
         go, Zo = orc.gradient_bh(rp, col, v32, Y, theta, 1.0)
         assert rel(g, go) <= (1e-5 if theta == 0 else 1e-4)
+
+
+@pytest.mark.parametrize("kind", ["gauss10", "blobs"])
+def test_hub_rows(T, orc, kind):
+    # rows of 2.5k-15k nonzeros (k_attract_long) among short ones (the TMA
+    # pipeline), including rows between 256 and 2048 (8-deep gathers)
+    N = 20000
+    rp, col, v32, _ = synth.hub_csr(N, 8, (300, 700, 1500, 2100, 2500, 5000, 15000), seed=17)
+    assert (np.diff(rp) > 2048).sum() >= 3
+    Y = synth.fixed_y(kind, N, seed=9)
+    g, Z = gpu_grad(T, rp, col, v32, Y, 0.5, 12.0)
+    go, Zo = orc.gradient_bh(rp, col, v32, Y, 0.5, 12.0)
+    assert rel(g, go) <= 1e-4
+    # the attractive part alone, row by row, through a theta = 0.5 gradient at exaggeration
+    # 1 and 2 (dY(2) - dY(1) = 4 A): checks the long rows' sums directly
+    g1, _ = gpu_grad(T, rp, col, v32, Y, 0.5, 1.0)
+    g2, _ = gpu_grad(T, rp, col, v32, Y, 0.5, 2.0)
+    A = orc.attractive(rp, col, v32, Y)
+    long_rows = np.nonzero(np.diff(rp) > 256)[0]
+    np.testing.assert_allclose((g2 - g1)[long_rows] / 4.0, A[long_rows], rtol=2e-4,
+                               atol=1e-6 * np.abs(A).max())
+
+
+def test_long_uniform_rows(T, orc):
+    # K = 150-like rows of 300 nonzeros everywhere (C4 shape)
+    N = 8000
+    rp, col, v32 = synth.random_rows_csr(N, 300, seed=5)
+    Y = synth.fixed_y("clustered", N, seed=2)
+    g1, _ = gpu_grad(T, rp, col, v32, Y, 0.5, 1.0)
+    g2, _ = gpu_grad(T, rp, col, v32, Y, 0.5, 2.0)
+    A = orc.attractive(rp, col, v32, Y)
+    assert rel((g2 - g1) / 4.0, A) <= 1e-5
