@@ -23,6 +23,9 @@
 namespace tsne {
 
 constexpr int kTravThreads = 256;
+#ifndef TSNE_TRAV_MINB
+#define TSNE_TRAV_MINB 5   // 48 registers, no spills: 40 warps per SM
+#endif
 
 // diagnostics (TSNE_TRAV_STATS=1): [0] sum of node visits, [1] sum over warps
 // of the warp's max visits, [2] accepted cells + exact pairs, [3] fp64 re-tests,
@@ -149,7 +152,7 @@ __device__ __forceinline__ void bucket_pairs(const float2* __restrict__ ys, int 
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(kTravThreads, 4)
+__global__ void __launch_bounds__(kTravThreads, TSNE_TRAV_MINB)
 k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            const double2* __restrict__ com64, const float2* __restrict__ ys,
            const int32_t* __restrict__ leafnode, const int32_t* __restrict__ perm,
