@@ -246,7 +246,8 @@ tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const floa
   Sched sc{cfg.exag_iters, exaggeration, cfg.mom0, cfg.mom1, learning_rate, cfg.min_gain};
   st = run_iterations(row_ptr, col, val, N, reinterpret_cast<float2*>(Y),
                       reinterpret_cast<float2*>(v), reinterpret_cast<float2*>(gains), t0, n_iter,
-                      theta, sc, cfg.use_graphs != 0, cfg.relabel_every, p.tree, p.opt, s);
+                      theta, sc, cfg.use_graphs != 0, cfg.relabel_every, p.tree, p.opt, s,
+                      /*cache_order=*/true);
   int32_t flag = 0;
   if (st == TSNE_OK) {
     cudaError_t e = cudaMemcpyAsync(&flag, p.opt.flag, sizeof(flag), cudaMemcpyDeviceToHost, s);
@@ -636,7 +637,7 @@ tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, 
     Sched sc{cfg.exag_iters, exaggeration, cfg.mom0, cfg.mom1, learning_rate, cfg.min_gain};
     if (st == TSNE_OK)
       st = run_iterations(rp, col, val, N, Y, V, G, 0, n_iter, theta, sc, cfg.use_graphs != 0,
-                          cfg.relabel_every, p.tree, p.opt, s);
+                          cfg.relabel_every, p.tree, p.opt, s, /*cache_order=*/false);
     if (st == TSNE_OK) {
       int32_t flag = 0;
       cudaMemcpyAsync(&flag, p.opt.flag, sizeof(flag), cudaMemcpyDeviceToHost, s);

@@ -4,6 +4,7 @@
 // and replayed; the iteration-dependent constants (exaggeration, momentum)
 // are read on the device from an iteration counter, so one graph serves the
 // whole run.
+#include <mutex>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -26,6 +27,9 @@ void carve_opt(Carver& c, OptWS& o, int64_t N, int64_t nnz) {
   o.lab = c.take<int32_t>(N);
   o.lab2 = c.take<int32_t>(N);
   o.inv = c.take<int32_t>(N);
+  o.dperm = c.take<int32_t>(N);
+  o.dtag = c.take<uint64_t>(1);
+  o.ws_base = reinterpret_cast<void*>(c.base);
   for (int h = 0; h < 2; ++h) {
     o.rp[h] = c.take<int64_t>(N + 1);
     o.col[h] = c.take<int32_t>(nnz + 4);
@@ -185,6 +189,76 @@ k_diffuse(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
   if (lane == 0) u2[i] = (sw > 0.f) ? make_float2(sx / sw, sy / sw) : u[i];
 }
 
+// The order depends only on P, so it is kept in the caller's workspace and
+// reused by later tsne_optimize calls with the same workspace and CSR.  The
+// host keeps (key, fingerprint of the stored order); a hit needs the stored
+// order to still hash to it (a 64-bit mix of every entry, recomputed on the
+// device: ~10 us), so a workspace reused for anything else is never trusted.
+struct DiffKey {
+  const void* ws;
+  const int64_t* rp;
+  const int32_t* col;
+  const float* val;
+  int64_t N, nnz;
+  uint64_t hash;
+};
+static std::mutex g_diff_mu;
+static std::vector<DiffKey> g_diff_cache;
+
+static bool same_key(const DiffKey& a, const DiffKey& b) {
+  return a.ws == b.ws && a.rp == b.rp && a.col == b.col && a.val == b.val && a.N == b.N &&
+         a.nnz == b.nnz;
+}
+
+__global__ void k_perm_hash(const int32_t* __restrict__ perm, int N,
+                            unsigned long long* __restrict__ out) {
+  unsigned long long h = 0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    unsigned long long x = ((unsigned long long)(uint32_t)perm[k] << 32) | (uint32_t)k;
+    x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    h += x;                                   // a sum: independent of the order of addition
+  }
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, h);
+}
+
+static bool perm_hash(const OptWS& o, int64_t N, uint64_t* h, cudaStream_t s) {
+  if (cudaMemsetAsync(o.dtag, 0, sizeof(uint64_t), s) != cudaSuccess) return false;
+  k_perm_hash<<<2 * kNumSMs, 256, 0, s>>>(o.dperm, (int)N, (unsigned long long*)o.dtag);
+  if (cudaGetLastError() != cudaSuccess) return false;
+  if (cudaMemcpyAsync(h, o.dtag, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return false;
+  return cudaStreamSynchronize(s) == cudaSuccess;
+}
+
+static bool diff_cached(const DiffKey& k, const OptWS& o, cudaStream_t s) {
+  uint64_t want = 0;
+  bool found = false;
+  {
+    std::lock_guard<std::mutex> g(g_diff_mu);
+    for (const auto& e : g_diff_cache)
+      if (same_key(e, k)) { want = e.hash; found = true; }
+  }
+  uint64_t h = 0;
+  return found && perm_hash(o, k.N, &h, s) && h == want;
+}
+
+static tsne_status diff_remember(DiffKey k, const OptWS& o, cudaStream_t s) {
+  uint64_t h = 0;
+  if (!perm_hash(o, k.N, &h, s)) {
+    set_error("diffusion order: fingerprint failed");
+    return TSNE_ERR_CUDA;
+  }
+  k.hash = h;
+  std::lock_guard<std::mutex> g(g_diff_mu);
+  for (auto& e : g_diff_cache)
+    if (e.ws == k.ws) { e = k; return TSNE_OK; }
+  if (g_diff_cache.size() > 64) g_diff_cache.erase(g_diff_cache.begin());
+  g_diff_cache.push_back(k);
+  return TSNE_OK;
+}
+
 static tsne_status diffusion_order(const int64_t* row_ptr, const int32_t* col, const float* val,
                                    int64_t N, TreeWS& w, OptWS& o, cudaStream_t s) {
   float2* u = o.tmp;
@@ -205,19 +279,26 @@ static tsne_status diffusion_order(const int64_t* row_ptr, const int32_t* col, c
 // Morton order of the caller's Y later (or the caller's order if !morton).
 static tsne_status enter(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t N,
                          float2* Y, float2* V, float2* G, int32_t t0, TreeWS& w, OptWS& o,
-                         bool morton, cudaStream_t s) {
+                         bool morton, bool cache_order, cudaStream_t s) {
   k_set_state<<<1, 1, 0, s>>>(o.t_dev, t0, o.flag);
   TSNE_LAUNCH_CHECK();
   tsne_status st;
   const int32_t* perm = nullptr;
   if (morton) {
     if (t0 < kMortonFrom) {
-      if ((st = diffusion_order(row_ptr, col, val, N, w, o, s)) != TSNE_OK) return st;
+      const DiffKey key{o.ws_base, row_ptr, col, val, N, o.nnz, 0};
+      if (!cache_order || !diff_cached(key, o, s)) {
+        if ((st = diffusion_order(row_ptr, col, val, N, w, o, s)) != TSNE_OK) return st;
+        TSNE_CUDA_TRY(cudaMemcpyAsync(o.dperm, w.perm, sizeof(int32_t) * N,
+                                      cudaMemcpyDeviceToDevice, s));
+        if (cache_order && (st = diff_remember(key, o, s)) != TSNE_OK) return st;
+      }
+      perm = o.dperm;
     } else {
       if ((st = launch_bbox(w, Y, s)) != TSNE_OK) return st;
       if ((st = build_tree(w, Y, /*apply_shift=*/false, s)) != TSNE_OK) return st;
     }
-    perm = w.perm;
+    if (!perm) perm = w.perm;
   }
   if ((st = launch_bbox(w, Y, s)) != TSNE_OK) return st;      // root box of the caller's Y
   return relabel(perm, (int)N, row_ptr, col, val, Y, V, G, nullptr, 0, o, s);
@@ -260,9 +341,9 @@ static tsne_status capture_pair(Graph& gr, int h, int64_t N, float theta, const 
 tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                            int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t n_iter,
                            float theta, const Sched& sc, bool use_graphs, int relabel_every,
-                           TreeWS& w, OptWS& o, cudaStream_t s) {
+                           TreeWS& w, OptWS& o, cudaStream_t s, bool cache_order) {
   SideRes side(o);
-  tsne_status st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, relabel_every > 0, s);
+  tsne_status st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, relabel_every > 0, cache_order, s);
   if (st != TSNE_OK) return st;
   int h = 0;                                   // P half in use
   const bool graphs = use_graphs && s != nullptr && n_iter >= 4;
@@ -308,7 +389,7 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
                                float theta, const Sched& sc, TreeWS& w, OptWS& o, double* stage_ms,
                                int32_t* kernels, cudaStream_t s) {
   SideRes side(o);
-  tsne_status st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, true, s);
+  tsne_status st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, true, true, s);
   if (st != TSNE_OK) return st;
   if (kernels) {  // count kernel nodes of one captured (never launched) iteration
     cudaGraph_t g = nullptr;

@@ -25,6 +25,9 @@ struct OptWS {
   cudaStream_t side = nullptr;           // attractive pass runs here, concurrently
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int32_t *lab = nullptr, *lab2 = nullptr, *inv = nullptr;
+  int32_t* dperm = nullptr;              // cached diffusion order of P (see enter())
+  uint64_t* dtag = nullptr;              // its validity tag (device copy)
+  void* ws_base = nullptr;               // the caller's workspace (cache key)
   int64_t* rp[2] = {nullptr, nullptr};
   int32_t* col[2] = {nullptr, nullptr};
   float* val[2] = {nullptr, nullptr};
@@ -48,7 +51,7 @@ tsne_status launch_update(const float2* Yin, const float2* A, int64_t N, TreeWS&
 tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                            int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t n_iter,
                            float theta, const Sched& sc, bool use_graphs, int relabel_every,
-                           TreeWS& w, OptWS& o, cudaStream_t s);
+                           TreeWS& w, OptWS& o, cudaStream_t s, bool cache_order);
 
 tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                                int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t reps,
