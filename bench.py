@@ -364,6 +364,25 @@ def run_ours(args, rank, world):
                               "frac": ach_attr / hbm, "traffic": tj.get("k_attract_tma"),
                               "algorithmic_bytes": bytes_attr}
     roof["update_hbm_gbs"] = bytes_upd / (prof["update_ms"] / 1e3) / 1e9
+    # the kNN stage against the tensor roofline: algorithmic flops of the
+    # candidate GEMM -- 2 D_p per (query, point) pair, each unordered pair once on the
+    # symmetric path -- over the whole stage's time (locality order, pilot, sweep,
+    # selection, fp64 re-rank included); peak = measured sustained bf16 (= fp16) rate
+    knn_roof = None
+    if stages.get("knn_ms"):
+        Dp = (cfg.D + 63) // 64 * 64
+        # per GPU: at N > 1 each rank sweeps its own N/world query rows against all N
+        pairs = N * N / 2 if kinfo["gemm_path"] == "tcgen05-sym" else N * N / world
+        flop = 2.0 * Dp * pairs
+        pk = None
+        pf = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(pf):
+            pk = json.load(open(pf)).get("bf16_tflops_sustained")
+        ach = flop / (stages["knn_ms"] / 1e3) / 1e12
+        knn_roof = {"kernel": "kNN stage (%s)" % kinfo["gemm_path"], "bound": "tensor",
+                    "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                    "frac": ach / pk if pk else None, "flop": flop,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (fp16 runs at the bf16 rate)"}
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -376,6 +395,7 @@ def run_ours(args, rank, world):
                    "knn_rows_uncertified": kinfo["rows_uncertified"]},
         "stages": stages,
         "roofline": roof,
+        "knn_roofline": knn_roof,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
