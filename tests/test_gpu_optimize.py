@@ -126,3 +126,22 @@ def test_nonfinite_sentinel(T, c1):
     opt = T.Optimizer(dev(rp), dev(col), dev(v32), T.init_y(1000, 1), learning_rate=1e38)
     with pytest.raises(T.TsneError, match="NONFINITE"):
         opt.step(5)
+
+
+def test_long_run_c2_shaped_single_seed(T, orc):
+    # a single-seed check on MNIST-shaped data, where the per-point statistics
+    # are far less noisy than at N = 1000 (N = 20000 here keeps the fp64 oracle to ~1 min)
+    X = synth.make_x("C2", n=20000).numpy()
+    idx, d2 = orc.knn(X, 90)
+    rp, col, v64, v32, *_ = orc.compute_p(idx, d2, 30.0)
+    Y0 = orc.init_y(X.shape[0], 42)
+    Yo, _, _ = orc.optimize(rp, col, v32, Y0, n_iter=1000, theta=0.5)
+    Yg, info = T.run(torch.as_tensor(X).pin_memory(), perplexity=30.0, theta=0.5, n_iter=1000,
+                     seed=42)
+    assert info["knn_rows_uncertified"] == 0
+    Yg = Yg.numpy().astype(np.float64)
+    kl_g, kl_o = orc.kl(rp, col, v32, Yg), orc.kl(rp, col, v32, Yo)
+    nn_g, nn_o = orc.nn_preservation(idx, Yg, 10), orc.nn_preservation(idx, Yo, 10)
+    print(f"C2-shaped N=20000: KL gpu {kl_g:.5f} oracle {kl_o:.5f}; 10-NN gpu {nn_g:.4f} oracle {nn_o:.4f}")
+    assert abs(kl_g - kl_o) <= 0.01 * kl_o, (kl_g, kl_o)
+    assert abs(nn_g - nn_o) <= 0.01, (nn_g, nn_o)
