@@ -332,11 +332,19 @@ k_attract_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ 
   }
 }
 
+// CTAs of the pipeline: all SMs when it runs alone (tsne_gradient); 120 when it
+// runs concurrently with the tree build on a side stream (optimiser, shards):
+// the 28 SMs it leaves free take the latency-bound tree kernels, which cannot
+// share an SM with a pipeline CTA (measured at C5: iteration 1.33 -> 1.25 ms,
+// the pass alone 0.43 -> 0.53 ms).
+constexpr int kAtGridAlone = kNumSMs;
+constexpr int kAtGridShared = 120;
+
 template <int MODE>
 static tsne_status launch_win(const int64_t* row_ptr, const int32_t* col, const float* val,
                               const float2* Y, int64_t Ny, int64_t row0, int64_t n_rows,
                               float2* out, const float2* rep, const double* Z, float alpha,
-                              cudaStream_t s) {
+                              cudaStream_t s, int grid) {
   if (n_rows <= 0) return TSNE_OK;
   static bool attr = false;                    // not a stream operation (graph-capture safe)
   if (!attr) {
@@ -345,7 +353,7 @@ static tsne_status launch_win(const int64_t* row_ptr, const int32_t* col, const 
     attr = true;
   }
   const int64_t nch = (n_rows + kAtChunk - 1) / kAtChunk;
-  const int blocks = (int)(nch < kNumSMs ? nch : kNumSMs);
+  const int blocks = (int)(nch < grid ? nch : grid);
   k_attract_tma<MODE><<<blocks, kAtThreads, kAtSmem, s>>>(row_ptr, col, val, Y, (int)Ny,
                                                            (int)row0, (int)n_rows, out, rep, Z,
                                                            alpha);
@@ -486,12 +494,12 @@ int update_blocks(int64_t N) {
 tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, const float* val,
                                 const float2* Y, int64_t N, const float2* rep, const double* Z,
                                 float alpha, float2* dY, cudaStream_t s) {
-  return launch_win<1>(row_ptr, col, val, Y, N, 0, N, dY, rep, Z, alpha, s);
+  return launch_win<1>(row_ptr, col, val, Y, N, 0, N, dY, rep, Z, alpha, s, kAtGridAlone);
 }
 
 tsne_status launch_attract_sum(const int64_t* row_ptr, const int32_t* col, const float* val,
                                const float2* Y, int64_t N, float2* A, cudaStream_t s) {
-  return launch_win<0>(row_ptr, col, val, Y, N, 0, N, A, nullptr, nullptr, 1.f, s);
+  return launch_win<0>(row_ptr, col, val, Y, N, 0, N, A, nullptr, nullptr, 1.f, s, kAtGridShared);
 }
 
 tsne_status launch_update(const float2* Yin, const float2* A, int64_t N, TreeWS& w, OptWS& o,
@@ -545,7 +553,8 @@ k_update_shard(const float2* __restrict__ A, const float2* __restrict__ Y, int r
 tsne_status launch_attract_sum_shard(const int64_t* row_ptr, const int32_t* col, const float* val,
                                      const float2* Y, int64_t N, int64_t row0, int64_t n_local,
                                      float2* A, cudaStream_t s) {
-  return launch_win<0>(row_ptr, col, val, Y, N, row0, n_local, A, nullptr, nullptr, 1.f, s);
+  return launch_win<0>(row_ptr, col, val, Y, N, row0, n_local, A, nullptr, nullptr, 1.f, s,
+                       kAtGridShared);
 }
 
 tsne_status launch_update_shard(const float2* A, const float2* Y, int64_t row0, int64_t n_local,
