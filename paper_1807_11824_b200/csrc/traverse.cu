@@ -42,15 +42,6 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-// the rare fp64 re-test of the criterion (D25), kept out of line so the hot
-// loop does not issue its predicated-off instructions
-__device__ __noinline__ bool accept_fp64(const double2* __restrict__ c64, float2 yi, double r2,
-                                         double theta2d) {
-  const double2 c = *c64;
-  const double ex = __dsub_rn((double)yi.x, c.x), ey = __dsub_rn((double)yi.y, c.y);
-  const double D2d = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
-  return r2 < __dmul_rn(theta2d, D2d);
-}
 
 // Exact pairs inside each point's own bucket (a level-16 cell holding several
 // points, D9): every member opens its bucket (D11) and takes all pairs with
@@ -225,9 +216,9 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
     bool acc = diff > marg;
     // cells below level kDeepFp32 are decided, and their offset y_i - com
     // taken, in fp64: their size approaches the fp32 spacing of the coordinates
-    const bool deep = !leaf && lvl > kDeepFp32;
+    // (inside the fp32 band, too, the decision is taken in fp64, D25)
     float ddx = dx, ddy = dy, dd2 = D2;
-    if (deep && !self_in) {
+    if (!leaf && !self_in && (lvl > kDeepFp32 || fabsf(diff) <= marg)) {
       const double2 c = com64[cur];
       const double ex = __dsub_rn((double)yi.x, c.x), ey = __dsub_rn((double)yi.y, c.y);
       const double D2d = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
@@ -235,9 +226,6 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
       ddx = (float)ex;
       ddy = (float)ey;
       dd2 = __fadd_rn(__fmul_rn(ddx, ddx), __fmul_rn(ddy, ddy));
-      if (stats) ++n_f64;
-    } else if (!leaf && !self_in && fabsf(diff) <= marg) {   // inside the band: decide in fp64
-      acc = accept_fp64(com64 + cur, yi, s_r2d[lvl], theta2d);
       if (stats) ++n_f64;
     }
     // exact leaf of one point: the exact pair; internal cell: the criterion;
