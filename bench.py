@@ -337,6 +337,8 @@ def run_ours(args, rank, world):
     tf = os.path.join(ROOT, "profiles", "traffic.json")      # dram bytes per launch (ncu)
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get(stage_kern[kern])
+        if cfg.name != "C5-imagenet-resnet-shaped":
+            traffic = None                        # the ncu captures are of C5
     roof = {"kernel": stage_kern[kern], "kernel_ms": prof[kern],
             "iteration_overlapped_ms": prof.get("iteration_overlapped_ms")}
     if kern == "attract_ms":
@@ -350,18 +352,26 @@ def run_ours(args, rank, world):
         # achieved = the kernel's warp instructions per launch (ncu, profiles/traffic.json)
         # / its CUDA-event time.  The HBM-bound attractive pass is reported beside it.
         tj = json.load(open(tf)) if os.path.exists(tf) else {}
-        inst = tj.get("k_traverse_warp_inst")
+        # measured per workload (the count depends on the tree, i.e. on the data)
+        inst = (tj.get("k_traverse_warp_inst") or {}).get(cfg.name) if kern == "traverse_ms" else None
         clk_mhz = clk.summary().get("sm_mhz") or 1965.0
         peak_issue = 148 * 4 * clk_mhz * 1e6 / 1e9            # G warp-instructions / s
         ach = inst / (prof[kern] / 1e3) / 1e9 if inst else None
-        roof.update({"bound": "alu", "achieved": ach, "peak": peak_issue,
-                     "unit": "G warp-instructions/s", "frac": ach / peak_issue if ach else None,
+        if kern == "tree_ms":
+            roof["note"] = "tree build: 14 short dependent launches, latency bound (DESIGN.md 6.2)"
+        elif inst is None:
+            roof["note"] = "issue-rate roofline needs the ncu instruction count, measured for C5"
+        roof.update({"bound": "alu" if kern == "traverse_ms" else "latency", "achieved": ach,
+                     "peak": peak_issue if ach else None,
+                     "unit": "G warp-instructions/s" if ach else None,
+                     "frac": ach / peak_issue if ach else None,
                      "traffic": traffic, "peak_source": "148 SMs x 4 issue/clk x measured SM clock",
                      "warp_instructions_per_launch": inst})
         ach_attr = bytes_attr / (prof["attract_ms"] / 1e3) / 1e9
         roof["hbm_kernel"] = {"kernel": "k_attract_tma", "kernel_ms": prof["attract_ms"],
                               "bound": "hbm", "achieved": ach_attr, "peak": hbm, "unit": "GB/s",
-                              "frac": ach_attr / hbm, "traffic": tj.get("k_attract_tma"),
+                              "frac": ach_attr / hbm,
+                              "traffic": tj.get("k_attract_tma") if traffic is not None else None,
                               "algorithmic_bytes": bytes_attr}
     roof["update_hbm_gbs"] = bytes_upd / (prof["update_ms"] / 1e3) / 1e9
     # the kNN stage against the tensor roofline: algorithmic flops of the

@@ -56,7 +56,7 @@ static tsne_status one_iteration(const int64_t* row_ptr, const int32_t* col, con
                                  cudaStream_t s) {
   TSNE_CUDA_TRY(cudaEventRecord(o.ev_fork, s));
   TSNE_CUDA_TRY(cudaStreamWaitEvent(o.side, o.ev_fork, 0));
-  tsne_status st = launch_attract_sum(row_ptr, col, val, Yin, N, o.A, o.side);
+  tsne_status st = launch_attract_sum(row_ptr, col, val, Yin, N, o.nnz, o.A, o.side);
   if (st != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaEventRecord(o.ev_join, o.side));
   if ((st = build_tree(w, Yin, /*apply_shift=*/true, s)) != TSNE_OK) return st;
@@ -423,7 +423,7 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
     cudaEventRecord(e[1], s);
     if (st == TSNE_OK) st = launch_traverse(w, theta, s);
     cudaEventRecord(e[2], s);
-    if (st == TSNE_OK) st = launch_attract_sum(o.rp[0], o.col[0], o.val[0], a, N, o.A, s);
+    if (st == TSNE_OK) st = launch_attract_sum(o.rp[0], o.col[0], o.val[0], a, N, o.nnz, o.A, s);
     cudaEventRecord(e[3], s);
     if (st == TSNE_OK) st = launch_update(a, o.A, N, w, o, sc, b, o.V, o.G, s);
     cudaEventRecord(e[4], s);

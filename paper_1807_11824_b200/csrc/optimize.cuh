@@ -42,7 +42,7 @@ tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, cons
                                 const float2* Y, int64_t N, const float2* rep, const double* Z,
                                 float alpha, float2* dY, cudaStream_t s);
 tsne_status launch_attract_sum(const int64_t* row_ptr, const int32_t* col, const float* val,
-                               const float2* Y, int64_t N, float2* A, cudaStream_t s);
+                               const float2* Y, int64_t N, int64_t nnz, float2* A, cudaStream_t s);
 tsne_status launch_update(const float2* Yin, const float2* A, int64_t N, TreeWS& w, OptWS& o,
                           const Sched& sc, float2* Yout, float2* V, float2* G, cudaStream_t s);
 
