@@ -330,9 +330,11 @@ __global__ void __launch_bounds__(1024) k_bscan(longlong2* __restrict__ bsum, in
 // ---------------------------------------------------------------- H3 Karras
 // common-prefix length of sorted keys a, b within the kKeyBits-bit keys;
 // equal keys are told apart by their index (kKeyBits + prefix of a ^ b)
-__device__ __forceinline__ int kdelta(const uint64_t* __restrict__ k, int N, int a, int b) {
-  if (b < 0 || b >= N) return -1;
-  uint64_t ka = k[a], kb = k[b];
+// (the key of a is passed in a register: every search step of a node compares against it)
+__device__ __forceinline__ int kdelta_k(const uint64_t* __restrict__ k, int N, uint64_t ka, int a,
+                                        int b) {
+  if ((unsigned)b >= (unsigned)N) return -1;
+  const uint64_t kb = __ldg(k + b);
   if (ka != kb) return __clzll(ka ^ kb) - (64 - kKeyBits);
   return kKeyBits + __clz((uint32_t)a ^ (uint32_t)b);
 }
@@ -362,19 +364,20 @@ k_karras(const uint64_t* __restrict__ keys, int N, int32_t* __restrict__ bfirst,
     if (i <= N) S[i] = make_longlong2(ox + ix - v.x, oy + iy - v.y);
   }
   if (i >= N - 1) return;
-  int d = (kdelta(keys, N, i, i + 1) - kdelta(keys, N, i, i - 1)) >= 0 ? 1 : -1;
-  int dmin = kdelta(keys, N, i, i - d);
+  const uint64_t ki = __ldg(keys + i);
+  int d = (kdelta_k(keys, N, ki, i, i + 1) - kdelta_k(keys, N, ki, i, i - 1)) >= 0 ? 1 : -1;
+  int dmin = kdelta_k(keys, N, ki, i, i - d);
   int lmax = 2;
-  while (kdelta(keys, N, i, i + lmax * d) > dmin) lmax <<= 1;
+  while (kdelta_k(keys, N, ki, i, i + lmax * d) > dmin) lmax <<= 1;
   int l = 0;
   for (int t = lmax >> 1; t >= 1; t >>= 1)
-    if (kdelta(keys, N, i, i + (l + t) * d) > dmin) l += t;
+    if (kdelta_k(keys, N, ki, i, i + (l + t) * d) > dmin) l += t;
   int j = i + l * d;
-  int dnode = kdelta(keys, N, i, j);
+  int dnode = kdelta_k(keys, N, ki, i, j);
   int s = 0, t = l;
   do {
     t = (t + 1) >> 1;
-    if (kdelta(keys, N, i, i + (s + t) * d) > dnode) s += t;
+    if (kdelta_k(keys, N, ki, i, i + (s + t) * d) > dnode) s += t;
   } while (t > 1);
   int gamma = i + s * d + (d < 0 ? -1 : 0);
   int lo = min(i, j), hi = max(i, j);
