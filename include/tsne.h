@@ -137,7 +137,8 @@ tsne_status tsne_compute_p(const int32_t* idx, const double* d2, int64_t N, int3
  *   w = 1/(1 + D^2), Z = sum_i z_i
  * Tree and criterion definitions: D7-D11 (r = half side of a square cell,
  * y_cell = centre of mass, strict r^2 < theta^2 D^2, a cell containing i is
- * always opened), decided as in fp64 (D25).
+ * always opened; leaves hold one point or are level-24 cells evaluated
+ * pairwise, D9), decided as in fp64 (D25).
  *
  *   row_ptr/col/val  CSR of P as produced by tsne_compute_p; col and val
  *             must be 16-byte aligned (they are streamed as 16-byte vectors),

@@ -43,7 +43,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 
-// Exact pairs inside each point's own bucket (a level-16 cell holding several
+// Exact pairs inside each point's own bucket (a level-24 cell holding several
 // points, D9): every member opens its bucket (D11) and takes all pairs with
 // the other members.  Done here, before the traversal, warp-synchronously:
 // the lanes of a warp that share a bucket walk its members together (one

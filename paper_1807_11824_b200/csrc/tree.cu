@@ -1,7 +1,7 @@
 // tree.cu -- quadtree build over the 2-D embedding (P:L136 steps 1-4).
 //
 //  k_bbox        step 1: exact min/max, root box (D8)         [H1]
-//  k_keys        fp64 quantisation -> 32-bit Morton key (D8)  [H2]
+//  k_keys        fp64 quantisation -> 48-bit Morton key (D8, D9) [H2]
 //  radix sort    (key, point id) pairs                         [H2]
 //  k_gather      Y in Morton order + fixed-point coordinates + block sums
 //  k_bscan       exclusive scan of the block sums (one block)
@@ -14,9 +14,10 @@
 //
 // The compressed quadtree is derived from a Karras (2012) binary radix tree:
 // a binary node whose common prefix has length delta lies in the cell of
-// level L = min(delta, 32) / 2; it is a quad node iff its parent's level is
-// smaller (otherwise it merges into the parent).  Keys tie-break by index
-// (delta >= 32 -> identical keys -> a level-16 bucket).  DESIGN.md sec. 6.
+// level L = min(delta, 48) / 2 (48-bit keys, 24 levels, D9); it is a quad
+// node iff its parent's level is smaller (otherwise it merges into the
+// parent).  Keys tie-break by index (delta >= 48 -> identical keys -> a
+// level-24 bucket).  DESIGN.md sec. 6.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 

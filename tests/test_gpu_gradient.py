@@ -69,7 +69,7 @@ def test_other_thetas(T, orc, theta):
 
 
 def test_duplicates_and_buckets(T, orc):
-    # coincident points -> level-16 buckets (tested and exact), D9
+    # coincident points -> level-24 buckets (tested and exact), D9
     N = 3000
     Y = np.round(synth.fixed_y("gauss10", N, seed=5) / 2.0).astype(np.float32) * 2.0
     Y[:50] = Y[0]                       # one large bucket
