@@ -243,18 +243,47 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
       if (e0 >= a_lo && e1 <= a_hi) {             // the row is staged (the common case)
         const int32_t* cr = cs + (e0 - a_lo);
         const float* vr = vs + (e0 - a_lo);
+        // The first 32 entries decide the mode: if several of their columns lie
+        // outside the window (neighbourhoods spread over the labels, e.g. the
+        // GloVe-shaped C4), the rest of the row is issued as one predicated
+        // block of 8 gathers per lane, so the L2 latency is paid once per 256
+        // entries; otherwise the loops below (few L2 gathers) run.
         int q = lane;
-        // long rows (K = 150 workloads): 8 gathers in flight per lane -- their
-        // neighbours are spread and many gathers go to L2
-        for (; q + 7 * 32 < n; q += 8 * 32) {
-          float2 yj[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) yj[u] = win_y(sbase, Y, cr[q + 32 * u], wlo, wn);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) win_accum(yi, yj[u], vr[q + 32 * u], ax, ay);
+        bool far;
+        {
+          const bool in = q < n;
+          const int c = in ? cr[q] : i;
+          const float p = in ? vr[q] : 0.f;
+          far = __popc(__ballot_sync(0xffffffffu, (unsigned)(c - wlo) >= (unsigned)wn)) >= 4;
+          win_accum(yi, win_y(sbase, Y, c, wlo, wn), p, ax, ay);
+          q += 32;
         }
+        if (far) {
+          for (; q < n; q += 8 * 32) {
+            float2 yj[8];
+            float pj[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int e = q + 32 * u;
+              const bool in = e < n;
+              yj[u] = win_y(sbase, Y, in ? cr[e] : i, wlo, wn);
+              pj[u] = in ? vr[e] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) win_accum(yi, yj[u], pj[u], ax, ay);
+          }
+        } else {
+          // long rows (K = 150 workloads): 8 gathers in flight per lane
+          for (; q + 7 * 32 < n; q += 8 * 32) {
+            float2 yj[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) yj[u] = win_y(sbase, Y, cr[q + 32 * u], wlo, wn);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) win_accum(yi, yj[u], vr[q + 32 * u], ax, ay);
+          }
 #pragma unroll 4
-        for (; q < n; q += 32) win_accum(yi, win_y(sbase, Y, cr[q], wlo, wn), vr[q], ax, ay);
+          for (; q < n; q += 32) win_accum(yi, win_y(sbase, Y, cr[q], wlo, wn), vr[q], ax, ay);
+        }
       } else if (n <= kAtLong) {
         for (int q = lane; q < n; q += 32)
           win_accum(yi, win_y(sbase, Y, __ldcs(col + e0 + q), wlo, wn), __ldcs(val + e0 + q), ax,
@@ -308,8 +337,26 @@ k_attract_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ 
         b &= b - 1;
         const float2 yi = Y[row0 + l];
         float ax = 0.f, ay = 0.f;
-        for (int64_t e = row_ptr[l] + threadIdx.x; e < row_ptr[l + 1]; e += kLongThreads)
-          win_accum(yi, __ldg(Y + __ldcs(col + e)), __ldcs(val + e), ax, ay);
+        const int64_t eb = row_ptr[l], ee = row_ptr[l + 1];
+        for (int64_t e = eb + threadIdx.x; e < ee; e += 4 * kLongThreads) {   // 4 in flight
+          int c[4];
+          float p[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t f = e + u * kLongThreads;
+            c[u] = row0 + l;                           // absent: the point itself, p = 0
+            p[u] = 0.f;
+            if (f < ee) {
+              c[u] = __ldcs(col + f);
+              p[u] = __ldcs(val + f);
+            }
+          }
+          float2 yj[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) yj[u] = __ldg(Y + c[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) win_accum(yi, yj[u], p[u], ax, ay);
+        }
         ax = warp_sum(ax);
         ay = warp_sum(ay);
         if (lane == 0) s_red[wid] = make_float2(ax, ay);
