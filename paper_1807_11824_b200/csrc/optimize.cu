@@ -312,6 +312,48 @@ static tsne_status leave(int64_t N, const float2* Ycur, float2* Y, float2* V, fl
   return TSNE_OK;
 }
 
+// Relabel only if the Morton order of the embedding puts more of P's
+// nonzeros near their row than the current labels do (a sample of rows;
+// "near" = within the attractive pass's half window).  On data whose kNN
+// graph has no spatial structure in the embedding (C4) the diffusion order
+// stays; on clustered data the Morton order wins once the clusters form.
+__global__ void k_inv_perm(const int32_t* __restrict__ perm, int N, int32_t* __restrict__ inv) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < N) inv[perm[k]] = k;
+}
+
+__global__ void k_far_counts(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const int32_t* __restrict__ inv, int N, int stride,
+                             unsigned long long* __restrict__ cnt) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) * stride;
+  unsigned long long cur = 0, nw = 0;
+  if (r < N) {
+    const int ir = inv[r];
+    for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+      const int c = col[e];
+      cur += (unsigned)abs(c - r) > 6144u;
+      nw += (unsigned)abs(inv[c] - ir) > 6144u;
+    }
+  }
+  atomicAdd(cnt, cur);
+  atomicAdd(cnt + 1, nw);
+}
+
+static bool morton_improves(const int64_t* rp, const int32_t* col, const int32_t* perm, int64_t N,
+                            OptWS& o, cudaStream_t s) {
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(o.len);   // scratch (relabel rewrites it)
+  k_inv_perm<<<(int)((N + 255) / 256), 256, 0, s>>>(perm, (int)N, o.inv);
+  const int stride = N > 65536 ? (int)(N / 65536) : 1;
+  const int rows = (int)((N + stride - 1) / stride);
+  unsigned long long h[2] = {0, 0};
+  if (cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess) return true;
+  k_far_counts<<<(rows + 255) / 256, 256, 0, s>>>(rp, col, o.inv, (int)N, stride, cnt);
+  if (cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return true;
+  return h[1] <= h[0];
+}
+
 struct Graph {
   cudaGraph_t g = nullptr;
   cudaGraphExec_t e = nullptr;
@@ -371,7 +413,8 @@ tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const flo
     }
     cur = (chunk % 2 == 0) ? o.Ya : o.Yb;
     done += chunk;
-    if (done < n_iter && t0 + done >= kMortonFrom) {
+    if (done < n_iter && t0 + done >= kMortonFrom &&
+        morton_improves(o.rp[h], o.col[h], w.perm, N, o, s)) {
       // chunks are even, so the state is in Ya; w.perm is the Morton order of
       // the last iteration's embedding (a permutation of the current labels).
       // The pending recentring shift is uniform, so it commutes with relabelling.
