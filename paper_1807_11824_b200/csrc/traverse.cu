@@ -64,10 +64,11 @@ __global__ void __launch_bounds__(kBucketThreads)
 k_bucket_pairs(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
                const float2* __restrict__ ys, const int32_t* __restrict__ leafnode, int N,
                const int32_t* __restrict__ list, const int32_t* __restrict__ nlist,
-               BucketSum* __restrict__ out) {
+               const int32_t* __restrict__ has_bucket, BucketSum* __restrict__ out) {
   const int tid = blockIdx.x * kBucketThreads + threadIdx.x;
   const bool active = tid < (list ? *nlist : N);
   const int k = active ? (list ? list[tid] : tid) : -1;
+  if (!*has_bucket) return;                         // no bucket in this tree (k_traverse knows)
   int s0 = -1, cnt = 0;
   float2 yi = make_float2(0.f, 0.f);
   if (active) {
@@ -151,7 +152,7 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            float theta, float2* __restrict__ rep, double* __restrict__ zpart,
            unsigned* __restrict__ counter, double* __restrict__ Zout,
            const int32_t* __restrict__ list, const int32_t* __restrict__ nlist, int row0,
-           const BucketSum* __restrict__ bsum) {
+           const BucketSum* __restrict__ bsum, const int32_t* __restrict__ has_bucket) {
   constexpr bool stats = STATS;
   // list (multi-GPU): the sorted positions of the points this rank owns
   // (original indices [row0, ...)); rep is then indexed by perm[k] - row0.
@@ -288,10 +289,12 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
     }
   }
   if (active) {
-    const BucketSum b = bsum[k];
-    fx += b.f.x;
-    fy += b.f.y;
-    z += b.z;
+    if (*has_bucket) {
+      const BucketSum b = bsum[k];
+      fx += b.f.x;
+      fy += b.f.y;
+      z += b.z;
+    }
     rep[perm[k] - row0] = make_float2(fx, fy);
   }
   if (stats) {
@@ -351,7 +354,8 @@ static tsne_status launch_bucket_pairs(TreeWS& w, const int32_t* list, const int
   const int N = (int)w.N;
   // the fixed-point coordinates are dead after the tree build: reuse them
   k_bucket_pairs<<<(N + kBucketThreads - 1) / kBucketThreads, kBucketThreads, 0, s>>>(
-      w.nodes, w.nfirst, w.ys, w.leafnode, N, list, nlist, reinterpret_cast<BucketSum*>(w.fq));
+      w.nodes, w.nfirst, w.ys, w.leafnode, N, list, nlist, w.has_bucket,
+      reinterpret_cast<BucketSum*>(w.fq));
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }
@@ -364,11 +368,11 @@ tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s) {
   if (trav_stats_on())
     k_traverse<true><<<traverse_blocks(N), kTravThreads, 0, s>>>(
         w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
-        w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0, bs);
+        w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0, bs, w.has_bucket);
   else
     k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
         w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
-        w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0, bs);
+        w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0, bs, w.has_bucket);
   TSNE_LAUNCH_CHECK();
   if (trav_stats_on()) {
     unsigned long long h[5];
@@ -391,7 +395,7 @@ tsne_status launch_traverse_list(TreeWS& w, float theta, const int32_t* list, co
   k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta,
       rep_local, w.zpart, w.counter + 1, z_partial, list, nlist, row0,
-      reinterpret_cast<const BucketSum*>(w.fq));
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }

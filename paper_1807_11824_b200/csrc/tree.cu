@@ -75,6 +75,7 @@ void carve_tree(Carver& c, TreeWS& w, int64_t N) {
   w.com64 = c.take<double2>(2 * N);
   w.leafnode = c.take<int32_t>(N);
   w.box = c.take<BoxInfo>(2);
+  w.has_bucket = c.take<int32_t>(1);
   w.rep = c.take<float2>(N);
   w.zpart = c.take<double>(traverse_blocks(N));
   w.Z = c.take<double>(2);
@@ -231,10 +232,11 @@ __device__ __forceinline__ uint32_t quantise(float y, double lo, double s) {
 // so the attractive pass may read Y concurrently.
 __global__ void k_keys(const float2* __restrict__ Y, int N, const BoxInfo* __restrict__ box,
                        int apply_shift, uint64_t* __restrict__ keys, int32_t* __restrict__ vals,
-                       int32_t* __restrict__ cnt) {
+                       int32_t* __restrict__ cnt, int32_t* __restrict__ has_bucket) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i > N) return;
   cnt[i] = 0;
+  if (i == 0) *has_bucket = 0;
   if (i == N) return;
   const BoxInfo b = *box;
   float2 y = Y[i];
@@ -435,7 +437,8 @@ __global__ void k_quad_emit(int N, const int32_t* __restrict__ bfirst,
                             const int32_t* __restrict__ base, const float2* __restrict__ ys,
                             const longlong2* __restrict__ S, const BoxInfo* __restrict__ box,
                             float4* __restrict__ nodes, int32_t* __restrict__ nfirst,
-                            double2* __restrict__ com64, int32_t* __restrict__ leafnode) {
+                            double2* __restrict__ com64, int32_t* __restrict__ leafnode,
+                            int32_t* __restrict__ has_bucket) {
   int id = blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= 2 * N - 1) return;
   int r = rank[id];
@@ -472,8 +475,10 @@ __global__ void k_quad_emit(int N, const int32_t* __restrict__ bfirst,
     double my = __ddiv_rn(__dmul_rn((double)(a.y - b.y), sc), (double)count);
     c64 = make_double2(__dadd_rn(box->cx, mx), __dadd_rn(box->cy, my));
     cxf = (float)c64.x; cyf = (float)c64.y;
-    if (level >= kLevelLeaf)
+    if (level >= kLevelLeaf) {
       for (int k = s; k <= e; ++k) leafnode[k] = pre;
+      atomicOr(has_bucket, 1);
+    }
   }
   nodes[pre] = make_float4(cxf, cyf, (float)count,
                            __uint_as_float((uint32_t)skip | ((uint32_t)level << 27)));
@@ -487,7 +492,8 @@ static inline int cdiv(int64_t a, int b) { return (int)((a + b - 1) / b); }
 tsne_status build_tree(TreeWS& w, const float2* Y, bool apply_shift, cudaStream_t s) {
   const int N = (int)w.N;
   const int T = 256;
-  k_keys<<<cdiv(N + 1, T), T, 0, s>>>(Y, N, w.box, apply_shift ? 1 : 0, w.keys_a, w.vals_a, w.cnt);
+  k_keys<<<cdiv(N + 1, T), T, 0, s>>>(Y, N, w.box, apply_shift ? 1 : 0, w.keys_a, w.vals_a, w.cnt,
+                                      w.has_bucket);
   TSNE_LAUNCH_CHECK();
   cub::DoubleBuffer<uint64_t> dk(w.keys_a, w.keys_b);
   cub::DoubleBuffer<int32_t> dv(w.vals_a, w.vals_b);
@@ -510,7 +516,7 @@ tsne_status build_tree(TreeWS& w, const float2* Y, bool apply_shift, cudaStream_
   TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.scan2_tmp, c2, w.cnt, w.base, N + 1, s));
   k_quad_emit<<<cdiv(2 * N - 1, T), T, 0, s>>>(N, w.bfirst, w.blast, w.bdelta, w.bparent, w.rank,
                                                 w.base, w.ys, w.S, w.box, w.nodes, w.nfirst,
-                                                w.com64, w.leafnode);
+                                                w.com64, w.leafnode, w.has_bucket);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }

@@ -59,6 +59,7 @@ struct TreeWS {
   int32_t* nfirst = nullptr;
   double2* com64 = nullptr;
   int32_t* leafnode = nullptr; // N, indexed by sorted position
+  int32_t* has_bucket = nullptr; // 1 if the last tree has a bucket (several points in a leaf)
   BoxInfo* box = nullptr;
   float2* rep = nullptr;       // N repulsive numerators f_i (original order)
   double* zpart = nullptr;     // per traversal block
