@@ -23,19 +23,21 @@ constexpr int kAttrWarps = kAttrThreads / 32;
 // ---------------------------------------------------------------- H7
 // Attractive pass as a persistent TMA pipeline (one CTA per SM).  The CTA
 // owns a contiguous range of rows, cut into batches of at most kAtRows rows
-// whose nonzeros fit a stage buffer.  A
-// producer warp streams each batch's col/val span (contiguous in the CSR)
-// into a kAtStages-deep shared-memory ring with cp.async.bulk + mbarriers
-// (the bulk copies keep ~3 batches of the 8-byte-per-nonzero stream in flight
-// per SM without holding registers); the embedding window
-// Y[wlo, wlo + kAtWin) around the CTA's rows is staged once the same way.
-// Two groups of kAtRows consumer warps take alternate batches (latency hiding
-// for the L2 gathers); warp w of a group computes row w of its batches: lanes take consecutive
-// nonzeros from shared memory, gather y_j from the window (columns outside it,
-// rare once the labels are in a locality order -- DESIGN.md 6.4-6.5 -- come
-// from L2), and reduce with a fixed butterfly (deterministic; the result does
-// not depend on which path an operand came from).  A batch whose span does
-// not fit a stage buffer is read from global memory directly.
+// whose nonzeros fit a stage buffer.  A producer warp streams each batch's
+// col/val span (contiguous in the CSR) into a kAtStages-deep shared-memory
+// ring with cp.async.bulk + mbarriers (the bulk copies keep ~3 batches of the
+// 8-byte-per-nonzero stream in flight per SM without holding registers); the
+// embedding window Y[wlo, wlo + kAtWin) around the CTA's rows is staged once
+// the same way.  Two groups of kAtRows consumer warps take alternate batches
+// (latency hiding for the L2 gathers); warp w of a group computes row w of
+// its batches: lanes take consecutive nonzeros from shared memory, gather y_j
+// from the window (columns outside it, rare once the labels are in a locality
+// order -- DESIGN.md 6.4-6.5 -- come from L2), and reduce with a fixed
+// butterfly (deterministic; the result does not depend on which path an
+// operand came from).  A batch whose span does not fit a stage buffer is read
+// from global memory directly; rows of more than kAtLong nonzeros go to
+// k_attract_long.  The sizes below are the measured best of the variants in
+// DESIGN.md 6.4 (overridable at compile time for such experiments).
 #ifndef TSNE_AT_ROWS
 #define TSNE_AT_ROWS 15
 #define TSNE_AT_GROUPS 2
