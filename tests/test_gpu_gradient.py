@@ -163,3 +163,21 @@ def test_long_uniform_rows(T, orc):
     g2, _ = gpu_grad(T, rp, col, v32, Y, 0.5, 2.0)
     A = orc.attractive(rp, col, v32, Y)
     assert rel((g2 - g1) / 4.0, A) <= 1e-5
+
+
+@pytest.mark.parametrize("name", ["five_point_theta05", "half_side_theta05"])
+def test_hand_worked_goldens(T, name):
+    """The GPU path on the hand-worked goldens (tests/golden): query point 0 has
+    no attractive term (its CSR row is empty), so dY_0 = -4 f_0 / Z (Eq. 6-7);
+    the half-side golden separates D7's half-side reading from the full-side
+    and geometric-centre readings."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", name + ".json")))
+    Y = np.array(g["points"], np.float32)
+    rp = np.array([0, 0, 0, 0, 1, 2], np.int64)
+    col = np.array([4, 3], np.int32)
+    val = np.array([0.5, 0.5], np.float32)
+    dY, Z = gpu_grad(T, rp, col, val, Y, g["theta"], 1.0)
+    f0 = -dY[0].astype(np.float64) * Z / 4.0
+    np.testing.assert_allclose(f0, g["bh"]["f0"], rtol=2e-6)

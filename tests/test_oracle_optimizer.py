@@ -83,3 +83,70 @@ def test_nn_preservation_identity(orc):
     Y = synth.fixed_y("gauss10", 300, seed=1)
     idx, _ = orc.knn(Y, 10)
     assert orc.nn_preservation(idx, Y.astype(np.float64), 10) == 1.0
+
+
+def _two_point_grad(Y, alpha, p):
+    """Closed form of Eq. 7 for N = 2 with P_12 = P_21 = p (Eqs. 4-6 by hand):
+    w = 1/(1 + |y1 - y2|^2), Z = 2w, A_1 = p w (y1 - y2), F_rep,1 = -w^2 (y1 - y2) / Z
+    -> g_1 = 4 w (alpha p - 1/2) (y1 - y2), g_2 = -g_1."""
+    d = Y[0] - Y[1]
+    w = 1.0 / (1.0 + d @ d)
+    g1 = 4.0 * w * (alpha * p - 0.5) * d
+    return np.array([g1, -g1])
+
+
+def test_two_steps_across_exaggeration_switch(orc):
+    """O9-O10 pinned across t = 249 -> 250 (D12, D13): the step at t = 249
+    uses alpha = exag and mu = mom0, the step at t = 250 alpha = 1 and mu = mom1;
+    both gain branches (signs differ -> +0.2, same sign -> x0.8, sign(0) = 0), the
+    min_gain floor, v != 0, and the recentring are exercised.  Fails under
+    `t <= exag_iters`, swapped momenta, swapped gain branches or a missing floor
+    (each checked by a temporary mutation of the oracle)."""
+    p, eta, exag, mom0, mom1, floor_ = 0.25, 0.01, 12.0, 0.5, 0.8, 0.01
+    rp, col, val = np.array([0, 1, 2]), np.array([1, 0]), np.array([p, p], np.float32)
+    Y0 = np.array([[-0.75, 0.0], [0.5, 0.0]])
+    v0 = np.array([[0.3, 0.0], [0.1, 0.0]])
+    g0 = np.array([[1.0, 0.011], [0.5, 0.011]])
+    # expected, by the rule written out
+    Y, v, gains = Y0.copy(), v0.copy(), g0.copy()
+    branches = set()
+    for t in (249, 250):
+        alpha, mu = (exag, mom0) if t < 250 else (1.0, mom1)
+        g = _two_point_grad(Y, alpha, p)
+        for a in range(2):
+            for c in range(2):
+                differ = np.sign(g[a, c]) != np.sign(v[a, c])
+                branches.add((t, bool(differ)))
+                gn = gains[a, c] + 0.2 if differ else gains[a, c] * 0.8
+                gains[a, c] = max(gn, floor_)
+                v[a, c] = mu * v[a, c] - eta * gains[a, c] * g[a, c]
+                Y[a, c] = Y[a, c] + v[a, c]
+        Y -= Y.mean(0)
+    assert branches == {(249, True), (249, False), (250, True), (250, False)}
+    assert gains[0, 1] == floor_ and gains[1, 1] == floor_
+    Yo, vo, go = orc.optimize(rp, col, val, Y0, v0, g0, t0=249, n_iter=2, theta=0.5, eta=eta,
+                              exaggeration=exag, exag_iters=250, mom0=mom0, mom1=mom1,
+                              min_gain=floor_)
+    np.testing.assert_allclose(go, gains, rtol=1e-14)
+    np.testing.assert_allclose(vo, v, rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(Yo, Y, rtol=1e-12, atol=1e-15)
+
+
+def test_nn_preservation_hand_example(orc):
+    """O12 10-NN preservation on a hand-worked case with value != 1:
+    mean_i |NN_k^X(i) & NN_k^Y(i)| / k, NN^Y a brute-force 2-D kNN excluding i,
+    ties by index, NN^X the first k entries of rows of stride Kx.
+    Y on a line: 0, 1, 3, 3, 10 (points 2 and 3 coincide).  k = 2:
+      NN^Y(0) = {1, 2}  (d 1; d 9 tie with 3 -> lower index 2)
+      NN^Y(1) = {0, 2}  (d 1, 4; tie 2/3 -> 2)
+      NN^Y(2) = {3, 1}  (d 0, 4)
+      NN^Y(3) = {2, 1}  (d 0, 4)
+      NN^Y(4) = {2, 3}  (d 49, 49)
+    NN^X rows (first 2 of 3): {1,3}, {0,3}, {4,0}, {2,1}, {0,1}
+    overlaps 1, 1, 0, 2, 0 -> (1+1+0+2+0) / (5*2) = 0.4 (ties taken by the higher
+    index would give 2, 2, 0, 2, 0 -> 0.6; i counted as its own neighbour, less)."""
+    Y = np.array([[0, 0], [1, 0], [3, 0], [3, 0], [10, 0]], np.float64)
+    idx_x = np.array([[1, 3, 4], [0, 3, 4], [4, 0, 1], [2, 1, 0], [0, 1, 2]], np.int32)
+    assert abs(orc.nn_preservation(idx_x, Y, 2) - 0.4) < 1e-15
+    # k = 1: NN^Y = 1, 0, 3, 2, 2; NN^X = 1, 0, 4, 2, 0 -> 3/5
+    assert abs(orc.nn_preservation(idx_x, Y, 1) - 0.6) < 1e-15

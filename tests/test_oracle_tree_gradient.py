@@ -53,6 +53,21 @@ def test_five_point_hand_example(orc):
     np.testing.assert_allclose(f0[0], g["exact"]["f0"], rtol=1e-14)
 
 
+def test_half_side_hand_example(orc):
+    """D7 pinned: r_cell is HALF the side.  The decisive cell has r_half/D =
+    0.257 in [0.25, 0.5), so the full-side reading (and the geometric-centre
+    reading) give different z0, f0 -- hand-worked in tests/golden."""
+    g = json.load(open(os.path.join(GOLD, "half_side_theta05.json")))
+    Y = np.array(g["points"], np.float32)
+    f, z, Z, st = orc.repulsive_bh(Y, g["theta"])
+    assert abs(z[0] - g["bh"]["z0"]) <= 1e-15
+    np.testing.assert_allclose(f[0], g["bh"]["f0"], rtol=1e-14)
+    assert abs(z[0] - g["full_side_reading"]["z0"]) > 1e-3      # the readings are told apart
+    f0, z0, _, _ = orc.repulsive_bh(Y, 0.0)
+    assert abs(z0[0] - g["exact"]["z0"]) <= 1e-15
+    np.testing.assert_allclose(f0[0], g["exact"]["f0"], rtol=1e-14)
+
+
 def test_tree_invariants_unit_square(orc):
     # S:L256 unit-square corners: root count 4, COM (0.5, 0.5), four children of count 1
     Y = np.array([[0, 0], [0, 1], [1, 0], [1, 1]], np.float32)
