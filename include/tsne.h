@@ -73,15 +73,20 @@ int32_t tsne_abi_version(void);
  *        (d2, index) -- ties broken by the lower index (D18).
  *   d2   [N x K] float64 out: exact squared Euclidean distances (D19).
  * Requires N >= 2, 1 <= K < N, D >= 1.
+ * Exactness (D26): a row is accepted from its K' candidates only if an
+ * a-priori error bound of the fp16 / fp32 candidate distances, valid for
+ * EVERY point of the data set (element rounding 2^-11, norm and FFMA
+ * rounding 2^-24, fp32 accumulation Dp 2^-22 |x_i||x_j|), proves that no
+ * non-candidate can be nearer than the K-th re-ranked neighbour; rows it
+ * cannot certify are recomputed by an exact fp64 scan of all N points.
  * `info` (HOST, nullable): when non-NULL the call synchronises `stream` and
- * reports how many rows failed the candidate-margin certificate (D26) and
- * were recomputed by the exact fallback scan.
+ * reports how many rows failed the certificate and were rescanned.
  * ------------------------------------------------------------------------ */
 typedef struct {
   int64_t rows_uncertified;  /* rows re-done by the exact fallback scan      */
   int32_t candidates;        /* K' used                                       */
   int32_t gemm_path;         /* 2 = tcgen05 symmetric search, 1 = tcgen05 row
-                                sweep, 0 = CUDA-core                         */
+                                sweep (CTA pairs)                            */
 } tsne_knn_info;
 
 size_t tsne_knn_workspace_size(int64_t N, int32_t D, int32_t K);
@@ -114,7 +119,8 @@ tsne_status tsne_knn_rows(const float* X, int64_t N, int32_t D, int32_t K,
  *             diagonal; val[(i,j)] == val[(j,i)] bitwise; sum(val) = 1.
  *   nnz_out   HOST out: number of nonzeros (this call synchronises stream).
  *   beta_out  [N] float64 out (nullable): 1/(2 sigma_i^2).
- * Requires 1 < perplexity < K.  Returns TSNE_ERR_DEGENERATE (outputs valid)
+ * Requires 1 < perplexity < K and 2 N K < 2^31 (the directed edges of the
+ * symmetrisation are indexed in int32), else TSNE_ERR_ARG.  Returns TSNE_ERR_DEGENERATE (outputs valid)
  * if some row had no finite root -- all neighbours equidistant (uniform over
  * K) or >= perplexity ties at the minimum (uniform over the ties) (D3).
  * ------------------------------------------------------------------------ */
@@ -141,13 +147,16 @@ tsne_status tsne_compute_p(const int32_t* idx, const double* d2, int64_t N, int3
  * pairwise, D9), decided as in fp64 (D25).
  *
  *   row_ptr/col/val  CSR of P as produced by tsne_compute_p; col and val
- *             must be 16-byte aligned (they are streamed as 16-byte vectors),
- *             Y and dY 8-byte aligned, else TSNE_ERR_ARG.
+ *             must be 16-byte aligned (they are streamed by bulk copies),
+ *             Y 16-byte aligned (a window of it is staged by bulk copies)
+ *             and dY 8-byte aligned, else TSNE_ERR_ARG.
  *   Y     [N x 2] float32 (x,y interleaved), finite.
  *   dY    [N x 2] float32 out.
  *   Z_out HOST out (nullable): Z; when non-NULL the call synchronises.
- * Requires N >= 2, theta >= 0 (theta == 0 is the exact O(N^2) sum),
- * exaggeration > 0.
+ * Requires 2 <= N < 2^25 (the node index fits 27 bits and the fixed-point
+ * centre-of-mass sums fit int64; the same limit holds for every entry point
+ * that builds the quadtree), theta >= 0 (theta == 0 is the exact O(N^2) sum,
+ * P:L130), exaggeration > 0.
  * ------------------------------------------------------------------------ */
 size_t tsne_gradient_workspace_size(int64_t N);
 tsne_status tsne_gradient(const int64_t* row_ptr, const int32_t* col, const float* val,
@@ -246,7 +255,8 @@ tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, 
  *      rep_local[i - row0] = f_i, z_partial[0] = sum over owned i of z_i
  *      (z_partial: 2 doubles, DEVICE).  Y is NOT modified.
  *   1'. tsne_shard_attract (may run concurrently with 1 on another stream:
- *      it only reads Y): A_local[i - row0] = sum_j P_ij (y_i - y_j) q_ij Z.
+ *      it only reads Y; Y 16-byte aligned): A_local[i - row0] =
+ *      sum_j P_ij (y_i - y_j) q_ij Z.
  *   2. caller: all-gather the ranks' z_partial pairs (NCCL) -> z_partials
  *      [world x 2] DEVICE, in rank order.
  *   3. tsne_shard_update (same workspace as 1): Eq. 7 with Z = sum_r
@@ -282,11 +292,13 @@ tsne_status tsne_init_y(int64_t N, uint64_t seed, float* Y, tsne_stream_t stream
  *   X      [N x D] float32, HOST or DEVICE (detected); finite.
  *   Y_out  [N x 2] float32, HOST or DEVICE (detected).
  * The only allocating entry points: device memory for the whole pipeline
- * is allocated with cudaMallocAsync on an internal stream and released
- * before return.  Blocking.  Exaggeration lasts 250 iterations, momentum
+ * is allocated with one cudaMalloc (measured: it maps tens of GB in
+ * milliseconds where the stream-ordered pool took seconds) and released with
+ * cudaFree before return; the work runs on an internal stream.  Blocking.  Exaggeration lasts 250 iterations, momentum
  * 0.5 -> 0.8, Y0 from Philox seed 42 (see tsne_config for _ex).
  * Requires N >= 2, 1 < perplexity < K, theta >= 0, learning_rate > 0,
- * n_iter >= 1, exaggeration >= 1.  Non-finite X -> TSNE_ERR_ARG.
+ * n_iter >= 1, exaggeration >= 1, 2 <= N < 2^25, 2 N K < 2^31.
+ * Non-finite X -> TSNE_ERR_ARG.
  * ------------------------------------------------------------------------ */
 tsne_status tsne_run(const float* X, int64_t N, int32_t D, float perplexity, float theta,
                      float learning_rate, int32_t n_iter, float exaggeration, float* Y_out);

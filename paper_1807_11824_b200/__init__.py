@@ -163,7 +163,7 @@ def knn(X: torch.Tensor, K: int, rows=None):
         _check(lib().tsne_knn_rows(_ptr(X), N, D, K, q0, q1 - q0, _ptr(idx), _ptr(d2), _ptr(ws),
                                    ws.numel(), C.byref(info), _stream()), "tsne_knn_rows")
     return idx, d2, {"rows_uncertified": info.rows_uncertified, "candidates": info.candidates,
-                     "gemm_path": {2: "tcgen05-sym", 1: "tcgen05"}.get(info.gemm_path, "cuda-core")}
+                     "gemm_path": {2: "tcgen05-sym", 1: "tcgen05"}[info.gemm_path]}
 
 
 # ---------------------------------------------------------------- U2 + U3

@@ -133,13 +133,13 @@ tsne_status tsne_gradient(const int64_t* row_ptr, const int32_t* col, const floa
                           const float* Y, float theta, float exaggeration, float* dY,
                           double* Z_out, void* ws, size_t ws_bytes, tsne_stream_t stream) {
   clear_error();
-  TSNE_ARG_CHECK(N >= 2 && N < (int64_t(1) << 27), "N must be in [2, 2^27) (got %lld)",
+  TSNE_ARG_CHECK(N >= 2 && N <= kMaxTreePoints, "N must be in [2, 2^25) (got %lld)",
                  (long long)N);
   TSNE_ARG_CHECK(row_ptr && col && val && Y && dY, "null pointer argument");
   TSNE_ARG_CHECK(theta >= 0.f && std::isfinite(theta), "theta must be >= 0 (got %g)", theta);
   TSNE_ARG_CHECK(exaggeration > 0.f && std::isfinite(exaggeration), "exaggeration must be > 0");
-  TSNE_ARG_CHECK(aligned(Y, 8) && aligned(dY, 8) && aligned(col, 16) && aligned(val, 16),
-                 "Y, dY need 8-byte and col, val 16-byte alignment");
+  TSNE_ARG_CHECK(aligned(Y, 16) && aligned(dY, 8) && aligned(col, 16) && aligned(val, 16),
+                 "Y, col, val need 16-byte and dY 8-byte alignment");
   GradPlan p;
   size_t need = grad_plan(nullptr, N, p);
   if (!ws || ws_bytes < need) {
@@ -219,7 +219,7 @@ tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const floa
   tsne_config cfg;
   tsne_config_default(&cfg);
   if (cfg_in) cfg = *cfg_in;
-  TSNE_ARG_CHECK(N >= 2 && N < (int64_t(1) << 27), "N must be in [2, 2^27)");
+  TSNE_ARG_CHECK(N >= 2 && N <= kMaxTreePoints, "N must be in [2, 2^25) (got %lld)", (long long)N);
   TSNE_ARG_CHECK(row_ptr && col && val && Y && v && gains, "null pointer argument");
   TSNE_ARG_CHECK(theta >= 0.f && std::isfinite(theta), "theta must be >= 0");
   TSNE_ARG_CHECK(learning_rate > 0.f, "learning_rate must be > 0");
@@ -275,7 +275,7 @@ tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, 
   tsne_config cfg;
   tsne_config_default(&cfg);
   if (cfg_in) cfg = *cfg_in;
-  TSNE_ARG_CHECK(N >= 2 && N < (int64_t(1) << 27), "N must be in [2, 2^27)");
+  TSNE_ARG_CHECK(N >= 2 && N <= kMaxTreePoints, "N must be in [2, 2^25) (got %lld)", (long long)N);
   TSNE_ARG_CHECK(row_ptr && col && val && Y && v && gains && stage_ms, "null pointer argument");
   TSNE_ARG_CHECK(reps >= 1 && t0 >= 0, "reps must be >= 1");
   tsne_status st = check_device();
@@ -313,7 +313,7 @@ tsne_status tsne_shard_forces(const float* Y, int64_t N, int64_t row0, int64_t r
                               int32_t recentre, float* rep_local, double* z_partial, void* ws,
                               size_t ws_bytes, tsne_stream_t stream) {
   clear_error();
-  TSNE_ARG_CHECK(N >= 2 && N < (int64_t(1) << 27), "N must be in [2, 2^27)");
+  TSNE_ARG_CHECK(N >= 2 && N <= kMaxTreePoints, "N must be in [2, 2^25) (got %lld)", (long long)N);
   TSNE_ARG_CHECK(0 <= row0 && row0 <= row1 && row1 <= N, "bad row range [%lld, %lld)",
                  (long long)row0, (long long)row1);
   TSNE_ARG_CHECK(Y && z_partial && (rep_local || row1 == row0), "null pointer argument");
@@ -338,9 +338,11 @@ tsne_status tsne_shard_attract(const int64_t* row_ptr_local, const int32_t* col_
                                const float* val_local, int64_t N, int64_t row0, int64_t row1,
                                const float* Y, float* A_local, tsne_stream_t stream) {
   clear_error();
-  TSNE_ARG_CHECK(N >= 2 && 0 <= row0 && row0 <= row1 && row1 <= N, "bad row range");
+  TSNE_ARG_CHECK(N >= 2 && N <= kMaxTreePoints, "N must be in [2, 2^25) (got %lld)", (long long)N);
+  TSNE_ARG_CHECK(0 <= row0 && row0 <= row1 && row1 <= N, "bad row range");
   TSNE_ARG_CHECK(Y && (row1 == row0 || (row_ptr_local && col_local && val_local && A_local)),
                  "null pointer argument");
+  TSNE_ARG_CHECK(aligned(Y, 16), "Y must be 16-byte aligned (bulk copies of its window)");
   TSNE_ARG_CHECK(row1 == row0 || (aligned(col_local, 16) && aligned(val_local, 16)),
                  "col and val must be 16-byte aligned");
   tsne_status st = check_device();
@@ -486,6 +488,8 @@ tsne_status tsne_compute_p(const int32_t* idx, const double* d2, int64_t N, int3
   TSNE_ARG_CHECK(perplexity > 1.f && perplexity < (float)K,
                  "perplexity must satisfy 1 < perplexity < K (got %g, K=%d)", perplexity, K);
   TSNE_ARG_CHECK(idx && d2 && row_ptr && col && val && nnz_out, "null pointer argument");
+  TSNE_ARG_CHECK(2 * N * (int64_t)K < (int64_t(1) << 31),
+                 "2 N K must be < 2^31 (directed edges of the symmetrisation, int32 positions)");
   PWS w;
   Carver c0(nullptr);
   carve_p(c0, w, N, K);
@@ -515,7 +519,7 @@ tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, 
   tsne_config cfg;
   tsne_config_default(&cfg);
   if (cfg_in) cfg = *cfg_in;
-  TSNE_ARG_CHECK(N >= 2 && N < (int64_t(1) << 27), "N must be in [2, 2^27)");
+  TSNE_ARG_CHECK(N >= 2 && N <= kMaxTreePoints, "N must be in [2, 2^25) (got %lld)", (long long)N);
   TSNE_ARG_CHECK(D >= 1, "D must be >= 1");
   TSNE_ARG_CHECK(X && Y_out, "null pointer argument");
   int32_t K = cfg.K > 0 ? cfg.K : (int32_t)std::floor(3.0 * (double)perplexity);
@@ -527,6 +531,8 @@ tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, 
   TSNE_ARG_CHECK(learning_rate > 0.f, "learning_rate must be > 0");
   TSNE_ARG_CHECK(n_iter >= 1, "n_iter must be >= 1");
   TSNE_ARG_CHECK(exaggeration >= 1.f, "exaggeration must be >= 1");
+  TSNE_ARG_CHECK(2 * N * (int64_t)K < (int64_t(1) << 31),
+                 "2 N K must be < 2^31 (directed edges of the symmetrisation, int32 positions)");
   tsne_status st = check_device();
   if (st != TSNE_OK) return st;
 

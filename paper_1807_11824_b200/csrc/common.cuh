@@ -54,6 +54,11 @@ inline bool aligned(const void* p, size_t a) {
 
 constexpr int kNumSMs = 148;
 
+// Largest N of the entry points that build the quadtree: the fixed-point
+// centre-of-mass sums hold count * 2^38 < 2^63 (|q| < 2^38 per point) (tree.cuh kFixScale) and the
+// node index (< 2N) fits the 27-bit skip field of a node record.
+constexpr int64_t kMaxTreePoints = (int64_t(1) << 25) - 1;
+
 // ---------------------------------------------------------------- device
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -57,8 +57,10 @@ void carve_knn(Carver& c, KnnWS& w, int64_t N, int32_t D, int32_t K) {
   w.cand = c.take<u64>((size_t)N * w.Kc);
   w.uncert = c.take<u64>(2);
   w.rows_bad = c.take<int32_t>(N);
-  w.sync = c.take<unsigned>(knn_tc_sync_words(N, N) > knn_tc2_sync_words(N, N) ? knn_tc_sync_words(N, N)
-                                                                           : knn_tc2_sync_words(N, N));
+  {
+    const size_t a = knn_tc2_sync_words(N, N), b = knn_sym_sync_words(N);
+    w.sync = c.take<unsigned>(a > b ? a : b);
+  }
   w.sd = c.take<double>((size_t)kScanRows * N);
   w.sd_alt = c.take<double>(N);
   w.si = c.take<int32_t>(N);
@@ -113,7 +115,7 @@ __global__ void k_colsum_part(const float* __restrict__ X, int64_t N, int D,
 __global__ void k_colsum_final(const double* __restrict__ part, int64_t N, int D,
                                float* __restrict__ mean, unsigned* amax) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d == 0) *amax = 0u;
+  if (d == 0) { amax[0] = 0u; amax[1] = 0u; }
   if (d >= D) return;
   double s = 0.0;
   for (int b = 0; b < kColRB; ++b) s += part[(size_t)b * D + d];
@@ -162,130 +164,15 @@ __global__ void k_convert(const float* __restrict__ X, int64_t N, int D, int Dp,
   if (lane == 0) nrm[row] = row < N ? (float)acc : 0.f;
 }
 
-// ---------------------------------------------------------------- v1 candidates (CUDA cores)
-constexpr int kS_BN = 64, kS_BK = 32, kS_Threads = 256, kS_SortWarps = 8;
-
-struct SimtSmem {
-  float As[kS_BK][kKnnBM + 4];
-  float Bs[kS_BK][kS_BN + 4];
-  float tile[kKnnBM][kS_BN + 1];
-  u64 tau[kKnnBM];
-  int cnt[kKnnBM];
-  int flag;
-  u64 sortbuf[kS_SortWarps][kCandCap];
-};
-
-__global__ void __launch_bounds__(kS_Threads, 1)
-k_cand_simt(const __half* __restrict__ Xh, const float* __restrict__ nrm, int N, int qs, int nq,
-            int Dp, int Kc, u64* __restrict__ buf, u64* __restrict__ cand) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  SimtSmem& sm = *reinterpret_cast<SimtSmem*>(smraw);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int tx = tid & 15, ty = tid >> 4;
-  u64* mybuf = buf + (size_t)blockIdx.x * kKnnBM * kCandCap;
-  const int nrb = (nq + kKnnBM - 1) / kKnnBM;
-  for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
-    const int q0 = qs + rb * kKnnBM;                     // first global query row of the block
-    if (tid < kKnnBM) { sm.cnt[tid] = 0; sm.tau[tid] = kKeyMax; }
-    __syncthreads();
-    for (int c0 = 0; c0 < N; c0 += kS_BN) {
-      float acc[8][4];
-#pragma unroll
-      for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-      for (int k0 = 0; k0 < Dp; k0 += kS_BK) {
-        // A: 128 rows x 32 halves; each thread 16 halves (rows may exceed N: slack rows are 0)
-        {
-          const int r = tid >> 1, kk = (tid & 1) * 16;
-          const __half* src = Xh + (size_t)(q0 + r) * Dp + k0 + kk;
-          const uint4 v0 = *reinterpret_cast<const uint4*>(src);
-          const uint4 v1 = *reinterpret_cast<const uint4*>(src + 8);
-          const __half* h0 = reinterpret_cast<const __half*>(&v0);
-          const __half* h1 = reinterpret_cast<const __half*>(&v1);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            sm.As[kk + q][r] = __half2float(h0[q]);
-            sm.As[kk + 8 + q][r] = __half2float(h1[q]);
-          }
-        }
-        {
-          const int r = tid >> 2, kk = (tid & 3) * 8;
-          const __half* src = Xh + (size_t)(c0 + r) * Dp + k0 + kk;
-          const uint4 v0 = *reinterpret_cast<const uint4*>(src);
-          const __half* h0 = reinterpret_cast<const __half*>(&v0);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) sm.Bs[kk + q][r] = __half2float(h0[q]);
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int k = 0; k < kS_BK; ++k) {
-          float a[8], b[4];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) a[q] = sm.As[k][ty * 8 + q];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) b[q] = sm.Bs[k][tx * 4 + q];
-#pragma unroll
-          for (int p = 0; p < 8; ++p)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[p][q] = fmaf(a[p], b[q], acc[p][q]);
-        }
-        __syncthreads();
-      }
-#pragma unroll
-      for (int p = 0; p < 8; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int j = c0 + tx * 4 + q;
-          const float nj = (j < N) ? nrm[j] : 0.f;
-          sm.tile[ty * 8 + p][tx * 4 + q] = nj - 2.f * acc[p][q];
-        }
-      __syncthreads();
-      // offer: thread t owns query row q0 + t
-      if (tid < kKnnBM) {
-        const int q = q0 + tid;
-        if (q < qs + nq) {
-          int cnt = sm.cnt[tid];
-          const u64 tau = sm.tau[tid];
-          u64* rowbuf = mybuf + (size_t)tid * kCandCap;
-          const int cmax = min(kS_BN, N - c0);
-          for (int c = 0; c < cmax; ++c) {
-            const int j = c0 + c;
-            if (j == q) continue;
-            const u64 key = mkkey(sm.tile[tid][c], j);
-            if (key < tau) rowbuf[cnt++] = key;
-          }
-          sm.cnt[tid] = cnt;
-        }
-      }
-      if (tid == 0) sm.flag = 0;
-      __syncthreads();
-      if (tid < kKnnBM && sm.cnt[tid] > kCandCap - kS_BN) sm.flag = 1;
-      __syncthreads();
-      if (sm.flag) {
-        for (int r = wid; r < kKnnBM; r += kS_Threads / 32) {
-          if (sm.cnt[r] > kCandCap - kS_BN) {
-            u64 t;
-            const int keep = reduce_keys(mybuf + (size_t)r * kCandCap, sm.cnt[r], Kc,
-                                         kCandCap - kS_BN, sm.sortbuf[wid], lane, t);
-            if (lane == 0) { sm.cnt[r] = keep; sm.tau[r] = t; }
-            __syncwarp();
-          }
-        }
-        __syncthreads();
-      }
-    }
-    // final: every row -> its Kc best keys
-    for (int r = wid; r < kKnnBM; r += kS_Threads / 32) {
-      const int q = q0 + r;
-      if (q < qs + nq) {
-        u64 t;
-        compact_keys(mybuf + (size_t)r * kCandCap, sm.cnt[r], Kc, sm.sortbuf[wid], lane,
-                     cand + (size_t)(q - qs) * Kc, t);
-      }
-    }
-    __syncthreads();
-  }
+// max_j |x_h,j|^2 over the N points (float bits into amax[1]): the norm bound
+// of the D26 certificate
+__global__ void k_nrm_max(const float* __restrict__ nrm, int64_t N, unsigned* amax) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, nrm[i]);
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(amax + 1, __float_as_uint(m));  // non-negative
 }
 
 // ---------------------------------------------------------------- re-rank
@@ -297,7 +184,7 @@ k_rerank(const float* __restrict__ X, int N, int qs, int nq, int D, int K, int K
          const float* __restrict__ nrm, const float* __restrict__ scale,
          int32_t* __restrict__ idx, double* __restrict__ d2, u64* __restrict__ uncert,
          int32_t* __restrict__ rows_bad, int force_mod, const int32_t* __restrict__ perm,
-         const int32_t* __restrict__ inv) {
+         const int32_t* __restrict__ inv, const unsigned* __restrict__ amax, int Dp) {
   // perm / inv (nullable): the candidates are stored by locality position
   // (symmetric search) with locality-position indices in their keys
   __shared__ double s_d[kRR_Threads / 32][256];
@@ -315,7 +202,6 @@ k_rerank(const float* __restrict__ X, int N, int qs, int nq, int D, int K, int K
   const u64* ci = cand + (size_t)(perm ? w : il) * Kc;
   const double inv2 = (double)scale[1];
   const double nrm_i = (double)nrm[i];
-  double emax = 0.0;
   for (int c = 0; c < Kc; ++c) {
     const u64 key = ci[c];
     const int j = perm ? perm[key_idx(key)] : key_idx(key);
@@ -330,10 +216,10 @@ k_rerank(const float* __restrict__ X, int N, int qs, int nq, int D, int K, int K
       sd[c] = acc;
       sj[c] = j;
     }
-    const double approx = ((double)key_val(key) + nrm_i) * inv2;
-    emax = fmax(emax, fabs(approx - acc));
   }
-  const double tau_approx = ((double)key_val(ci[Kc - 1]) + nrm_i) * inv2;
+  // approximate (scaled) distance of the K'-th candidate: every point that is
+  // not a candidate has an approximate key >= this one
+  const double tau_scaled = (double)key_val(ci[Kc - 1]) + nrm_i;
   int P = 32;
   while (P < Kc) P <<= 1;
   for (int c = Kc + lane; c < P; c += 32) { sd[c] = DBL_MAX; sj[c] = 0x7fffffff; }
@@ -359,7 +245,29 @@ k_rerank(const float* __restrict__ X, int N, int qs, int nq, int D, int K, int K
   }
   if (lane == 0) {
     const bool all = (Kc >= N - 1);
-    bool cert = all || (sd[K - 1] < tau_approx - 2.0 * emax);
+    // D26 certificate, an a-priori bound valid for EVERY point j (not only the
+    // candidates).  In the scaled, centred units of the candidate stage
+    // (c = (x - mean) 2^e real, h = fp16(c)), approx_ij = |h_j|^2 - 2 h_i.h_j +
+    // |h_i|^2 with |h_k - c_k| <= u |c_k| + a per element (u = 2^-11 fp16
+    // rounding + 2^-23 for the fp32 centring; a = 2^-25, fp16 subnormals), so
+    //   | |h_i - h_j|^2 - |c_i - c_j|^2 | <= 2 |c_i - c_j| E1 + E1^2,
+    //   E1 = u (|c_i| + |c_j|) + 2 a sqrt(Dp);
+    // the computed key adds the fp32 rounding of the norms (2^-24 each), of
+    // the tensor-core dot product (<= Dp 2^-22 |h_i| |h_j|, a conservative
+    // model of fp32 accumulation) and of the FFMA (2^-24 |key|).  The error
+    // grows with the distance, so if a non-candidate j had exact d_ij <= d_(K),
+    // then approx_ij <= d_(K) + err(d_(K)) < tau: contradiction.  Hence
+    // certified iff tau > d_(K) + err(d_(K)), with the norm bound M of all
+    // points (amax[1]).
+    const double u = 0x1p-11 + 0x1p-23, a = 0x1p-25, sqD = sqrt((double)Dp);
+    const double M = (sqrt((double)__uint_as_float(amax[1]) * (1.0 + 0x1p-23)) + a * sqD) / (1.0 - u);
+    const double ni = (sqrt(nrm_i * (1.0 + 0x1p-23)) + a * sqD) / (1.0 - u);
+    const double E1 = u * (ni + M) + 2.0 * a * sqD;
+    const double dK = sd[K - 1] / inv2 * (1.0 + 1e-12);          // scaled exact d_(K)
+    const double G = 0x1p-24 * (M * M + ni * ni) + 2.0 * ((double)Dp * 0x1p-22) * ni * M +
+                     0x1p-24 * (M * M + 2.0 * ni * M);
+    const double bound = dK + 2.0 * sqrt(dK) * E1 + E1 * E1 + G;
+    bool cert = all || (tau_scaled > bound * (1.0 + 1e-12));
     if (force_mod > 0 && i % force_mod == 0) cert = false;   // test hook (fallback coverage)
     if (!cert) {
       const u64 pos = atomicAdd(uncert, 1ull);
@@ -675,46 +583,44 @@ tsne_status run_knn(const float* X, int64_t N, int32_t D, int32_t K, int64_t q0,
     k_convert<<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(X, N, D, Dp, w.mean, w.scale, w.Xh,
                                                             w.nrm);
     TSNE_LAUNCH_CHECK();
+    k_nrm_max<<<4 * kNumSMs, 256, 0, s>>>(w.nrm, N, w.amax);
+    TSNE_LAUNCH_CHECK();
   }
   TSNE_CUDA_TRY(cudaMemsetAsync(w.uncert, 0, 2 * sizeof(u64), s));
-  // TSNE_KNN_PATH=simt forces the CUDA-core candidate stage, =tc2 / =tc1 the
-  // row-by-row tensor-core sweeps, =sym the symmetric search (cross-checks).
-  // By default a full-N call uses the symmetric search (knn_sym.cu) where the
-  // tensor work dominates its list appends -- large N and D (measured: C5
-  // 1.28M x 2048 5.8 s -> 3.2 s; C2/C4 (D <= 784) are faster row by row)
+  // A full-N call uses the symmetric search (knn_sym.cu) where the tensor
+  // work dominates its list appends -- large N and D (measured: C5
+  // 1.28M x 2048 5.8 s -> 3.2 s; C2/C4 (D <= 784) are faster row by row);
+  // otherwise the CTA-pair row sweep (knn_tc2.cu).  Test hook:
+  // TSNE_KNN_PATH=tc2 / =sym forces one of the two (results are identical).
+  if (!knn_tc_available()) {
+    set_error("tcgen05 path unavailable (no sm_100 device or no cuTensorMapEncodeTiled)");
+    return TSNE_ERR_CUDA;
+  }
   const char* force = getenv("TSNE_KNN_PATH");
-  bool tc = knn_tc_available() && Dp % 64 == 0 && !(force && strcmp(force, "simt") == 0);
   const bool sym_default = N >= (int64_t(1) << 18) && Dp >= 1024;
-  const bool sym = tc && w.sym && q0 == 0 && nq == N &&
+  const bool sym = w.sym && q0 == 0 && nq == N &&
                    (force ? strcmp(force, "sym") == 0 : sym_default);
   if (sym) {
     tsne_status st = sym_candidates(N, w, s);
     if (st != TSNE_OK) return st;
-  } else if (tc) {
+  } else {
     tsne_status st = launch_cand_tc(w.Xh, w.nrm, (int)N, (int)q0, (int)nq, Dp, Kc, w.buf, w.cand, w.slots, w.sync, s);
     if (st != TSNE_OK) return st;
-  } else {
-    const size_t smem = sizeof(SimtSmem);
-    TSNE_CUDA_TRY(cudaFuncSetAttribute(k_cand_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-    k_cand_simt<<<w.slots, kS_Threads, smem, s>>>(w.Xh, w.nrm, (int)N, (int)q0, (int)nq, Dp, Kc,
-                                                   w.buf, w.cand);
-    TSNE_LAUNCH_CHECK();
   }
-  w.path = sym ? 2 : (tc ? 1 : 0);
+  w.path = sym ? 2 : 1;
   const char* fm = getenv("TSNE_KNN_FORCE_FALLBACK");      // test hook: every fm-th row
   const int force_mod = fm ? atoi(fm) : 0;
   k_rerank<<<(int)((nq + 7) / 8), kRR_Threads, 0, s>>>(X, (int)N, (int)q0, (int)nq, D, K, Kc,
                                                       w.cand, w.nrm, w.scale,
                                                      idx, d2, w.uncert, w.rows_bad, force_mod,
-                                                     sym ? w.perm : nullptr, sym ? w.inv : nullptr);
+                                                     sym ? w.perm : nullptr, sym ? w.inv : nullptr,
+                                                     w.amax, Dp);
   TSNE_LAUNCH_CHECK();
   // uncertified rows (D26): exact fp64 scan of the whole data set
   u64 h = 0;
   TSNE_CUDA_TRY(cudaMemcpyAsync(&h, w.uncert, sizeof(h), cudaMemcpyDeviceToHost, s));
   TSNE_CUDA_TRY(cudaStreamSynchronize(s));
-  const char* dbg = getenv("TSNE_KNN_DEBUG_NO_EPILOGUE");  // diagnostics: results invalid
-  if (h > 0 && !(dbg && atoi(dbg) != 0)) {
+  if (h > 0) {
     int32_t* rows = (int32_t*)malloc(h * sizeof(int32_t));
     if (!rows) {
       set_error("host allocation failed");

@@ -38,13 +38,11 @@ constexpr uint32_t P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;       // 32 KB
 constexpr uint32_t P_IDESC = (1u << 4) | ((uint32_t)(P_BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 constexpr size_t P_SMEM = 1024 + P_STAGES * P_STAGE_BYTES + 256 + 4 * P_CAP * 8;
 
-__device__ unsigned long long g_dbg_stats[4];   // diagnostics (TSNE_KNN_DEBUG_NO_EPILOGUE=5)
-
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_b,
            const float* __restrict__ nrm, int N, int q0, int nq, int Dp,
            int Kc, u64* __restrict__ buf, u64* __restrict__ cand, unsigned* __restrict__ sync,
-           int dbg_skip_epilogue, int self_excl, int win_tiles, const int32_t* __restrict__ qid) {
+           int self_excl, int win_tiles, const int32_t* __restrict__ qid) {
   // rows: queries q0 .. q0+nq-1 of the A map; columns: the N points of the B
   // map with norms nrm (the same point set as the rows when self_excl != 0);
   // win_tiles > 0 restricts each CTA pair to win_tiles column tiles around
@@ -199,12 +197,10 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
             nv[4 * u] = v.x; nv[4 * u + 1] = v.y; nv[4 * u + 2] = v.z; nv[4 * u + 3] = v.w;
           }
           tmem_wait_ld();
-          if (dbg_skip_epilogue == 1) continue;   // diagnostics: MMA pipeline alone
           // fast path: 2 instructions per distance (FFMA + FMNMX), no branches
           float mn = INFINITY;
 #pragma unroll
           for (int t = 0; t < 64; ++t) mn = fminf(mn, fmaf(-2.f, __uint_as_float(r[t]), nv[t]));
-          if (dbg_skip_epilogue == 2) { if (mn == 1234.5f) rowbuf[0] = 0; continue; }   // diagnostics
           if (!__any_sync(0xffffffffu, qok && mn <= tf)) continue;
           // slow path: the columns holding a candidate for some lane of the warp
           uint64_t m = 0;
@@ -215,10 +211,6 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
           const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)m);
           const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(m >> 32));
           uint64_t u = ((uint64_t)hi << 32) | lo;
-          if (dbg_skip_epilogue == 5 && lane == 0) {
-            atomicAdd(&g_dbg_stats[0], 1ull);
-            atomicAdd(&g_dbg_stats[1], (unsigned long long)__popcll(u));
-          }
           while (u) {                                    // warp-uniform loop over hit columns
             const int t = __ffsll((long long)u) - 1;
             u &= u - 1;
@@ -227,8 +219,7 @@ k_cand_tc2(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUt
             const int j = j0 + t;
             if ((m >> t) & 1) {
               const u64 key = mkkey(dist, j);
-              if (dbg_skip_epilogue == 3) { if (key == 0) rowbuf[0] = 0; }
-              else if (j < N && (j != q || !self_excl) && key < tau) rowbuf[cnt++] = key;
+              if (j < N && (j != q || !self_excl) && key < tau) rowbuf[cnt++] = key;
             }
           }
         }
@@ -286,20 +277,11 @@ tsne_status launch_cand_tc2(const CUtensorMap& map, const CUtensorMap& map_b, co
   int grid = 2 * (npairs < kNumSMs / 2 ? npairs : kNumSMs / 2);
   if (grid > slots) grid = slots & ~1;
   if (sync) TSNE_CUDA_TRY(cudaMemsetAsync(sync, 0, sizeof(unsigned) * knn_tc2_sync_words(N, nq), s));
-  const char* dbg = getenv("TSNE_KNN_DEBUG_NO_EPILOGUE");
   if (win_tiles > 0) sync = nullptr;          // pairs stream different tiles: no lockstep
   k_cand_tc2<<<grid, P_THREADS, P_SMEM, s>>>(map, map_b, nrm, N, q0, nq, Dp, Kc, buf, cand,
-                                              grid == kNumSMs ? sync : nullptr, dbg ? atoi(dbg) : 0,
+                                              grid == kNumSMs ? sync : nullptr,
                                               self_excl, win_tiles, qid);
   TSNE_LAUNCH_CHECK();
-  if (dbg && atoi(dbg) == 5) {
-    unsigned long long h[4];
-    TSNE_CUDA_TRY(cudaMemcpyFromSymbolAsync(h, g_dbg_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, s));
-    TSNE_CUDA_TRY(cudaStreamSynchronize(s));
-    const double chunks = (double)((nq + 31) / 32) * (double)((N + 63) / 64);
-    fprintf(stderr, "knn_tc2 stats: slow chunks %llu of %.0f (%.3f), hit columns %llu (%.2f per slow chunk)\n",
-            h[0], chunks, h[0] / chunks, h[1], h[1] / (double)(h[0] ? h[0] : 1));
-  }
   return TSNE_OK;
 }
 

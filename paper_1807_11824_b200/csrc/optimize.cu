@@ -200,6 +200,7 @@ struct DiffKey {
   const int32_t* col;
   const float* val;
   int64_t N, nnz;
+  uint64_t csr;    // fingerprint of the CSR's contents (the allocator may reuse addresses)
   uint64_t hash;
 };
 static std::mutex g_diff_mu;
@@ -207,7 +208,39 @@ static std::vector<DiffKey> g_diff_cache;
 
 static bool same_key(const DiffKey& a, const DiffKey& b) {
   return a.ws == b.ws && a.rp == b.rp && a.col == b.col && a.val == b.val && a.N == b.N &&
-         a.nnz == b.nnz;
+         a.nnz == b.nnz && a.csr == b.csr;
+}
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull;
+  return x ^ (x >> 33);
+}
+
+// order-independent 64-bit fingerprint of (row_ptr, col, val): a sum of mixed
+// (position, content) words, ~0.25 ms at C5
+__global__ void k_csr_hash(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                           const float* __restrict__ val, int64_t N, int64_t nnz,
+                           unsigned long long* __restrict__ out) {
+  unsigned long long h = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= N; k += stride)
+    h += mix64(((unsigned long long)k << 1) ^ ((unsigned long long)rp[k] * 0x9e3779b97f4a7c15ull));
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += stride)
+    h += mix64(((unsigned long long)e << 1 | 1ull) ^
+               (((unsigned long long)(uint32_t)__ldcs(col + e) << 32) |
+                __float_as_uint(__ldcs(val + e))));
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, h);
+}
+
+static bool csr_hash(const int64_t* rp, const int32_t* col, const float* val, int64_t N,
+                     int64_t nnz, const OptWS& o, uint64_t* h, cudaStream_t s) {
+  if (cudaMemsetAsync(o.dtag, 0, sizeof(uint64_t), s) != cudaSuccess) return false;
+  k_csr_hash<<<4 * kNumSMs, 256, 0, s>>>(rp, col, val, N, nnz, (unsigned long long*)o.dtag);
+  if (cudaGetLastError() != cudaSuccess) return false;
+  if (cudaMemcpyAsync(h, o.dtag, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return false;
+  return cudaStreamSynchronize(s) == cudaSuccess;
 }
 
 __global__ void k_perm_hash(const int32_t* __restrict__ perm, int N,
@@ -286,7 +319,11 @@ static tsne_status enter(const int64_t* row_ptr, const int32_t* col, const float
   const int32_t* perm = nullptr;
   if (morton) {
     if (t0 < kMortonFrom) {
-      const DiffKey key{o.ws_base, row_ptr, col, val, N, o.nnz, 0};
+      DiffKey key{o.ws_base, row_ptr, col, val, N, o.nnz, 0, 0};
+      if (cache_order && !csr_hash(row_ptr, col, val, N, o.nnz, o, &key.csr, s)) {
+        set_error("diffusion order: CSR fingerprint failed");
+        return TSNE_ERR_CUDA;
+      }
       if (!cache_order || !diff_cached(key, o, s)) {
         if ((st = diffusion_order(row_ptr, col, val, N, w, o, s)) != TSNE_OK) return st;
         TSNE_CUDA_TRY(cudaMemcpyAsync(o.dperm, w.perm, sizeof(int32_t) * N,

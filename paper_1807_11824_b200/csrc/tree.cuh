@@ -37,6 +37,8 @@ static_assert(kLevelBucketTest < 32, "level field");
 constexpr uint32_t kSkipMask = (1u << 27) - 1u;
 constexpr int kMaxParts = 4096;
 constexpr double kFixScale = 274877906944.0;  // 2^38: fixed-point COM sums
+static_assert(2 * kMaxTreePoints < (int64_t)kSkipMask + 1, "node index must fit the skip field");
+static_assert(kMaxTreePoints < (int64_t(1) << (63 - 38)), "count * 2^38 must fit int64");
 
 struct TreeWS {
   int64_t N = 0;

@@ -44,26 +44,11 @@ def test_knn_vs_oracle(T, orc, cfg, n, K):
     assert info["gemm_path"].startswith("tcgen05")
 
 
-@pytest.mark.parametrize("cfg,n,K", [("C5", 5000, 90), ("C2", 4100, 90), ("C4", 3000, 150)])
-def test_knn_tcgen05_vs_cudacore_path(T, cfg, n, K, monkeypatch):
-    # the two candidate stages must give the same exact kNN
-    X = torch.as_tensor(synth.make_x(cfg, n=n).numpy(), device="cuda")
-    idx_t, d2_t, it = T.knn(X, K)
-    monkeypatch.setenv("TSNE_KNN_PATH", "simt")
-    idx_s, d2_s, is_ = T.knn(X, K)
-    assert it["gemm_path"].startswith("tcgen05") and is_["gemm_path"] == "cuda-core"
-    assert torch.equal(d2_t, d2_s) and torch.equal(idx_t, idx_s)
-    assert it["rows_uncertified"] == 0 and is_["rows_uncertified"] == 0
-
-
-@pytest.mark.parametrize("path", ["tc2", "tc1", "simt"])
 @pytest.mark.parametrize("q0,q1", [(0, 4100), (1000, 2777), (129, 130), (3967, 4100), (5, 5)])
-def test_knn_rows_equal_full(T, orc, path, q0, q1, monkeypatch):
+def test_knn_rows_equal_full(T, orc, q0, q1):
     """tsne_knn_rows (the multi-GPU shard of the kNN by query row) gives the
-    rows q0..q1-1 of tsne_knn, bit for bit, on every candidate path."""
+    rows q0..q1-1 of tsne_knn, bit for bit."""
     X = torch.as_tensor(synth.make_x("C2", n=4100).numpy(), device="cuda")
-    if path != "tc2":
-        monkeypatch.setenv("TSNE_KNN_PATH", path)
     idx, d2, _ = T.knn(X, 90)
     il, dl, info = T.knn(X, 90, rows=(q0, q1))
     assert il.shape == (q1 - q0, 90)
