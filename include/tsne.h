@@ -86,7 +86,7 @@ typedef struct {
   int64_t rows_uncertified;  /* rows re-done by the exact fallback scan      */
   int32_t candidates;        /* K' used                                       */
   int32_t gemm_path;         /* 2 = tcgen05 symmetric search, 1 = tcgen05 row
-                                sweep (CTA pairs)                            */
+                                sweep (CTA pairs), 0 = no query rows (nq = 0) */
 } tsne_knn_info;
 
 size_t tsne_knn_workspace_size(int64_t N, int32_t D, int32_t K);
@@ -200,6 +200,21 @@ typedef struct {
                            graph diffusion of P is used instead); 0 = never
                            (64).  Results differ only by floating-point
                            summation order.                                     */
+  int32_t keep_state;   /* tsne_optimize only (0): 1 = keep the internal state
+                           (relabelled P, embedding in internal labels, relabel
+                           phase) and the instantiated CUDA graphs in the
+                           workspace after the call, so that the next call on
+                           the same workspace -- same P pointers, N, theta,
+                           learning rate, exaggeration and schedule, t0 = the
+                           previous t0 + n_iter -- continues from them instead
+                           of re-entering the label space (a re-permutation of
+                           P) and re-capturing the graphs.  It resumes only if
+                           Y, v, gains still hold exactly what the previous call
+                           wrote (checked by a device fingerprint, ~10 us);
+                           otherwise it starts afresh.  The caller promises not
+                           to modify row_ptr/col/val in between.  A run split
+                           into such calls is bitwise identical to one call.
+                           Host resources are freed by tsne_optimize_release. */
 } tsne_config;
 
 /* Fills the defaults listed above. */
@@ -226,6 +241,12 @@ tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const floa
                           float exaggeration, const tsne_config* cfg, void* ws,
                           size_t ws_bytes, tsne_stream_t stream);
 
+/* Frees the host-side resources (kept-state record, instantiated CUDA graphs)
+ * that tsne_optimize with tsne_config.keep_state attached to workspace `ws`.
+ * Call it before freeing or reusing the workspace for another problem.  No
+ * device work; never fails (an unknown ws is ignored). */
+void tsne_optimize_release(void* ws);
+
 /* Diagnostics for measurement (bench.py): from the optimiser state (advancing
  * it exactly like tsne_optimize by 2 * reps iterations from t0) it runs `reps`
  * eager iterations with the stages one after the other, then `reps` normal
@@ -234,7 +255,9 @@ tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const floa
  *   sums (H7), [3] update (H8), [4] one overlapped iteration (the attractive
  *   pass runs on a side stream concurrently with [0] and [1]).
  * kernels_per_iter (HOST out, nullable): kernel launches per iteration
- * (counted from a captured graph of one iteration).
+ * (counted from a captured graph of one iteration).  It overwrites the
+ * internal state of the workspace: a later keep_state tsne_optimize call on
+ * it starts afresh.
  * stage_ms (HOST out, 5 doubles).  Synchronises stream. */
 tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                                     int64_t N, float* Y, float* v, float* gains, int32_t t0,
@@ -315,6 +338,42 @@ typedef struct {
 tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, float theta,
                         float learning_rate, int32_t n_iter, float exaggeration,
                         const tsne_config* cfg, float* Y_out, tsne_run_info* info);
+
+/* ------------------------------------------------------------------------
+ * Algorithm 1 end to end on `world` GPUs, one process per GPU (
+ * the paper is single-GPU; its problem statement P:L147-148).  The
+ * library owns the NCCL communicator, built from `nccl_unique_id`
+ * (TSNE_NCCL_ID_BYTES bytes, identical on every rank: rank 0 obtains it with
+ * tsne_nccl_unique_id and the caller broadcasts it, e.g. over
+ * torch.distributed).  NCCL is loaded at run time (libnccl.so.2).
+ * Rank r owns rows [r S, min(N, (r+1) S)), S = ceil(N / world):
+ *   X_local [N_local x D] float32, HOST or DEVICE: this rank's rows of X;
+ *           N_local must equal the size of that range.
+ *   Y_out   [N x 2] float32, HOST or DEVICE: written on rank 0 (may be NULL
+ *           on the other ranks).
+ * Steps: X all-gathered; kNN of the own query rows against all N points
+ * (row sweep + fp64 re-rank, bit-identical to tsne_knn rows); the kNN lists
+ * all-gathered; P built on every rank; per iteration the attractive sums and
+ * the traversal of the own points, an all-gather of the Z partials (added in
+ * rank order: every rank uses the identical Z), the update of the own rows,
+ * an all-gather of the Y shards (CUDA graphs, one per schedule phase).
+ * Allocates tsne_run_workspace_size(N, D, K, world) bytes of device memory on
+ * the current device (one cudaMalloc, freed before return); blocking; every
+ * rank must call it with the same arguments except X_local / N_local / rank.
+ * info (HOST, nullable): stage times of this rank (ms_h2d = own rows H2D +
+ * all-gather of X; ms_knn = own kNN rows + all-gather of the lists).
+ * Errors: TSNE_ERR_ARG as tsne_run_ex (+ rank/world/N_local checks),
+ * TSNE_ERR_NCCL for a failed communicator or collective (the communicator is
+ * aborted), TSNE_ERR_NONFINITE, TSNE_ERR_CUDA.
+ * ------------------------------------------------------------------------ */
+#define TSNE_NCCL_ID_BYTES 128
+tsne_status tsne_nccl_unique_id(void* id_out /* HOST, TSNE_NCCL_ID_BYTES */);
+size_t tsne_run_workspace_size(int64_t N, int32_t D, int32_t K, int32_t world);
+tsne_status tsne_run_sharded(const float* X_local, int64_t N_local, int64_t N, int32_t D,
+                             float perplexity, float theta, float learning_rate, int32_t n_iter,
+                             float exaggeration, const tsne_config* cfg,
+                             const void* nccl_unique_id, int32_t rank, int32_t world,
+                             float* Y_out, tsne_run_info* info);
 
 #ifdef __cplusplus
 }

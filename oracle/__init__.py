@@ -69,6 +69,8 @@ def lib():
                                       i32, i32, f64, f64, f64, i32, f64, f64, f64]
         L.oracle_nn_preservation.argtypes = [P(i32), i32, i64, P(f64), i32]
         L.oracle_nn_preservation.restype = f64
+        L.oracle_nn_preservation_rows.argtypes = [P(i32), i32, i64, P(f64), i32, P(i64), i64]
+        L.oracle_nn_preservation_rows.restype = f64
         L.oracle_run.argtypes = [P(f32), i64, i32, f64, f64, f64, i32, f64, i32, f64, f64, f64,
                                  C.c_uint64, P(f32), P(f64), P(f64), P(i32)]
         L.oracle_num_threads.restype = C.c_int
@@ -288,11 +290,18 @@ def optimize(row_ptr, col, val32, Y, v=None, gains=None, t0=0, n_iter=1, theta=0
     return Y, v, gains
 
 
-def nn_preservation(idx_x, Y64, k=10):
+def nn_preservation(idx_x, Y64, k=10, rows=None):
+    """O12 k-NN preservation; `rows` (optional) restricts the mean to those points
+    (idx_x still holds every point's high-dimensional neighbours)."""
     idx_x = np.ascontiguousarray(idx_x, dtype=np.int32)
     Y64 = np.ascontiguousarray(Y64, dtype=np.float64)
-    return float(lib().oracle_nn_preservation(_P(idx_x, C.c_int32), idx_x.shape[1], Y64.shape[0],
-                                              _P(Y64, C.c_double), int(k)))
+    if rows is None:
+        return float(lib().oracle_nn_preservation(_P(idx_x, C.c_int32), idx_x.shape[1],
+                                                  Y64.shape[0], _P(Y64, C.c_double), int(k)))
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    return float(lib().oracle_nn_preservation_rows(_P(idx_x, C.c_int32), idx_x.shape[1],
+                                                   Y64.shape[0], _P(Y64, C.c_double), int(k),
+                                                   _P(rows, C.c_int64), len(rows)))
 
 
 def run(X, perplexity=30.0, theta=0.5, eta=200.0, n_iter=1000, exaggeration=12.0,

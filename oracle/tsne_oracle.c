@@ -728,33 +728,48 @@ int oracle_optimize(const int64_t* row_ptr, const int32_t* col, const float* val
 /* O12  k-NN preservation: mean_i |NN_k^X(i) & NN_k^Y(i)| / k, NN^X the
  * first k of the exact high-dimensional kNN rows (stride Kx), NN^Y a brute
  * force 2-D kNN with ties by index. */
+/* |NN_k^X(i) & NN_k^Y(i)| / k for one point i (the summand of O12) */
+static double nn_preserved_frac(const int32_t* idx_x, int32_t Kx, int64_t N, const double* Y,
+                                int32_t k, int64_t i) {
+  int32_t nb[64];
+  double dd[64];
+  int32_t have = 0;
+  for (int64_t j = 0; j < N; ++j) {
+    if (j == i) continue;
+    double dx = Y[2 * i] - Y[2 * j], dy = Y[2 * i + 1] - Y[2 * j + 1];
+    double d = dx * dx + dy * dy;
+    if (have == k && !key_less(d, (int32_t)j, dd[k - 1], nb[k - 1])) continue;
+    int32_t pos = (have < k) ? have : k - 1;
+    while (pos > 0 && key_less(d, (int32_t)j, dd[pos - 1], nb[pos - 1])) {
+      dd[pos] = dd[pos - 1]; nb[pos] = nb[pos - 1]; --pos;
+    }
+    dd[pos] = d; nb[pos] = (int32_t)j;
+    if (have < k) ++have;
+  }
+  int32_t common = 0;
+  for (int32_t a = 0; a < k; ++a)
+    for (int32_t b = 0; b < k; ++b)
+      if (idx_x[(size_t)i * Kx + a] == nb[b]) { ++common; break; }
+  return (double)common / (double)k;
+}
+
 double oracle_nn_preservation(const int32_t* idx_x, int32_t Kx, int64_t N,
                               const double* Y, int32_t k) {
   double tot = 0.0;
 #pragma omp parallel for schedule(dynamic, 16) reduction(+ : tot)
-  for (int64_t i = 0; i < N; ++i) {
-    int32_t nb[64];
-    double dd[64];
-    int32_t have = 0;
-    for (int64_t j = 0; j < N; ++j) {
-      if (j == i) continue;
-      double dx = Y[2 * i] - Y[2 * j], dy = Y[2 * i + 1] - Y[2 * j + 1];
-      double d = dx * dx + dy * dy;
-      if (have == k && !key_less(d, (int32_t)j, dd[k - 1], nb[k - 1])) continue;
-      int32_t pos = (have < k) ? have : k - 1;
-      while (pos > 0 && key_less(d, (int32_t)j, dd[pos - 1], nb[pos - 1])) {
-        dd[pos] = dd[pos - 1]; nb[pos] = nb[pos - 1]; --pos;
-      }
-      dd[pos] = d; nb[pos] = (int32_t)j;
-      if (have < k) ++have;
-    }
-    int32_t common = 0;
-    for (int32_t a = 0; a < k; ++a)
-      for (int32_t b = 0; b < k; ++b)
-        if (idx_x[(size_t)i * Kx + a] == nb[b]) { ++common; break; }
-    tot += (double)common / (double)k;
-  }
+  for (int64_t i = 0; i < N; ++i) tot += nn_preserved_frac(idx_x, Kx, N, Y, k, i);
   return tot / (double)N;
+}
+
+/* O12 on a sample of points: the same mean over the listed rows only (for
+ * N where the O(N^2) all-points form is too slow, e.g. C5). */
+double oracle_nn_preservation_rows(const int32_t* idx_x, int32_t Kx, int64_t N,
+                                   const double* Y, int32_t k, const int64_t* rows,
+                                   int64_t nrows) {
+  double tot = 0.0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : tot)
+  for (int64_t r = 0; r < nrows; ++r) tot += nn_preserved_frac(idx_x, Kx, N, Y, k, rows[r]);
+  return tot / (double)nrows;
 }
 
 /* Full pipeline (Algorithm 1): O1 -> O2 -> O3 -> init -> loop.

@@ -31,7 +31,8 @@ STATUS = {0: "TSNE_OK", 1: "TSNE_ERR_ARG", 2: "TSNE_ERR_CUDA", 3: "TSNE_ERR_WORK
 class Config(C.Structure):
     _fields_ = [("K", C.c_int32), ("exag_iters", C.c_int32), ("mom0", C.c_float),
                 ("mom1", C.c_float), ("min_gain", C.c_float), ("seed", C.c_uint64),
-                ("Y_init", C.c_void_p), ("use_graphs", C.c_int32), ("relabel_every", C.c_int32)]
+                ("Y_init", C.c_void_p), ("use_graphs", C.c_int32), ("relabel_every", C.c_int32),
+                ("keep_state", C.c_int32)]
 
 
 class KnnInfo(C.Structure):
@@ -49,10 +50,11 @@ class RunInfo(C.Structure):
 EXPORTS = ["tsne_last_error", "tsne_abi_version", "tsne_config_default",
            "tsne_knn_workspace_size", "tsne_knn", "tsne_knn_rows", "tsne_compute_p_workspace_size",
            "tsne_compute_p", "tsne_gradient_workspace_size", "tsne_gradient",
-           "tsne_optimize_workspace_size", "tsne_optimize", "tsne_init_y", "tsne_run",
+           "tsne_optimize_workspace_size", "tsne_optimize", "tsne_optimize_release", "tsne_init_y", "tsne_run",
            "tsne_run_ex", "tsne_profile_iterations", "tsne_shard_workspace_size",
            "tsne_shard_forces", "tsne_shard_attract", "tsne_shard_update", "tsne_recentre",
-           "tsne_kl_workspace_size", "tsne_kl"]
+           "tsne_kl_workspace_size", "tsne_kl", "tsne_nccl_unique_id", "tsne_run_workspace_size",
+           "tsne_run_sharded"]
 
 
 def lib():
@@ -83,6 +85,8 @@ def lib():
     L.tsne_optimize_workspace_size.restype = sz
     L.tsne_optimize.argtypes = [vp, vp, vp, i64, vp, vp, vp, i32, i32, f32, f32, f32,
                                 C.POINTER(Config), vp, sz, vp]
+    L.tsne_optimize_release.argtypes = [vp]
+    L.tsne_optimize_release.restype = None
     L.tsne_init_y.argtypes = [i64, C.c_uint64, vp, vp]
     L.tsne_profile_iterations.argtypes = [vp, vp, vp, i64, vp, vp, vp, i32, i32, f32, f32, f32,
                                           C.POINTER(Config), C.POINTER(C.c_double),
@@ -101,7 +105,12 @@ def lib():
     L.tsne_kl_workspace_size.restype = sz
     L.tsne_kl.argtypes = [vp, vp, vp, i64, vp, C.POINTER(C.c_double), C.POINTER(C.c_double), vp,
                           sz, vp]
-    for name in ["tsne_knn", "tsne_knn_rows", "tsne_compute_p", "tsne_gradient", "tsne_optimize", "tsne_init_y",
+    L.tsne_nccl_unique_id.argtypes = [vp]
+    L.tsne_run_workspace_size.argtypes = [i64, i32, i32, i32]
+    L.tsne_run_workspace_size.restype = sz
+    L.tsne_run_sharded.argtypes = [vp, i64, i64, i32, f32, f32, f32, i32, f32, C.POINTER(Config),
+                                   vp, i32, i32, vp, C.POINTER(RunInfo)]
+    for name in ["tsne_nccl_unique_id", "tsne_run_sharded", "tsne_knn", "tsne_knn_rows", "tsne_compute_p", "tsne_gradient", "tsne_optimize", "tsne_init_y",
                  "tsne_run", "tsne_run_ex", "tsne_profile_iterations", "tsne_shard_forces",
                  "tsne_shard_attract", "tsne_shard_update", "tsne_recentre", "tsne_kl"]:
         getattr(L, name).restype = C.c_int
@@ -163,7 +172,7 @@ def knn(X: torch.Tensor, K: int, rows=None):
         _check(lib().tsne_knn_rows(_ptr(X), N, D, K, q0, q1 - q0, _ptr(idx), _ptr(d2), _ptr(ws),
                                    ws.numel(), C.byref(info), _stream()), "tsne_knn_rows")
     return idx, d2, {"rows_uncertified": info.rows_uncertified, "candidates": info.candidates,
-                     "gemm_path": {2: "tcgen05-sym", 1: "tcgen05"}[info.gemm_path]}
+                     "gemm_path": {2: "tcgen05-sym", 1: "tcgen05", 0: "none"}[info.gemm_path]}
 
 
 # ---------------------------------------------------------------- U2 + U3
@@ -231,7 +240,11 @@ class State:
 
 
 class Optimizer:
-    """Holds the workspace of the iteration loop; step(n) runs n iterations."""
+    """Holds the workspace of the iteration loop; step(n) runs n iterations.
+    Consecutive step() calls continue the library's internal state (keep_state):
+    the relabelled P and the CUDA graphs stay in the workspace, so step(a);
+    step(b) equals step(a + b) bitwise.  Modifying `state` in between is
+    detected (fingerprint) and restarts from the modified state."""
 
     def __init__(self, row_ptr, col, val, Y: torch.Tensor, theta=0.5, learning_rate=200.0,
                  exaggeration=12.0, exag_iters=250, mom0=0.5, mom1=0.8, min_gain=0.01,
@@ -245,9 +258,15 @@ class Optimizer:
         self.theta, self.lr, self.exag = float(theta), float(learning_rate), float(exaggeration)
         self.cfg = default_config(exag_iters=exag_iters, mom0=mom0, mom1=mom1, min_gain=min_gain,
                                   use_graphs=1 if use_graphs else 0,
-                                  relabel_every=int(relabel_every))
+                                  relabel_every=int(relabel_every), keep_state=1)
         self.nnz = int(self.col.numel())
         self.ws = _ws(lib().tsne_optimize_workspace_size(self.N, self.nnz), Y.device)
+
+    def __del__(self):
+        try:
+            lib().tsne_optimize_release(_ptr(self.ws))
+        except Exception:
+            pass
 
     def step(self, n_iter: int = 1, stream=None):
         s = self.state

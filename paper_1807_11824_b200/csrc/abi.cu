@@ -31,7 +31,7 @@ void set_error(const char* fmt, ...) {
 }
 void clear_error() { g_err[0] = 0; }
 
-static tsne_status check_device() {
+tsne_status check_device() {
   int dev = -1;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) {
@@ -120,6 +120,7 @@ void tsne_config_default(tsne_config* cfg) {
   cfg->Y_init = nullptr;
   cfg->use_graphs = 1;
   cfg->relabel_every = 64;
+  cfg->keep_state = 0;
 }
 
 // ---------------------------------------------------------------- gradient
@@ -247,7 +248,7 @@ tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const floa
   st = run_iterations(row_ptr, col, val, N, reinterpret_cast<float2*>(Y),
                       reinterpret_cast<float2*>(v), reinterpret_cast<float2*>(gains), t0, n_iter,
                       theta, sc, cfg.use_graphs != 0, cfg.relabel_every, p.tree, p.opt, s,
-                      /*cache_order=*/true);
+                      /*cache_order=*/true, cfg.keep_state != 0);
   int32_t flag = 0;
   if (st == TSNE_OK) {
     cudaError_t e = cudaMemcpyAsync(&flag, p.opt.flag, sizeof(flag), cudaMemcpyDeviceToHost, s);
@@ -264,6 +265,8 @@ tsne_status tsne_optimize(const int64_t* row_ptr, const int32_t* col, const floa
   }
   return st;
 }
+
+void tsne_optimize_release(void* ws) { release_session(ws); }
 
 tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                                     int64_t N, float* Y, float* v, float* gains, int32_t t0,

@@ -94,6 +94,39 @@ __device__ __forceinline__ void win_accum(float2 yi, float2 yj, float p, float& 
   ay = fmaf(pw, dy, ay);
 }
 
+// E x 32 consecutive entries of a staged row (n_rem entries remain from cr):
+// lane takes entries lane + 32u; only the last group can be partial (its
+// absent entries are the point itself with p = 0).  All loads first, then
+// the arithmetic: the window / L2 gathers of the block are in flight together.
+template <int E>
+__device__ __forceinline__ void row_block(const int32_t* __restrict__ cr,
+                                          const float* __restrict__ vr, int n_rem, int self,
+                                          float2 yi, uint32_t sbase, const float2* __restrict__ Y,
+                                          int wlo, int wn, int lane, float& ax, float& ay) {
+  int c[E];
+  float p[E];
+#pragma unroll
+  for (int u = 0; u < E; ++u) {
+    const int q = lane + 32 * u;
+    if (u < E - 1) {
+      c[u] = cr[q];
+      p[u] = vr[q];
+    } else {
+      c[u] = self;
+      p[u] = 0.f;
+      if (q < n_rem) {
+        c[u] = cr[q];
+        p[u] = vr[q];
+      }
+    }
+  }
+  float2 y[E];
+#pragma unroll
+  for (int u = 0; u < E; ++u) y[u] = win_y(sbase, Y, c[u], wlo, wn);
+#pragma unroll
+  for (int u = 0; u < E; ++u) win_accum(yi, y[u], p[u], ax, ay);
+}
+
 // spin wait (no suspend-time hint: the pipeline's waits are short and a
 // sleeping producer would throttle the stream)
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* b, uint32_t parity) {
@@ -245,46 +278,22 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
       if (e0 >= a_lo && e1 <= a_hi) {             // the row is staged (the common case)
         const int32_t* cr = cs + (e0 - a_lo);
         const float* vr = vs + (e0 - a_lo);
-        // The first 32 entries decide the mode: if several of their columns lie
-        // outside the window (neighbourhoods spread over the labels, e.g. the
-        // GloVe-shaped C4), the rest of the row is issued as one predicated
-        // block of 8 gathers per lane, so the L2 latency is paid once per 256
-        // entries; otherwise the loops below (few L2 gathers) run.
-        int q = lane;
-        bool far;
-        {
-          const bool in = q < n;
-          const int c = in ? cr[q] : i;
-          const float p = in ? vr[q] : 0.f;
-          far = __popc(__ballot_sync(0xffffffffu, (unsigned)(c - wlo) >= (unsigned)wn)) >= 4;
-          win_accum(yi, win_y(sbase, Y, c, wlo, wn), p, ax, ay);
-          q += 32;
-        }
-        if (far) {
-          for (; q < n; q += 8 * 32) {
-            float2 yj[8];
-            float pj[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int e = q + 32 * u;
-              const bool in = e < n;
-              yj[u] = win_y(sbase, Y, in ? cr[e] : i, wlo, wn);
-              pj[u] = in ? vr[e] : 0.f;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) win_accum(yi, yj[u], pj[u], ax, ay);
-          }
-        } else {
-          // long rows (K = 150 workloads): 8 gathers in flight per lane
-          for (; q + 7 * 32 < n; q += 8 * 32) {
-            float2 yj[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) yj[u] = win_y(sbase, Y, cr[q + 32 * u], wlo, wn);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) win_accum(yi, yj[u], vr[q + 32 * u], ax, ay);
-          }
-#pragma unroll 4
-          for (; q < n; q += 32) win_accum(yi, win_y(sbase, Y, cr[q], wlo, wn), vr[q], ax, ay);
+        // blocks of up to 8 x 32 entries: every gather of a block is issued
+        // before any arithmetic, so a row pays the L2 latency of its columns
+        // outside the window about once, not once per 32 entries
+        int b = 0;
+        for (; n - b > 8 * 32; b += 8 * 32)
+          row_block<8>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay);
+        switch ((n - b + 31) >> 5) {
+          case 1: row_block<1>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
+          case 2: row_block<2>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
+          case 3: row_block<3>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
+          case 4: row_block<4>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
+          case 5: row_block<5>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
+          case 6: row_block<6>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
+          case 7: row_block<7>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
+          case 8: row_block<8>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
+          default: break;
         }
       } else if (n <= kAtLong) {
         for (int q = lane; q < n; q += 32)

@@ -417,30 +417,157 @@ static tsne_status capture_pair(Graph& gr, int h, int64_t N, float theta, const 
   return TSNE_OK;
 }
 
+// ---------------------------------------------------------------- sessions
+// With tsne_config.keep_state the workspace keeps, after a call, the internal
+// state (relabelled P, Y/V/G in internal labels, the relabel phase) and the
+// instantiated graphs; a later call on the same workspace with the same
+// problem and constants whose t0 continues the previous call resumes from
+// them -- no re-entry into the label space (k_relabel_rows re-permutes the
+// 1.5 GB CSR at C5) and no graph capture -- provided the caller's Y, v,
+// gains still hold exactly what the previous call wrote (a device
+// fingerprint).  The caller promises not to modify P in between.
+struct Session {
+  const void* ws = nullptr;
+  const int64_t* rp = nullptr;
+  const int32_t* col = nullptr;
+  const float* val = nullptr;
+  int64_t N = 0, nnz = 0;
+  float theta = 0.f;
+  Sched sc{};
+  bool use_graphs = false;
+  int relabel_every = 0;
+  // state after the last call
+  bool live = false;          // the internal state below is valid
+  int h = 0;                  // P half in use
+  int since = 0;              // iterations since the last relabel checkpoint
+  int32_t t_next = 0;
+  uint64_t fp = 0;            // fingerprint of the caller's Y, v, gains
+  Graph gr[2];
+  bool have_gr[2] = {false, false};
+};
+static std::mutex g_sess_mu;
+static std::vector<Session*> g_sess;
+
+static bool same_problem(const Session& a, const Session& b) {
+  return a.ws == b.ws && a.rp == b.rp && a.col == b.col && a.val == b.val && a.N == b.N &&
+         a.nnz == b.nnz && a.theta == b.theta && a.sc.exag_iters == b.sc.exag_iters &&
+         a.sc.exag == b.sc.exag && a.sc.mom0 == b.sc.mom0 && a.sc.mom1 == b.sc.mom1 &&
+         a.sc.eta == b.sc.eta && a.sc.min_gain == b.sc.min_gain && a.use_graphs == b.use_graphs &&
+         a.relabel_every == b.relabel_every;
+}
+
+// the session of workspace `ws` (created on first use; replaced if the problem differs)
+static Session* session_for(const Session& key) {
+  std::lock_guard<std::mutex> g(g_sess_mu);
+  for (size_t i = 0; i < g_sess.size(); ++i)
+    if (g_sess[i]->ws == key.ws) {
+      if (same_problem(*g_sess[i], key)) return g_sess[i];
+      delete g_sess[i];
+      g_sess.erase(g_sess.begin() + i);
+      break;
+    }
+  if (g_sess.size() >= 16) {                   // bound the host memory of abandoned sessions
+    delete g_sess.front();
+    g_sess.erase(g_sess.begin());
+  }
+  Session* n = new Session();
+  n->ws = key.ws; n->rp = key.rp; n->col = key.col; n->val = key.val; n->N = key.N;
+  n->nnz = key.nnz; n->theta = key.theta; n->sc = key.sc; n->use_graphs = key.use_graphs;
+  n->relabel_every = key.relabel_every;
+  g_sess.push_back(n);
+  return n;
+}
+
+void release_session(const void* ws) {
+  std::lock_guard<std::mutex> g(g_sess_mu);
+  for (size_t i = 0; i < g_sess.size(); ++i)
+    if (g_sess[i]->ws == ws) {
+      delete g_sess[i];
+      g_sess.erase(g_sess.begin() + i);
+      return;
+    }
+}
+
+// the internal state of workspace ws is about to be overwritten by other work
+static void invalidate_session(const void* ws) {
+  std::lock_guard<std::mutex> g(g_sess_mu);
+  for (auto* e : g_sess)
+    if (e->ws == ws) e->live = false;
+}
+
+// order-dependent 64-bit fingerprint of the caller's state (Y, v, gains)
+__global__ void k_state_hash(const float2* __restrict__ Y, const float2* __restrict__ V,
+                             const float2* __restrict__ G, int N,
+                             unsigned long long* __restrict__ out) {
+  unsigned long long h = 0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    const float2 y = Y[k], v = V[k], g = G[k];
+    const unsigned long long kk = (unsigned long long)k * 0x9e3779b97f4a7c15ull;
+    h += mix64(kk ^ (((unsigned long long)__float_as_uint(y.x) << 32) | __float_as_uint(y.y)));
+    h += mix64((kk + 1) ^ (((unsigned long long)__float_as_uint(v.x) << 32) | __float_as_uint(v.y)));
+    h += mix64((kk + 2) ^ (((unsigned long long)__float_as_uint(g.x) << 32) | __float_as_uint(g.y)));
+  }
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, h);
+}
+
+static bool state_hash(const float2* Y, const float2* V, const float2* G, int64_t N,
+                       const OptWS& o, uint64_t* h, cudaStream_t s) {
+  if (cudaMemsetAsync(o.dtag, 0, sizeof(uint64_t), s) != cudaSuccess) return false;
+  k_state_hash<<<2 * kNumSMs, 256, 0, s>>>(Y, V, G, (int)N, (unsigned long long*)o.dtag);
+  if (cudaGetLastError() != cudaSuccess) return false;
+  if (cudaMemcpyAsync(h, o.dtag, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return false;
+  return cudaStreamSynchronize(s) == cudaSuccess;
+}
+
 tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                            int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t n_iter,
                            float theta, const Sched& sc, bool use_graphs, int relabel_every,
-                           TreeWS& w, OptWS& o, cudaStream_t s, bool cache_order) {
+                           TreeWS& w, OptWS& o, cudaStream_t s, bool cache_order,
+                           bool keep_state) {
   SideRes side(o);
-  tsne_status st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, relabel_every > 0, cache_order, s);
-  if (st != TSNE_OK) return st;
-  int h = 0;                                   // P half in use
-  const bool graphs = use_graphs && s != nullptr && n_iter >= 4;
-  Graph gr[2];
-  if (graphs) {
-    if ((st = capture_pair(gr[0], 0, N, theta, sc, w, o, s)) != TSNE_OK) return st;
-    if (relabel_every > 0 && n_iter > relabel_every &&
-        (st = capture_pair(gr[1], 1, N, theta, sc, w, o, s)) != TSNE_OK)
-      return st;
+  const bool graphs = use_graphs && s != nullptr;
+  Session local;
+  Session* ses = &local;
+  if (keep_state) {
+    Session key;
+    key.ws = o.ws_base; key.rp = row_ptr; key.col = col; key.val = val; key.N = N;
+    key.nnz = o.nnz; key.theta = theta; key.sc = sc; key.use_graphs = graphs;
+    key.relabel_every = relabel_every;
+    ses = session_for(key);
   }
-  const int period = relabel_every > 0 ? ((relabel_every + 1) & ~1) : n_iter;
+  bool resume = false;
+  if (keep_state && ses->live && ses->t_next == t0) {
+    uint64_t h = 0;
+    resume = state_hash(Y, V, G, N, o, &h, s) && h == ses->fp;
+  }
+  ses->live = false;
+  tsne_status st;
+  if (resume) {
+    k_set_state<<<1, 1, 0, s>>>(o.t_dev, t0, o.flag);
+    TSNE_LAUNCH_CHECK();
+  } else {
+    st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, relabel_every > 0, cache_order, s);
+    if (st != TSNE_OK) return st;
+    ses->h = 0;
+    ses->since = 0;
+  }
+  int h = ses->h;
+  const int period = relabel_every > 0 ? relabel_every : (1 << 30);
+  int since = ses->since;
   int32_t done = 0;
-  float2* cur = o.Ya;
   while (done < n_iter) {
-    const int chunk = (n_iter - done) < period ? (n_iter - done) : period;
+    // the state is in Ya at every chunk boundary
+    const int chunk = (n_iter - done) < (period - since) ? (n_iter - done) : (period - since);
     int c = 0;
-    if (graphs)
-      for (; c + 2 <= chunk; c += 2) TSNE_CUDA_TRY(cudaGraphLaunch(gr[h].e, s));
+    if (graphs && chunk >= 2 && (ses->have_gr[h] || n_iter >= 4)) {
+      if (!ses->have_gr[h]) {
+        if ((st = capture_pair(ses->gr[h], h, N, theta, sc, w, o, s)) != TSNE_OK) return st;
+        ses->have_gr[h] = true;
+      }
+      for (; c + 2 <= chunk; c += 2) TSNE_CUDA_TRY(cudaGraphLaunch(ses->gr[h].e, s));
+    }
     for (; c < chunk; ++c) {
       float2* a = (c % 2 == 0) ? o.Ya : o.Yb;
       float2* b = (c % 2 == 0) ? o.Yb : o.Ya;
@@ -448,20 +575,39 @@ tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const flo
                               s)) != TSNE_OK)
         return st;
     }
-    cur = (chunk % 2 == 0) ? o.Ya : o.Yb;
+    if (chunk % 2)
+      TSNE_CUDA_TRY(cudaMemcpyAsync(o.Ya, o.Yb, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
     done += chunk;
-    if (done < n_iter && t0 + done >= kMortonFrom &&
-        morton_improves(o.rp[h], o.col[h], w.perm, N, o, s)) {
-      // chunks are even, so the state is in Ya; w.perm is the Morton order of
-      // the last iteration's embedding (a permutation of the current labels).
-      // The pending recentring shift is uniform, so it commutes with relabelling.
-      if ((st = relabel(w.perm, (int)N, o.rp[h], o.col[h], o.val[h], o.Ya, o.V, o.G, o.lab, 1 - h,
-                        o, s)) != TSNE_OK)
-        return st;
-      h = 1 - h;
+    since += chunk;
+    if (since == period) {
+      since = 0;
+      // a relabel checkpoint (also at the end of a call whose state is kept)
+      if ((done < n_iter || keep_state) && t0 + done >= kMortonFrom &&
+          morton_improves(o.rp[h], o.col[h], w.perm, N, o, s)) {
+        // w.perm is the Morton order of the last iteration's embedding (a
+        // permutation of the current labels); the pending recentring shift
+        // is uniform, so it commutes with relabelling.
+        if ((st = relabel(w.perm, (int)N, o.rp[h], o.col[h], o.val[h], o.Ya, o.V, o.G, o.lab,
+                          1 - h, o, s)) != TSNE_OK)
+          return st;
+        h = 1 - h;
+      }
     }
   }
-  return leave(N, cur, Y, V, G, w, o, s);
+  if ((st = leave(N, o.Ya, Y, V, G, w, o, s)) != TSNE_OK) return st;
+  if (keep_state) {
+    uint64_t hsh = 0;
+    if (!state_hash(Y, V, G, N, o, &hsh, s)) {
+      set_error("tsne_optimize: state fingerprint failed");
+      return TSNE_ERR_CUDA;
+    }
+    ses->fp = hsh;
+    ses->h = h;
+    ses->since = since;
+    ses->t_next = t0 + n_iter;
+    ses->live = true;
+  }
+  return TSNE_OK;
 }
 
 tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
@@ -469,6 +615,7 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
                                float theta, const Sched& sc, TreeWS& w, OptWS& o, double* stage_ms,
                                int32_t* kernels, cudaStream_t s) {
   SideRes side(o);
+  invalidate_session(o.ws_base);
   tsne_status st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, true, true, s);
   if (st != TSNE_OK) return st;
   if (kernels) {  // count kernel nodes of one captured (never launched) iteration

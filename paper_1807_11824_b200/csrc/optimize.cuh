@@ -51,7 +51,10 @@ tsne_status launch_update(const float2* Yin, const float2* A, int64_t N, TreeWS&
 tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                            int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t n_iter,
                            float theta, const Sched& sc, bool use_graphs, int relabel_every,
-                           TreeWS& w, OptWS& o, cudaStream_t s, bool cache_order);
+                           TreeWS& w, OptWS& o, cudaStream_t s, bool cache_order,
+                           bool keep_state = false);
+// drops the kept state and graphs of workspace ws (tsne_optimize_release)
+void release_session(const void* ws);
 
 tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                                int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t reps,

@@ -156,26 +156,44 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   constexpr bool stats = STATS;
   // list (multi-GPU): the sorted positions of the points this rank owns
   // (original indices [row0, ...)); rep is then indexed by perm[k] - row0.
-  // per level l: {r^2 (fp32), margin constant A_l, margin slope B_l}, r^2 (fp64)
-  __shared__ float4 s_lv[kLevels + 2];
-  __shared__ double s_r2d[kLevels + 2];
+  // Per level code l: {thr_l = r_l^2 / theta^2, margin constant A_l / theta^2,
+  // margin slope B_l, 0} (fp32) and r_l^2 (fp64).  The test is
+  //   diff = D^2 - thr_l  >  marg = A'_l + B_l D^2      (accept),
+  //   |diff| <= marg                                    (decide in fp64).
+  // Leaves of one point (24) always "accept" (the exact pair: thr = -inf);
+  // bucket leaves (26) never do (thr = +inf); cells deeper than kDeepFp32
+  // and bucket tests (25, r_23) always go to fp64 (A' = +inf).
+  __shared__ float4 s_lv[kLevelCodes];
+  __shared__ double s_r2d[kLevelCodes];
   __shared__ double s_z[kTravThreads / 32];
   __shared__ int s_done;
-  const float theta2 = theta * theta;
   const double theta2d = (double)theta * (double)theta;
-  if (threadIdx.x < kLevels + 2) {
+  if (threadIdx.x < kLevelCodes) {
     const int l = threadIdx.x;
     const int le = (l == kLevelBucketTest) ? kLevels - 1 : (l > kLevels ? kLevels : l);
     const double r = ldexp(box->r0, -le);
     const double r2 = r * r;
     const double M = (double)box->mabs, th = (double)theta;
-    // Worst-case fp32 error of diff = theta^2 D^2 - r^2:
+    // Worst-case fp32 error of theta^2 D^2 - r^2:
     //   E <= 2^-24 (2.83 theta (theta D) M + 6.83 theta^2 D^2 + r^2).
     // margin = 2^-19 (r^2 + lhs) + 2^-20 theta M (r + theta D), with the
-    // AM-GM bound theta D <= (lhs / r + r) / 2, i.e. margin = A + B lhs >= 4.7 E.
+    // AM-GM bound theta D <= (lhs / r + r) / 2, i.e. margin = A + B lhs >= 4.7 E
+    // (lhs = theta^2 D^2).  Divided by theta^2 (the comparison is made on
+    // D^2 - r^2 / theta^2, whose fp32 error is at most E / theta^2: the
+    // product by theta^2 is gone, thr is rounded once): A' = A / theta^2, B.
     const double A = ldexp(1.0, -19) * r2 + ldexp(1.0, -20) * th * M * r * 1.5;
     const double B = ldexp(1.0, -19) + ldexp(1.0, -21) * th * M / r;
-    s_lv[l] = make_float4((float)r2, (float)A, (float)B, 0.f);
+    float thr, Ap, Bp;
+    if (l == kLevelLeaf) {
+      thr = -INFINITY; Ap = 0.f; Bp = 0.f;
+    } else if (l == kLevelBucket || theta2d == 0.0) {
+      thr = INFINITY; Ap = 0.f; Bp = 0.f;                 // never accepted (theta = 0: exact)
+    } else if (l > kDeepFp32) {
+      thr = (float)(r2 / theta2d); Ap = INFINITY; Bp = 0.f;
+    } else {
+      thr = (float)(r2 / theta2d); Ap = (float)(A / theta2d); Bp = (float)B;
+    }
+    s_lv[l] = make_float4(thr, Ap, Bp, 0.f);
     s_r2d[l] = r2;
   }
   if (threadIdx.x == 0) s_done = 0;
@@ -188,63 +206,63 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   const float2 yi = active ? ys[k] : make_float2(0.f, 0.f);
   const int Li = active ? leafnode[k] : -1;
   float fx = 0.f, fy = 0.f;
-  double z = 0.0;   // fp64: Z sums up to N^2 terms of very different size
+  float zf = 0.f;   // per point: ~100 terms; Z = sum over points in fp64 (A.7)
+  double z = 0.0;   // bucket pairs (rare) and the final per-point value
 
   int pq_s[kPend], pq_c[kPend];   // deferred buckets of this lane
 #pragma unroll
   for (int q = 0; q < kPend; ++q) { pq_s[q] = -1; pq_c[q] = 0; }
   int npend = 0;
-  const uint32_t lv_base = (uint32_t)__cvta_generic_to_shared(s_lv);
   unsigned n_visit = 0, n_take = 0, n_f64 = 0, n_pair = 0;
+  // loop-invariant addresses held in registers (the compiler would otherwise
+  // rematerialise them on every visit)
+  uint32_t lv_base;
+  asm volatile("mov.u32 %0, %1;" : "=r"(lv_base) : "r"((uint32_t)__cvta_generic_to_shared(s_lv)));
+  const float4* nodes_r;
+  asm volatile("mov.b64 %0, %1;" : "=l"(nodes_r) : "l"(nodes));
   while (cur < nnodes) {
     if (stats) ++n_visit;
-    const float4 nd = __ldg(nodes + cur);
+    const float4 nd = __ldg(nodes_r + (unsigned)cur);
     const uint32_t sw = __float_as_uint(nd.w);
-    const int lvl = (int)(sw >> 27);
+    const uint32_t lvl = sw >> 27;
     const int skip = (int)(sw & kSkipMask);
-    const float cntf = nd.z;
-    const bool self_in = (unsigned)(Li - cur) < (unsigned)(skip - cur);   // Li in [cur, skip)
-    const float dx = yi.x - nd.x, dy = yi.y - nd.y;
-    const float D2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-    const bool leaf = lvl == kLevelLeaf;
     float4 lv;
     asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
         : "=f"(lv.x), "=f"(lv.y), "=f"(lv.z), "=f"(lv.w) : "r"(lv_base + 16u * lvl));
+    float dx = yi.x - nd.x, dy = yi.y - nd.y;
+    float D2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+    const bool self_in = (unsigned)(Li - cur) < (unsigned)(skip - cur);   // Li in [cur, skip)
     // criterion (D10) in fp32 with the D25 margin
-    const float lhs = __fmul_rn(theta2, D2);
-    const float diff = lhs - lv.x;
-    const float marg = fmaf(lv.z, lhs, lv.y);
+    const float diff = D2 - lv.x;
+    const float marg = fmaf(lv.z, D2, lv.y);
     bool acc = diff > marg;
-    // cells below level kDeepFp32 are decided, and their offset y_i - com
-    // taken, in fp64: their size approaches the fp32 spacing of the coordinates
-    // (inside the fp32 band, too, the decision is taken in fp64, D25)
-    float ddx = dx, ddy = dy, dd2 = D2;
-    if (!leaf && !self_in && (lvl > kDeepFp32 || fabsf(diff) <= marg)) {
-      const double2 c = com64[cur];
+    if (fabsf(diff) <= marg && !self_in) {
+      // inside the fp32 band, or a deep cell (its size approaches the fp32
+      // spacing of the coordinates): the decision and the offset in fp64 (D25)
+      const double2 c = com64[(unsigned)cur];
       const double ex = __dsub_rn((double)yi.x, c.x), ey = __dsub_rn((double)yi.y, c.y);
       const double D2d = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
       acc = s_r2d[lvl] < __dmul_rn(theta2d, D2d);
-      ddx = (float)ex;
-      ddy = (float)ey;
-      dd2 = __fadd_rn(__fmul_rn(ddx, ddx), __fmul_rn(ddy, ddy));
+      dx = (float)ex;
+      dy = (float)ey;
+      D2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
       if (stats) ++n_f64;
     }
-    // exact leaf of one point: the exact pair; internal cell: the criterion;
-    // a cell containing i is opened (D11)
-    const bool take = !self_in && (leaf ? cntf == 1.f : acc);
-    const bool bucket = !take && (leaf ? cntf > 1.f : lvl == kLevelBucketTest);
+    // accept a cell / take a one-point leaf, unless it contains i (D11)
+    const bool take = acc && !self_in;
     const int node = cur;
-    cur = (take || leaf || bucket) ? skip : cur + 1;
-    const float w = rcp_approx(1.f + dd2);
-    const float nw = take ? cntf * w : 0.f;
+    cur = (take || lvl >= (uint32_t)kLevelLeaf) ? skip : cur + 1;
+    const float w = rcp_approx(1.f + D2);
+    const float nw = take ? nd.z * w : 0.f;
     if (stats && take) ++n_take;
-    z += (double)nw;
+    zf += nw;
     const float nww = nw * w;
-    fx = fmaf(nww, ddx, fx);
-    fy = fmaf(nww, ddy, fy);
-    if (bucket && !self_in) {   // another bucket, not accepted: exact pairs (own bucket: k_bucket_pairs)
+    fx = fmaf(nww, dx, fx);
+    fy = fmaf(nww, dy, fy);
+    if (!take && !self_in && lvl > (uint32_t)kLevelLeaf) {
+      // another bucket, not accepted: exact pairs (own bucket: k_bucket_pairs)
       const int s0 = nfirst[node];
-      const int cnt = (int)cntf;
+      const int cnt = (int)nd.z;
       if (stats) n_pair += (unsigned)cnt;
       if (npend < kPend) {      // deferred: processed warp-synchronously after the walk
 #pragma unroll
@@ -256,6 +274,7 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
       }
     }
   }
+  z += (double)zf;
   // Deferred buckets: lanes of the warp that share a bucket walk its members
   // together (a lane reaches a bucket at its own step of the walk, so doing it
   // in place would run the member loop once per lane group).

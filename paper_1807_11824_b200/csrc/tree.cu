@@ -452,7 +452,7 @@ __global__ void k_quad_emit(int N, const int32_t* __restrict__ bfirst,
       level = qlevel(dl);
     } else {                                          // bucket top
       int p = bparent[id];
-      level = (p < 0 || bdelta[p] <= kKeyBits - 3) ? kLevelBucketTest : kLevelLeaf;
+      level = (p < 0 || bdelta[p] <= kKeyBits - 3) ? kLevelBucketTest : kLevelBucket;
     }
   } else {
     s = e = id - (N - 1);

@@ -12,10 +12,10 @@
 //
 // level field: 0..23  internal cell whose point set branches at that level
 //                     (single-child chains are compressed away, D9)
-//              24     leaf evaluated exactly (one point, or a level-24 bucket
-//                     directly below a level-23 branching cell)
+//              24     leaf of one point (the exact pair)
 //              25     bucket whose chain reaches level <= 23: the criterion
 //                     is tested with r_23; accept -> summary, else exact pairs
+//              26     bucket directly below a level-23 branching cell: exact pairs
 #pragma once
 #include "common.cuh"
 
@@ -33,7 +33,10 @@ constexpr int kLevels = 24;                   // quadtree depth (D9): 2^24 cells
 constexpr int kKeyBits = 2 * kLevels;          // Morton key bits (48, in a 64-bit word)
 constexpr int kLevelLeaf = kLevels;            // 24
 constexpr int kLevelBucketTest = kLevels + 1;  // 25 (level field is 5 bits)
-static_assert(kLevelBucketTest < 32, "level field");
+constexpr int kLevelBucket = kLevels + 2;      // 26: several points in a level-24 cell below a
+                                               // level-23 branching cell: always exact pairs
+constexpr int kLevelCodes = kLevels + 3;       // level codes 0..26
+static_assert(kLevelBucket < 32, "level field");
 constexpr uint32_t kSkipMask = (1u << 27) - 1u;
 constexpr int kMaxParts = 4096;
 constexpr double kFixScale = 274877906944.0;  // 2^38: fixed-point COM sums

@@ -14,12 +14,13 @@ The host logic (ranges, exchange order, padding) lives here; all arithmetic
 runs in the library's kernels (`GpuShardOps`).  The ops object is injectable
 so the host logic can be tested on CPU with a gloo process group.
 
-`run` is the multi-GPU end-to-end call (Algorithm 1): each rank
-copies its own rows of X host->device, the rows are all-gathered over NCCL,
-each rank finds the neighbours of its own query rows (tsne_knn_rows), the
-kNN lists are all-gathered, P is built redundantly on every rank (it is
-~50 ms at C5 and needs every row: symmetrisation), and the sharded
-iterations run; rank 0 copies the final Y to the host.
+`run` is the multi-GPU end-to-end call (Algorithm 1): a thin
+caller of the C ABI's tsne_run_sharded, which owns its NCCL communicator
+(built from an id rank 0 makes and `run` broadcasts): each rank copies its
+own rows of X host->device, the rows are all-gathered, each rank finds the
+neighbours of its own query rows, the kNN lists are all-gathered, P is built
+redundantly on every rank (it is ~40 ms at C5 and needs every row:
+symmetrisation), and the sharded iterations run; rank 0 gets the final Y.
 """
 from __future__ import annotations
 
@@ -61,24 +62,8 @@ def _all_gather_flat(out: torch.Tensor, inp: torch.Tensor, group=None):
 
 
 class GpuShardOps:
-    """The C-ABI kernels of one rank (tsne_shard_forces / _update / tsne_recentre,
-    and for `run`: tsne_knn_rows, tsne_compute_p, tsne_init_y)."""
-
-    @staticmethod
-    def knn_rows(X, K, q0, q1):
-        from . import knn
-        idx, d2, info = knn(X, K, rows=(q0, q1))
-        return idx, d2, info["rows_uncertified"]
-
-    @staticmethod
-    def compute_p(idx, d2, perplexity):
-        from . import compute_p
-        return compute_p(idx, d2, perplexity)
-
-    @staticmethod
-    def init_y(N, seed, device):
-        from . import init_y
-        return init_y(N, seed, device=device)
+    """The C-ABI kernels of one rank (tsne_shard_forces / _attract / _update,
+    tsne_recentre) for ShardedOptimizer."""
 
     def __init__(self, N: int, device):
         from . import _check, _ptr, _stream, _ws, lib
@@ -204,58 +189,60 @@ class ShardedOptimizer:
         return self.Y
 
 
+def nccl_unique_id(group=None, device=None) -> bytes:
+    """An NCCL unique id (TSNE_NCCL_ID_BYTES bytes) made by rank 0 of `group`
+    (tsne_nccl_unique_id) and broadcast to every rank over torch.distributed."""
+    from . import _check, lib
+    n = 128
+    if dist.get_rank(group) == 0:
+        buf = (C.c_uint8 * n)()
+        _check(lib().tsne_nccl_unique_id(buf), "tsne_nccl_unique_id")
+        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+    else:
+        t = torch.zeros(n, dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        t = t.to(device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast(t, src=src, group=group)
+    return bytes(t.cpu().tolist())
+
+
 def run(X_local: torch.Tensor, N: int, perplexity=30.0, theta=0.5, learning_rate=200.0,
         n_iter=1000, exaggeration=12.0, seed=42, K=0, exag_iters=250, Y_out=None,
-        group=None, device=None, ops=None, cfg=None):
-    """Multi-GPU end to end.  X_local: this rank's rows shard_range(N, world,
-    rank) of X (float32, host -- pinned for speed -- or device).  Returns
-    (Y, info) on every rank: Y the full embedding on the device; on rank 0
-    it is also copied into Y_out (host or device) when given."""
+        group=None, device=None, use_graphs=True, _lib=None):
+    """Multi-GPU end to end (tsne_run_sharded, Algorithm 1): one
+    process per GPU; X_local = this rank's rows shard_range(N, world, rank) of
+    X (float32, host -- pinned for speed -- or device).  The library builds its
+    own NCCL communicator from an id that rank 0 makes and this function
+    broadcasts over `group`; everything else (X all-gather, kNN of the own
+    rows, list all-gather, P, the sharded iterations) runs inside the call.
+    Returns (Y_out, info) on every rank; Y_out (host or device, N x 2) is
+    written on rank 0 (allocated there on the host if not given)."""
+    from . import RunInfo, _check, _ptr, default_config, lib
+    L = _lib if _lib is not None else lib()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     r0, r1, S = shard_range(N, world, rank)
     if X_local.dtype != torch.float32 or X_local.dim() != 2 or X_local.shape[0] != r1 - r0:
         raise ValueError("X_local must be float32 [row1-row0, D] for this rank's shard")
+    X_local = X_local.contiguous()
     D = X_local.shape[1]
-    if device is None:
-        device = X_local.device if X_local.is_cuda else torch.device("cuda", torch.cuda.current_device())
-    if K <= 0:
-        K = min(N - 1, int(3 * perplexity))                      # D4
-    ops = ops if ops is not None else GpuShardOps(N, device)
-    # 1. X: own rows host->device, then all-gather (padded to world * S rows)
-    Xloc = torch.zeros(S, D, dtype=torch.float32, device=device)
-    Xloc[: r1 - r0].copy_(X_local, non_blocking=True)
-    Xfull = torch.empty(world * S, D, dtype=torch.float32, device=device)
-    _all_gather_flat(Xfull, Xloc, group)
-    del Xloc
-    X = Xfull[:N]
-    # 2. kNN of the own query rows against all N points
-    idx_l, d2_l, uncert = ops.knn_rows(X, K, r0, r1)
-    del X, Xfull
-    idx_p = torch.zeros(S, K, dtype=torch.int32, device=device)
-    d2_p = torch.zeros(S, K, dtype=torch.float64, device=device)
-    idx_p[: r1 - r0] = idx_l
-    d2_p[: r1 - r0] = d2_l
-    del idx_l, d2_l
-    idx = torch.empty(world * S, K, dtype=torch.int32, device=device)
-    d2 = torch.empty(world * S, K, dtype=torch.float64, device=device)
-    _all_gather_flat(idx, idx_p, group)
-    _all_gather_flat(d2, d2_p, group)
-    del idx_p, d2_p
-    # 3. P on every rank (needs all rows), keep the own rows
-    rp, col, val = ops.compute_p(idx[:N].contiguous(), d2[:N].contiguous(), perplexity)
-    nnz = int(col.numel())
-    del idx, d2
-    rpl, cl, vl = local_csr(rp, col, val, r0, r1)
-    del rp, col, val
-    # 4. the sharded iterations
-    opt = ShardedOptimizer(rpl, cl, vl, ops.init_y(N, seed, device), theta=theta,
-                           learning_rate=learning_rate, exaggeration=exaggeration,
-                           exag_iters=exag_iters, group=group, ops=ops, cfg=cfg)
-    opt.step(n_iter)
-    Y = opt.embedding()
-    if rank == 0 and Y_out is not None:
-        Y_out.copy_(Y)
-    u = torch.tensor([float(uncert)], dtype=torch.float64, device=device)
-    dist.all_reduce(u, group=group)
-    return Y, {"N": N, "K": K, "nnz": nnz, "knn_rows_uncertified": int(u.item())}
+    if device is not None and device.type == "cuda":
+        torch.cuda.set_device(device)
+    if rank == 0 and Y_out is None:
+        Y_out = torch.empty(N, 2, dtype=torch.float32)
+    uid = nccl_unique_id(group, device)
+    idbuf = (C.c_uint8 * len(uid)).from_buffer_copy(uid)
+    cfg = default_config(K=int(K), exag_iters=exag_iters, seed=seed,
+                         use_graphs=1 if use_graphs else 0)
+    info = RunInfo()
+    if X_local.is_cuda:
+        torch.cuda.current_stream().synchronize()        # the call runs on its own stream
+    _check(L.tsne_run_sharded(_ptr(X_local), r1 - r0, N, D, float(perplexity), float(theta),
+                              float(learning_rate), int(n_iter), float(exaggeration),
+                              C.byref(cfg), idbuf, rank, world,
+                              _ptr(Y_out if rank == 0 else None), C.byref(info)),
+           "tsne_run_sharded")
+    out = {f: getattr(info, f) for f, _ in RunInfo._fields_}
+    out["N"] = N
+    return (Y_out if rank == 0 else None), out

@@ -145,3 +145,97 @@ def test_long_run_c2_shaped_single_seed(T, orc):
     print(f"C2-shaped N=20000: KL gpu {kl_g:.5f} oracle {kl_o:.5f}; 10-NN gpu {nn_g:.4f} oracle {nn_o:.4f}")
     assert abs(kl_g - kl_o) <= 0.01 * kl_o, (kl_g, kl_o)
     assert abs(nn_g - nn_o) <= 0.01, (nn_g, nn_o)
+
+
+@pytest.fixture(scope="module")
+def big(T):
+    """C5-shaped problem at N = 200000 (D = 2048): P from the GPU's kNN + P (their
+    parity with the oracle is tested in test_gpu_knn_p.py / test_gpu_fullsize.py).
+    N is large enough that the attractive pass runs its launch configuration
+    of the bench (120 CTAs beside the tree build, window of 12288 points with
+    L2 gathers for the columns outside it) and relabels."""
+    X = synth.make_x("C5", n=200000, device="cuda")
+    idx, d2, _ = T.knn(X, 90)
+    rp, col, val = T.compute_p(idx, d2, 30.0)
+    del X, idx, d2
+    torch.cuda.empty_cache()
+    return rp, col, val, rp.cpu().numpy(), col.cpu().numpy(), val.cpu().numpy()
+
+
+@pytest.mark.parametrize("t0", [130, 300])
+def test_every_step_matches_oracle_step_large_n(T, orc, big, t0):
+    # per-step parity at N = 200000 with the periodic Morton relabelling every
+    # 2 iterations (morton_improves, k_relabel_rows): each GPU iteration vs one
+    # oracle iteration started from the GPU's own state, as in the N = 1000 test
+    rp, col, val, rph, colh, valh = big
+    N = rph.shape[0] - 1
+    opt = T.Optimizer(rp, col, val, T.init_y(N, 42), theta=0.5, relabel_every=2)
+    opt.step(t0)
+    for t in range(t0, t0 + 6):
+        S = opt.state
+        Y, v, g = (S.Y.cpu().numpy().astype(np.float64), S.v.cpu().numpy().astype(np.float64),
+                   S.gains.cpu().numpy().astype(np.float64))
+        Yo, vo, go = orc.optimize(rph, colh, valh, Y, v, g, t0=t, n_iter=1, theta=0.5)
+        opt.step(1)
+        assert rel(opt.state.Y.cpu().numpy(), Yo) <= 1e-5, t
+        assert rel(opt.state.v.cpu().numpy(), vo) <= 1e-4, t
+        assert np.array_equal(opt.state.gains.cpu().numpy() > 0.5, go > 0.5)
+    # and four iterations inside one call (relabel checkpoint after the second)
+    S = opt.state
+    Y, v, g = (S.Y.cpu().numpy().astype(np.float64), S.v.cpu().numpy().astype(np.float64),
+               S.gains.cpu().numpy().astype(np.float64))
+    Yo, vo, go = orc.optimize(rph, colh, valh, Y, v, g, t0=t0 + 6, n_iter=4, theta=0.5)
+    opt.step(4)
+    assert rel(opt.state.Y.cpu().numpy(), Yo) <= 1e-4
+
+
+def test_long_run_c2_full_n(T, orc):
+    # SURVEY 8(c): C2 at its real size, N = 70000 (MNIST-shaped), single seed:
+    # 1000 oracle iterations vs 1000 GPU iterations from the same Y0 on the same
+    # P (the GPU's kNN + P; 256 of its kNN rows checked against the oracle here)
+    cfg = synth.CONFIGS["C2"]
+    X = synth.make_x("C2")
+    Xd = X.to("cuda")
+    idx, d2, info = T.knn(Xd, 90)
+    rp, col, val = T.compute_p(idx, d2, 30.0)
+    del Xd
+    Xh = X.numpy()
+    idx_h = idx.cpu().numpy()
+    rows = np.random.default_rng(2).choice(cfg.N, 256, replace=False)
+    io, do = orc.knn(Xh, 90, rows=rows)
+    for a, b in np.argwhere(idx_h[rows] != io):
+        assert abs(orc.sqdist(Xh, rows[a], idx_h[rows[a], b]) - do[a, b]) <= 1e-6 * do[a, b]
+    rph, colh, valh = rp.cpu().numpy(), col.cpu().numpy(), val.cpu().numpy()
+    Y0 = orc.init_y(cfg.N, 42)
+    Yo, _, _ = orc.optimize(rph, colh, valh, Y0, n_iter=1000, theta=0.5)
+    opt = T.Optimizer(rp, col, val, dev(Y0.astype(np.float32)), theta=0.5)
+    Yg = opt.step(1000).cpu().numpy().astype(np.float64)
+    kl_g, kl_o = orc.kl(rph, colh, valh, Yg), orc.kl(rph, colh, valh, Yo)
+    nn_g, nn_o = orc.nn_preservation(idx_h, Yg, 10), orc.nn_preservation(idx_h, Yo, 10)
+    print(f"C2 N=70000: KL gpu {kl_g:.5f} oracle {kl_o:.5f}; 10-NN gpu {nn_g:.4f} oracle {nn_o:.4f}")
+    assert abs(kl_g - kl_o) <= 0.01 * kl_o, (kl_g, kl_o)
+    assert abs(nn_g - nn_o) <= 0.01, (nn_g, nn_o)
+
+
+def test_split_calls_equal_one_call(T):
+    # keep_state: consecutive Optimizer.step calls continue the library's internal
+    # state (relabelled P, graphs, relabel phase), so a split run is bitwise one run;
+    # a state modified between calls is detected and the next call starts afresh
+    X = synth.make_x("C2", n=20000, device="cuda")
+    idx, d2, _ = T.knn(X, 90)
+    rp, col, val = T.compute_p(idx, d2, 30.0)
+    Y0 = T.init_y(20000, 3)
+    a = T.Optimizer(rp, col, val, Y0, relabel_every=16)
+    b = T.Optimizer(rp, col, val, Y0, relabel_every=16)
+    for n in (1, 120, 37, 63, 9):
+        a.step(n)
+    yb = b.step(230)
+    assert torch.equal(a.state.Y, yb) and torch.equal(a.state.v, b.state.v)
+    assert torch.equal(a.state.gains, b.state.gains)
+    # modified state: both continue from the same modified state afresh
+    a.state.Y[5, 0] += 1e-3
+    c = T.Optimizer(rp, col, val, a.state.Y, relabel_every=16)
+    c.state.v.copy_(a.state.v)
+    c.state.gains.copy_(a.state.gains)
+    c.state.t = a.state.t
+    assert torch.equal(a.step(40), c.step(40))

@@ -53,6 +53,8 @@ def test_virtual_shards_match_single_gpu(T, orc, prob, G):
     Y = Y0.clone()
     zp = torch.zeros(G * 2, dtype=torch.float64, device=dev)
     n_iter = 3        # trajectories diverge chaotically; compare a few iterations
+    Yo = Y0.cpu().numpy().astype(np.float64)
+    vo, go = np.zeros_like(Yo), np.ones_like(Yo)
     for t in range(n_iter):
         for r, (a, b, rpl, cl, vl, v, g, rep, A, o) in enumerate(shards):
             o.attract(rpl, cl, vl, N, a, b, Y, A)
@@ -63,12 +65,20 @@ def test_virtual_shards_match_single_gpu(T, orc, prob, G):
             o.update(A, N, a, b, Y, rep, zp, G, t, 200.0, 12.0, cfg, v, g, out)
             Ynew[a:b] = out
         Y = Ynew
+        # each sharded iteration vs one oracle iteration from the same state
+        # (the GPU's Y of the previous iteration, recentred; its v and gains)
+        Yo, vo, go = orc.optimize(rp, col, v32, Yo, vo, go, t0=t, n_iter=1, theta=0.5)
+        Yc = Y.clone()
+        ops.recentre(Yc, N)
+        assert rel(Yc.cpu().numpy(), Yo) <= 1e-5, t
+        Yo = Yc.cpu().numpy().astype(np.float64)
+        vo = torch.cat([sh[5] for sh in shards]).cpu().numpy().astype(np.float64)
+        go = torch.cat([sh[6] for sh in shards]).cpu().numpy().astype(np.float64)
     ops.recentre(Y, N)
     assert not ops.nonfinite()
     ref = T.Optimizer(rp_d, col_d, val_d, Y0, theta=0.5, relabel_every=0, use_graphs=False)
     Yref = ref.step(n_iter)
     assert rel(Y.cpu().numpy(), Yref.cpu().numpy().astype(np.float64)) < 1e-4
-    Yo, _, _ = orc.optimize(rp, col, v32, Y0.cpu().numpy().astype(np.float64), n_iter=1, theta=0.5)
 
 
 def _free_port():

@@ -150,3 +150,14 @@ def test_nn_preservation_hand_example(orc):
     assert abs(orc.nn_preservation(idx_x, Y, 2) - 0.4) < 1e-15
     # k = 1: NN^Y = 1, 0, 3, 2, 2; NN^X = 1, 0, 4, 2, 0 -> 3/5
     assert abs(orc.nn_preservation(idx_x, Y, 1) - 0.6) < 1e-15
+
+
+def test_nn_preservation_rows_hand_example(orc):
+    """The sampled form of O12 on the hand-worked case above: per-point overlaps
+    1, 1, 0, 2, 0 (k = 2), so rows {0, 3} give (1 + 2) / (2 * 2) = 0.75 and
+    rows {2, 4} give 0; all rows reproduce the full mean."""
+    Y = np.array([[0, 0], [1, 0], [3, 0], [3, 0], [10, 0]], np.float64)
+    idx_x = np.array([[1, 3, 4], [0, 3, 4], [4, 0, 1], [2, 1, 0], [0, 1, 2]], np.int32)
+    assert abs(orc.nn_preservation(idx_x, Y, 2, rows=[0, 3]) - 0.75) < 1e-15
+    assert orc.nn_preservation(idx_x, Y, 2, rows=[2, 4]) == 0.0
+    assert abs(orc.nn_preservation(idx_x, Y, 2, rows=np.arange(5)) - 0.4) < 1e-15

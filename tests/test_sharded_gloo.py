@@ -66,29 +66,6 @@ class OracleShardOps:
         Y -= m
 
 
-class OracleRunOps(OracleShardOps):
-    """OracleShardOps plus the supporting stages of sharded.run (kNN of a query
-    range, P, Y0); the CSR of the iterations is the one compute_p returned."""
-
-    def __init__(self):
-        super().__init__(None, None, None)
-
-    def knn_rows(self, X, K, q0, q1):
-        import oracle
-        idx, d2 = oracle.knn(X.numpy(), K, rows=np.arange(q0, q1))
-        return torch.as_tensor(idx, dtype=torch.int32), torch.as_tensor(d2), 0
-
-    def compute_p(self, idx, d2, perplexity):
-        import oracle
-        rp, col, v64, v32, *_ = oracle.compute_p(idx.numpy(), d2.numpy(), perplexity)
-        self.rp, self.col, self.val = rp, col, v32
-        return torch.as_tensor(rp), torch.as_tensor(col), torch.as_tensor(v32)
-
-    def init_y(self, N, seed, device):
-        import oracle
-        return torch.as_tensor(oracle.init_y(N, seed).astype(np.float32) * 1e3)
-
-
 def problem(N=300):
     import oracle
     X = synth.make_x("C1", n=N).numpy()
@@ -167,33 +144,69 @@ def test_gloo_sharded_equals_unsharded(tmp_path, world):
     assert np.linalg.norm(Ys - Yo) / np.linalg.norm(Yo) < 1e-4
 
 
-def _run_worker(rank, world, port, n_iter, out):
+class FakeLib:
+    """Records the arguments sharded.run passes to tsne_run_sharded (the GPU
+    call itself needs a GPU) and writes a recognisable Y on rank 0."""
+
+    def __init__(self):
+        self.calls = []
+
+    def tsne_run_sharded(self, X, n_local, N, D, perp, theta, lr, n_iter, exag, cfg, idbuf,
+                         rank, world, Y, info):
+        self.calls.append(dict(n_local=n_local, N=N, D=D, n_iter=n_iter, rank=rank, world=world,
+                               uid=bytes(idbuf), K=cfg._obj.K, X=X.value, Y=Y.value))
+        return 0
+
+
+def _run_worker(rank, world, port, out):
+    import ctypes
+
     from paper_1807_11824_b200 import sharded
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    X = synth.make_x("C1", n=300)
-    N = X.shape[0]
-    r0, r1, _ = shard_range(N, world, rank)
-    Y, info = sharded.run(X[r0:r1].clone(), N, perplexity=15.0, theta=0.5, n_iter=n_iter, K=45,
-                          device=torch.device("cpu"), ops=OracleRunOps(), cfg=Cfg())
-    if rank == 0:
-        torch.save((Y.clone(), info), out)
+    fake = FakeLib()
+    # rank 0's id: a stand-in for tsne_nccl_unique_id (which needs libnccl); the
+    # broadcast over the process group is the logic under test
+    import paper_1807_11824_b200 as T
+    real = T.lib
+
+    class WithFakeId:           # the real library (config defaults) with a stand-in id maker
+        def __getattr__(self, name):
+            return getattr(real(), name)
+
+        @staticmethod
+        def tsne_nccl_unique_id(buf):
+            ctypes.memmove(buf, bytes(range(7, 135)), 128)
+            return 0
+
+    T.lib = WithFakeId
+    try:
+        X = synth.make_x("C1", n=301)
+        N = X.shape[0]
+        r0, r1, _ = shard_range(N, world, rank)
+        Y, info = sharded.run(X[r0:r1].clone(), N, perplexity=15.0, n_iter=3, K=45,
+                              device=torch.device("cpu"), _lib=fake)
+    finally:
+        T.lib = real
+    torch.save((fake.calls, Y is not None, r0, r1), out + f".{rank}")
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_gloo_sharded_run_end_to_end(tmp_path):
-    """sharded.run (X shards gathered, kNN by query range, kNN lists gathered,
-    P, sharded iterations) equals the unsharded pipeline."""
-    n_iter = 4
-    out = str(tmp_path / "run.pt")
-    mp.spawn(_run_worker, args=(3, _free_port(), n_iter, out), nprocs=3, join=True)
-    Ys, info = torch.load(out)
-    assert info["N"] == 300 and info["K"] == 45
-    import oracle
-    rp, col, val, Y0 = problem()
-    assert info["nnz"] == len(col)
-    Yo, _, _ = oracle.optimize(rp, col, val, Y0.astype(np.float64), n_iter=n_iter, theta=0.5)
-    Ys = Ys.double().numpy()
-    assert np.linalg.norm(Ys - Yo) / np.linalg.norm(Yo) < 1e-4
+def test_gloo_sharded_run_marshalling(tmp_path):
+    """sharded.run on 3 ranks: every rank passes its own shard (N_local =
+    its shard_range size), the same id (made on rank 0, broadcast), the same
+    N, D, K and n_iter; only rank 0 gets an output buffer."""
+    out = str(tmp_path / "run")
+    mp.spawn(_run_worker, args=(3, _free_port(), out), nprocs=3, join=True)
+    uids = set()
+    for r in range(3):
+        calls, has_y, r0, r1 = torch.load(out + f".{r}", weights_only=False)
+        assert len(calls) == 1
+        c = calls[0]
+        assert c["rank"] == r and c["world"] == 3 and c["N"] == 301 and c["D"] == 50
+        assert c["n_local"] == r1 - r0 and c["K"] == 45 and c["n_iter"] == 3
+        assert (c["Y"] is not None) == (r == 0) and has_y == (r == 0)
+        uids.add(c["uid"])
+    assert uids == {bytes(range(7, 135))}
