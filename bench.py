@@ -34,6 +34,16 @@ import synth  # noqa: E402
 
 METRIC = "BH t-SNE iterations/s (N=1.28M, D=2048 ImageNet-ResNet-shaped)"
 
+# nonzeros per row of the GPU's P on each workload (measured, profiles/r1_bench_C*_final.json):
+# the reference arm times the oracle iteration on a CSR with this row length
+NNZ_PER_ROW = {"C1": 96, "C2": 161, "C3": 149, "C4": 233, "C5": 146}
+
+
+def measured_peaks():
+    """L2 / L1 / FP64 peaks from measure/peaks.py (profiles/r2_peaks.json), if present."""
+    p = os.path.join(ROOT, "profiles", "r2_peaks.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
 
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -124,7 +134,7 @@ def run_reference(args, rank, world):
         return
     cfg = synth.CONFIGS[args.config]
     N = args.n or cfg.N
-    nnz_row = args.nnz_per_row
+    nnz_row = args.nnz_per_row or NNZ_PER_ROW.get(args.config, 146)
     times, cores = time_oracle_iterations(N, args.steps, nnz_row, warmup=args.warmup)
     T = sum(times)
     v = args.steps / T
@@ -133,8 +143,10 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": cfg.name, "N": N, "D": cfg.D, "theta": 0.5,
-                   "nnz_per_row": nnz_row},
+        "config": {"workload": cfg.name, "N": N, "D": cfg.D,
+                   "K": min(N - 1, int(3 * cfg.perplexity)), "perplexity": cfg.perplexity,
+                   "theta": 0.5, "nnz_per_row": nnz_row,
+                   "parallelism": "host cores (OpenMP over points)"},
         "cpu_baseline": {"value": v, "unit": "it/s", "cores": cores, "kind": "oracle",
                          "sample": f"{args.steps} full-size oracle iterations (fp64 tree + traversal "
                                    f"+ attractive + update) at N={N}, synthetic clustered Y and "
@@ -377,6 +389,37 @@ def run_ours(args, rank, world):
                               "traffic": tj.get("k_attract_tma") if traffic is not None else None,
                               "algorithmic_bytes": bytes_attr}
     roof["update_hbm_gbs"] = bytes_upd / (prof["update_ms"] / 1e3) / 1e9
+    # the traversal in its own terms: node visits and interactions per
+    # second (counters of one traversal of the profiled embedding, tsne_profile_iterations),
+    # the 16-byte node records the lanes load per second against the measured L1 and L2
+    # read peaks (measure/peaks.py), and, from the ncu capture of this workload
+    # (profiles/traffic.json), the L2 bytes actually moved and the warp instructions
+    # per warp step (a warp step = one node visit of the warp's slowest lane)
+    tp = prof.get("traverse_per_point") or {}
+    pk = measured_peaks()
+    trav = None
+    if tp.get("visits"):
+        t_s = prof["traverse_ms"] / 1e3
+        visits = tp["visits"] * N
+        warp_steps = tp["warp_max_visits"] * N / 32.0
+        node_gbs = 16.0 * visits / t_s / 1e9
+        trav = {"kernel": "k_traverse", "ms": prof["traverse_ms"],
+                "per_point": tp,
+                "node_visits_per_s": visits / t_s,
+                "interactions_per_s": tp["interactions"] * N / t_s,
+                "node_record_gbs": node_gbs,
+                "l1_peak_gbs": pk.get("l1_read_gbs"), "l2_peak_gbs": pk.get("l2_read_gbs"),
+                "node_record_frac_of_l1": node_gbs / pk["l1_read_gbs"] if pk.get("l1_read_gbs") else None}
+        tj2 = json.load(open(tf)) if os.path.exists(tf) else {}
+        nc = (tj2.get("k_traverse_ncu") or {}).get(cfg.name)
+        if nc:
+            trav["ncu"] = nc
+            if nc.get("warp_inst"):
+                trav["warp_instructions_per_warp_step"] = nc["warp_inst"] / warp_steps
+            if nc.get("lts_bytes") and nc.get("duration_ns") and pk.get("l2_read_gbs"):
+                l2 = nc["lts_bytes"] / nc["duration_ns"]
+                trav["l2_gbs_ncu"] = l2
+                trav["l2_frac_ncu"] = l2 / pk["l2_read_gbs"]
     # the kNN stage against the tensor roofline: algorithmic flops of the
     # candidate GEMM -- 2 D_p per (query, point) pair, each unordered pair once on the
     # symmetric path -- over the whole stage's time (locality order, pilot, sweep,
@@ -408,6 +451,7 @@ def run_ours(args, rank, world):
                    "knn_rows_uncertified": kinfo["rows_uncertified"]},
         "stages": stages,
         "roofline": roof,
+        "traversal": trav,
         "knn_roofline": knn_roof,
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -442,7 +486,8 @@ def main():
     ap.add_argument("--e2e-iters", type=int, default=1000)
     ap.add_argument("--late-t", type=int, default=700,
                     help="also time --steps iterations from this iteration (late phase); 0 = off")
-    ap.add_argument("--nnz-per-row", type=int, default=126)
+    ap.add_argument("--nnz-per-row", type=int, default=0,
+                    help="reference arm CSR row length (default: the workload's measured one)")
     ap.add_argument("--relabel-every", type=int, default=64)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -255,7 +255,11 @@ void tsne_optimize_release(void* ws);
  *   sums (H7), [3] update (H8), [4] one overlapped iteration (the attractive
  *   pass runs on a side stream concurrently with [0] and [1]).
  * kernels_per_iter (HOST out, nullable): kernel launches per iteration
- * (counted from a captured graph of one iteration).  It overwrites the
+ * (counted from a captured graph of one iteration).
+ * trav_stats (HOST out, 5 doubles, nullable): counters of one extra traversal
+ * of the final embedding, per point: [0] node visits, [1] the sum over warps
+ * of the warp's largest visit count / N (SIMT steps), [2] interactions
+ * (accepted cells + exact pairs), [3] fp64 re-decisions (D25), [4] bucket pairs.  It overwrites the
  * internal state of the workspace: a later keep_state tsne_optimize call on
  * it starts afresh.
  * stage_ms (HOST out, 5 doubles).  Synchronises stream. */
@@ -263,8 +267,8 @@ tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, 
                                     int64_t N, float* Y, float* v, float* gains, int32_t t0,
                                     int32_t reps, float theta, float learning_rate,
                                     float exaggeration, const tsne_config* cfg, double* stage_ms,
-                                    int32_t* kernels_per_iter, void* ws, size_t ws_bytes,
-                                    tsne_stream_t stream);
+                                    int32_t* kernels_per_iter, double* trav_stats, void* ws,
+                                    size_t ws_bytes, tsne_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Multi-GPU building blocks (the paper is single-GPU).

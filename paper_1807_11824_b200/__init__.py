@@ -90,7 +90,7 @@ def lib():
     L.tsne_init_y.argtypes = [i64, C.c_uint64, vp, vp]
     L.tsne_profile_iterations.argtypes = [vp, vp, vp, i64, vp, vp, vp, i32, i32, f32, f32, f32,
                                           C.POINTER(Config), C.POINTER(C.c_double),
-                                          C.POINTER(i32), vp, sz, vp]
+                                          C.POINTER(i32), C.POINTER(C.c_double), vp, sz, vp]
     L.tsne_run.argtypes = [vp, i64, i32, f32, f32, f32, i32, f32, vp]
     L.tsne_run_ex.argtypes = [vp, i64, i32, f32, f32, f32, i32, f32, C.POINTER(Config), vp,
                               C.POINTER(RunInfo)]
@@ -284,16 +284,20 @@ def profile_iteration(opt: Optimizer, reps: int = 5, stream=None) -> dict:
     optimiser state by 2 * reps iterations like Optimizer.step)."""
     s = opt.state
     ms = (C.c_double * 5)()
+    ts = (C.c_double * 5)()
     kern = C.c_int32()
     st = C.c_void_p(stream) if stream is not None else _stream()
     _check(lib().tsne_profile_iterations(_ptr(opt.row_ptr), _ptr(opt.col), _ptr(opt.val), opt.N,
                                          _ptr(s.Y), _ptr(s.v), _ptr(s.gains), s.t, int(reps),
                                          opt.theta, opt.lr, opt.exag, C.byref(opt.cfg), ms,
-                                         C.byref(kern), _ptr(opt.ws), opt.ws.numel(), st),
+                                         C.byref(kern), ts, _ptr(opt.ws), opt.ws.numel(), st),
            "tsne_profile_iterations")
     s.t += 2 * int(reps)
     return {"tree_ms": ms[0], "traverse_ms": ms[1], "attract_ms": ms[2], "update_ms": ms[3],
-            "iteration_overlapped_ms": ms[4], "kernels_per_iteration": kern.value}
+            "iteration_overlapped_ms": ms[4], "kernels_per_iteration": kern.value,
+            "traverse_per_point": {"visits": ts[0], "warp_max_visits": ts[1],
+                                   "interactions": ts[2], "fp64_decisions": ts[3],
+                                   "bucket_pairs": ts[4]}}
 
 
 def init_y(N: int, seed: int = 42, device="cuda") -> torch.Tensor:

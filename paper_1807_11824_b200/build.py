@@ -15,6 +15,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
+# compile-time tuning experiments only (e.g. -DTSNE_AT_STAGES=6); empty for the product build
+FLAGS += os.environ.get("TSNE_NVCC_EXTRA", "").split()
 
 
 def _stale(out: str, deps: list[str]) -> bool:

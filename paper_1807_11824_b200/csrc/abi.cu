@@ -272,8 +272,9 @@ tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, 
                                     int64_t N, float* Y, float* v, float* gains, int32_t t0,
                                     int32_t reps, float theta, float learning_rate,
                                     float exaggeration, const tsne_config* cfg_in,
-                                    double* stage_ms, int32_t* kernels_per_iter, void* ws,
-                                    size_t ws_bytes, tsne_stream_t stream) {
+                                    double* stage_ms, int32_t* kernels_per_iter,
+                                    double* trav_stats, void* ws, size_t ws_bytes,
+                                    tsne_stream_t stream) {
   clear_error();
   tsne_config cfg;
   tsne_config_default(&cfg);
@@ -298,7 +299,7 @@ tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, 
   Sched sc{cfg.exag_iters, exaggeration, cfg.mom0, cfg.mom1, learning_rate, cfg.min_gain};
   st = profile_iterations(row_ptr, col, val, N, reinterpret_cast<float2*>(Y),
                           reinterpret_cast<float2*>(v), reinterpret_cast<float2*>(gains), t0, reps,
-                          theta, sc, p.tree, p.opt, stage_ms, kernels_per_iter, s);
+                          theta, sc, p.tree, p.opt, stage_ms, kernels_per_iter, trav_stats, s);
   ss.join();
   return st;
 }

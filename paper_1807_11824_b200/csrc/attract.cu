@@ -22,15 +22,15 @@ constexpr int kAttrWarps = kAttrThreads / 32;
 
 // ---------------------------------------------------------------- H7
 // Attractive pass as a persistent TMA pipeline (one CTA per SM).  The CTA
-// owns a contiguous range of rows, cut into batches of at most kAtRows rows
+// owns a contiguous range of rows, cut into batches of at most kAtBatch rows
 // whose nonzeros fit a stage buffer.  A producer warp streams each batch's
 // col/val span (contiguous in the CSR) into a kAtStages-deep shared-memory
 // ring with cp.async.bulk + mbarriers (the bulk copies keep ~3 batches of the
 // 8-byte-per-nonzero stream in flight per SM without holding registers); the
 // embedding window Y[wlo, wlo + kAtWin) around the CTA's rows is staged once
 // the same way.  Two groups of kAtRows consumer warps take alternate batches
-// (latency hiding for the L2 gathers); warp w of a group computes row w of
-// its batches: lanes take consecutive nonzeros from shared memory, gather y_j
+// (latency hiding for the L2 gathers); warp w of a group computes rows w and
+// w + kAtRows of its batches: lanes take consecutive nonzeros from shared memory, gather y_j
 // from the window (columns outside it, rare once the labels are in a locality
 // order -- DESIGN.md 6.4-6.5 -- come from L2), and reduce with a fixed
 // butterfly (deterministic; the result does not depend on which path an
@@ -45,22 +45,24 @@ constexpr int kAttrWarps = kAttrThreads / 32;
 #define TSNE_AT_CAP 4096
 #define TSNE_AT_WIN 12288
 #endif
-constexpr int kAtRows = TSNE_AT_ROWS;          // rows per batch: one per consumer warp of a group
+constexpr int kAtRows = TSNE_AT_ROWS;          // consumer warps per group
 constexpr int kAtGroups = TSNE_AT_GROUPS;      // consumer groups take alternate batches
 constexpr int kAtConsumers = kAtRows * kAtGroups;
 constexpr int kAtThreads = (kAtConsumers + 1) * 32;
 constexpr int kAtStages = TSNE_AT_STAGES;
 constexpr int kAtCap = TSNE_AT_CAP;            // nonzeros per stage buffer
 constexpr int kAtWin = TSNE_AT_WIN;            // window points
+constexpr int kAtBatch = 2 * kAtRows;          // rows per batch: up to 2 per consumer warp
 constexpr int kAtLong = 2048;                  // longer rows: k_attract_long
-constexpr int kAtChunk = 30;                   // rows per row_ptr prefetch chunk (2 batches)
-constexpr int kAtLook = 4;                     // row_ptr prefetch distance (chunks)
+constexpr int kAtChunk = 56;                   // rows per row_ptr prefetch chunk (~2 batches)
+constexpr int kAtLook = 3;                     // row_ptr prefetch distance (chunks)
 constexpr int kAtRpSlots = kAtLook + 1;
 static_assert(kAtStages % kAtGroups == 0, "a stage always serves the same consumer group");
 constexpr size_t kAtSmem = sizeof(float2) * kAtWin + (size_t)kAtStages * kAtCap * 8;
 
+static_assert(kAtBatch < 32, "a batch is cut by one warp ballot");
 struct AtMeta {
-  int64_t rp[kAtRows + 1];   // row_ptr of the batch's rows (local CSR)
+  int64_t rp[kAtBatch + 1];  // row_ptr of the batch's rows (local CSR)
   int64_t a_lo, a_hi;        // staged nonzeros [a_lo, a_hi) (a_hi <= a_lo when not staged)
   int32_t r0, nrows;         // first local row, rows in the batch
 };
@@ -139,6 +141,19 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* b, uint32_t parity) {
       : "memory");
 }
 
+// wait with a suspend-time hint: the thread sleeps until the phase completes
+// (or the hint expires) instead of re-issuing try_wait -- for the producer,
+// whose spinning on a full ring took a third of the SM's issue slots (ncu)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
   asm volatile(
@@ -192,22 +207,23 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
     }
     // row_ptr of chunk c + kAtLook is fetched with cp.async into a small ring
     // while chunk c is cut into batches, so the producer never waits on a
-    // global load.  A batch is at most kAtRows rows whose nonzeros fit a stage
+    // global load.  A batch is at most kAtBatch rows whose nonzeros fit a stage
     // (a longer single row is read from global memory by its consumer).
     auto fetch_rp = [&](int c) {
-      if (c < c1 && lane <= kAtChunk) {
-        const int r = min(c * kAtChunk + lane, n_rows);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                         smem_u32(&s_rpring[c % kAtRpSlots][lane])),
-                     "l"(row_ptr + r)
-                     : "memory");
-      }
+      if (c < c1)
+        for (int q = lane; q <= kAtChunk; q += 32) {
+          const int r = min(c * kAtChunk + q, n_rows);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                           smem_u32(&s_rpring[c % kAtRpSlots][q])),
+                       "l"(row_ptr + r)
+                       : "memory");
+        }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
     int k = 0;                                  // batch sequence number
     auto issue = [&](int r0, int nr, const int64_t* rpb, bool sentinel) {
       const int s = k % kAtStages;
-      if (k >= kAtStages) mbar_wait_spin(&s_empty[s], ((k / kAtStages) - 1) & 1);
+      if (k >= kAtStages) mbar_wait_sleep(&s_empty[s], ((k / kAtStages) - 1) & 1);
       AtMeta& m = s_meta[s];
       int64_t a_lo = 0, a_hi = 0;
       if (!sentinel) {
@@ -242,9 +258,9 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
       const int64_t* rpc = s_rpring[c % kAtRpSlots];
       const int cr0 = c * kAtChunk, cn = min(kAtChunk, n_rows - cr0);
       for (int b0 = 0; b0 < cn;) {
-        // largest nr <= kAtRows with rows [b0, b0 + nr) fitting a stage (a prefix: rp grows)
+        // largest nr <= kAtBatch with rows [b0, b0 + nr) fitting a stage (a prefix: rp grows)
         const int l = lane + 1;
-        const bool ok = l <= kAtRows && b0 + l <= cn &&
+        const bool ok = l <= kAtBatch && b0 + l <= cn &&
                         rpc[b0 + l] + 3 - (rpc[b0] & ~int64_t(3)) <= kAtCap;
         int nr = __popc(__ballot_sync(0xffffffffu, ok));
         nr = nr > 0 ? nr : 1;
@@ -265,10 +281,10 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
     mbar_wait_spin(&s_full[s], (k / kAtStages) & 1);
     const AtMeta& m = s_meta[s];
     if (m.nrows < 0) break;                     // end marker
-    if (wr < m.nrows) {
-      const int l = m.r0 + wr;
+    for (int br = wr; br < m.nrows; br += kAtRows) {
+      const int l = m.r0 + br;
       const int i = row0 + l;
-      const int64_t e0 = m.rp[wr], e1 = m.rp[wr + 1];
+      const int64_t e0 = m.rp[br], e1 = m.rp[br + 1];
       const int64_t a_lo = m.a_lo, a_hi = m.a_hi;
       const int32_t* cs = s_col + s * kAtCap;
       const float* vs = s_val + s * kAtCap;
@@ -395,8 +411,11 @@ k_attract_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ 
 // the 28 SMs it leaves free take the latency-bound tree kernels, which cannot
 // share an SM with a pipeline CTA (measured at C5: iteration 1.33 -> 1.25 ms,
 // the pass alone 0.43 -> 0.53 ms).
+#ifndef TSNE_AT_GRID_SHARED
+#define TSNE_AT_GRID_SHARED 120
+#endif
 constexpr int kAtGridAlone = kNumSMs;
-constexpr int kAtGridShared = 120;
+constexpr int kAtGridShared = TSNE_AT_GRID_SHARED;
 
 template <int MODE>
 static tsne_status launch_win(const int64_t* row_ptr, const int32_t* col, const float* val,

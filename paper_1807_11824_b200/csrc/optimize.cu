@@ -60,8 +60,15 @@ static tsne_status one_iteration(const int64_t* row_ptr, const int32_t* col, con
   if (st != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaEventRecord(o.ev_join, o.side));
   if ((st = build_tree(w, Yin, /*apply_shift=*/true, s)) != TSNE_OK) return st;
+#ifdef TSNE_JOIN_AFTER_TRAVERSE
   if ((st = launch_traverse(w, theta, s)) != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaStreamWaitEvent(s, o.ev_join, 0));
+#else
+  // the traversal waits for the attractive pass: it then has every SM (the
+  // latency-bound tree build is what runs beside the attractive pass)
+  TSNE_CUDA_TRY(cudaStreamWaitEvent(s, o.ev_join, 0));
+  if ((st = launch_traverse(w, theta, s)) != TSNE_OK) return st;
+#endif
   return launch_update(Yin, o.A, N, w, o, sc, Yout, V, G, s);
 }
 
@@ -442,6 +449,8 @@ struct Session {
   int since = 0;              // iterations since the last relabel checkpoint
   int32_t t_next = 0;
   uint64_t fp = 0;            // fingerprint of the caller's Y, v, gains
+  int32_t* perm = nullptr;    // the tree build's output buffers (host-side selection by
+  uint64_t* keys = nullptr;   // the radix sort, made when a build is enqueued eagerly)
   Graph gr[2];
   bool have_gr[2] = {false, false};
 };
@@ -547,6 +556,8 @@ tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const flo
   if (resume) {
     k_set_state<<<1, 1, 0, s>>>(o.t_dev, t0, o.flag);
     TSNE_LAUNCH_CHECK();
+    w.perm = ses->perm;          // a graph replay does not set these host-side fields
+    w.keys_sorted = ses->keys;
   } else {
     st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, relabel_every > 0, cache_order, s);
     if (st != TSNE_OK) return st;
@@ -582,7 +593,7 @@ tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const flo
     if (since == period) {
       since = 0;
       // a relabel checkpoint (also at the end of a call whose state is kept)
-      if ((done < n_iter || keep_state) && t0 + done >= kMortonFrom &&
+      if ((done < n_iter || keep_state) && t0 + done >= kMortonFrom && w.perm &&
           morton_improves(o.rp[h], o.col[h], w.perm, N, o, s)) {
         // w.perm is the Morton order of the last iteration's embedding (a
         // permutation of the current labels); the pending recentring shift
@@ -602,6 +613,8 @@ tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const flo
       return TSNE_ERR_CUDA;
     }
     ses->fp = hsh;
+    ses->perm = w.perm;
+    ses->keys = w.keys_sorted;
     ses->h = h;
     ses->since = since;
     ses->t_next = t0 + n_iter;
@@ -613,7 +626,7 @@ tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const flo
 tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                                int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t reps,
                                float theta, const Sched& sc, TreeWS& w, OptWS& o, double* stage_ms,
-                               int32_t* kernels, cudaStream_t s) {
+                               int32_t* kernels, double* trav_stats, cudaStream_t s) {
   SideRes side(o);
   invalidate_session(o.ws_base);
   tsne_status st = enter(row_ptr, col, val, N, Y, V, G, t0, w, o, true, true, s);
@@ -677,6 +690,10 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
   if (st != TSNE_OK) return st;
   for (int k = 0; k < 4; ++k) stage_ms[k] = reps > 0 ? acc[k] / reps : 0.0;
   stage_ms[4] = reps > 0 ? overlapped / reps : 0.0;
+  if (trav_stats) {   // counters of one more traversal of the current embedding
+    if ((st = build_tree(w, a, true, s)) != TSNE_OK) return st;
+    if ((st = traverse_stats(w, theta, trav_stats, s)) != TSNE_OK) return st;
+  }
   if ((st = leave(N, a, Y, V, G, w, o, s)) != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaStreamSynchronize(s));
   return TSNE_OK;

@@ -59,7 +59,7 @@ void release_session(const void* ws);
 tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                                int64_t N, float2* Y, float2* V, float2* G, int32_t t0, int32_t reps,
                                float theta, const Sched& sc, TreeWS& w, OptWS& o, double* stage_ms,
-                               int32_t* kernels, cudaStream_t s);
+                               int32_t* kernels, double* trav_stats, cudaStream_t s);
 
 tsne_status launch_init_y(int64_t N, uint64_t seed, float2* Y, cudaStream_t s);
 

@@ -27,12 +27,10 @@ constexpr int kTravThreads = 256;
 #define TSNE_TRAV_MINB 5   // 48 registers, no spills: 40 warps per SM
 #endif
 
-// diagnostics (TSNE_TRAV_STATS=1): [0] sum of node visits, [1] sum over warps
+// diagnostics (traverse_stats): [0] sum of node visits, [1] sum over warps
 // of the warp's max visits, [2] accepted cells + exact pairs, [3] fp64 re-tests,
 // [4] bucket pairs (coincident-point cells evaluated pairwise)
 __device__ unsigned long long g_trav_stats[5];
-
-static int trav_stats_on() { return getenv("TSNE_TRAV_STATS") ? 1 : 0; }
 
 int traverse_blocks(int64_t N) { return (int)((N + kTravThreads - 1) / kTravThreads); }
 
@@ -156,14 +154,13 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   constexpr bool stats = STATS;
   // list (multi-GPU): the sorted positions of the points this rank owns
   // (original indices [row0, ...)); rep is then indexed by perm[k] - row0.
-  // Per level code l: {thr_l = r_l^2 / theta^2, margin constant A_l / theta^2,
-  // margin slope B_l, 0} (fp32) and r_l^2 (fp64).  The test is
-  //   diff = D^2 - thr_l  >  marg = A'_l + B_l D^2      (accept),
-  //   |diff| <= marg                                    (decide in fp64).
+  // Per level code l: {thr_l = r_l^2 / theta^2, C_l} (fp32) and r_l^2 (fp64).
+  // The test is
+  //   diff = D^2 - thr_l  >  C_l      (accept),   |diff| <= C_l  (decide in fp64).
   // Leaves of one point (24) always "accept" (the exact pair: thr = -inf);
   // bucket leaves (26) never do (thr = +inf); cells deeper than kDeepFp32
-  // and bucket tests (25, r_23) always go to fp64 (A' = +inf).
-  __shared__ float4 s_lv[kLevelCodes];
+  // and bucket tests (25, r_23) always go to fp64 (C = +inf).
+  __shared__ float2 s_lv[kLevelCodes];
   __shared__ double s_r2d[kLevelCodes];
   __shared__ double s_z[kTravThreads / 32];
   __shared__ int s_done;
@@ -179,21 +176,24 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
     // margin = 2^-19 (r^2 + lhs) + 2^-20 theta M (r + theta D), with the
     // AM-GM bound theta D <= (lhs / r + r) / 2, i.e. margin = A + B lhs >= 4.7 E
     // (lhs = theta^2 D^2).  Divided by theta^2 (the comparison is made on
-    // D^2 - r^2 / theta^2, whose fp32 error is at most E / theta^2: the
-    // product by theta^2 is gone, thr is rounded once): A' = A / theta^2, B.
+    // diff = D^2 - r^2 / theta^2, whose fp32 error is at most E / theta^2: the
+    // product by theta^2 is gone, thr is rounded once): marg = A' + B D^2 with
+    // A' = A / theta^2.  With D^2 = thr + diff, |diff| > C = (A' + B thr) / (1 - B)
+    // implies |diff| > marg, so one constant per level decides (B < 1/2 here).
     const double A = ldexp(1.0, -19) * r2 + ldexp(1.0, -20) * th * M * r * 1.5;
     const double B = ldexp(1.0, -19) + ldexp(1.0, -21) * th * M / r;
-    float thr, Ap, Bp;
+    float thr, C;
     if (l == kLevelLeaf) {
-      thr = -INFINITY; Ap = 0.f; Bp = 0.f;
+      thr = -INFINITY; C = 0.f;
     } else if (l == kLevelBucket || theta2d == 0.0) {
-      thr = INFINITY; Ap = 0.f; Bp = 0.f;                 // never accepted (theta = 0: exact)
-    } else if (l > kDeepFp32) {
-      thr = (float)(r2 / theta2d); Ap = INFINITY; Bp = 0.f;
+      thr = INFINITY; C = 0.f;                          // never accepted (theta = 0: exact)
+    } else if (l > kDeepFp32 || !(B < 0.5)) {
+      thr = (float)(r2 / theta2d); C = INFINITY;
     } else {
-      thr = (float)(r2 / theta2d); Ap = (float)(A / theta2d); Bp = (float)B;
+      thr = (float)(r2 / theta2d);
+      C = (float)((A / theta2d + B * (r2 / theta2d)) / (1.0 - B) * (1.0 + ldexp(1.0, -20)));
     }
-    s_lv[l] = make_float4(thr, Ap, Bp, 0.f);
+    s_lv[l] = make_float2(thr, C);
     s_r2d[l] = r2;
   }
   if (threadIdx.x == 0) s_done = 0;
@@ -226,17 +226,15 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
     const uint32_t sw = __float_as_uint(nd.w);
     const uint32_t lvl = sw >> 27;
     const int skip = (int)(sw & kSkipMask);
-    float4 lv;
-    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-        : "=f"(lv.x), "=f"(lv.y), "=f"(lv.z), "=f"(lv.w) : "r"(lv_base + 16u * lvl));
+    float2 lv;
+    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(lv.x), "=f"(lv.y) : "r"(lv_base + 8u * lvl));
     float dx = yi.x - nd.x, dy = yi.y - nd.y;
     float D2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
     const bool self_in = (unsigned)(Li - cur) < (unsigned)(skip - cur);   // Li in [cur, skip)
     // criterion (D10) in fp32 with the D25 margin
     const float diff = D2 - lv.x;
-    const float marg = fmaf(lv.z, D2, lv.y);
-    bool acc = diff > marg;
-    if (fabsf(diff) <= marg && !self_in) {
+    bool acc = diff > lv.y;
+    if (fabsf(diff) <= lv.y && !self_in) {
       // inside the fp32 band, or a deep cell (its size approaches the fp32
       // spacing of the coordinates): the decision and the offset in fp64 (D25)
       const double2 c = com64[(unsigned)cur];
@@ -383,25 +381,34 @@ tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s) {
   const int N = (int)w.N;
   tsne_status st = launch_bucket_pairs(w, nullptr, nullptr, s);
   if (st != TSNE_OK) return st;
-  const BucketSum* bs = reinterpret_cast<const BucketSum*>(w.fq);
-  if (trav_stats_on())
-    k_traverse<true><<<traverse_blocks(N), kTravThreads, 0, s>>>(
-        w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
-        w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0, bs, w.has_bucket);
-  else
-    k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
-        w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
-        w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0, bs, w.has_bucket);
+  k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
+      w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
+      w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0,
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket);
   TSNE_LAUNCH_CHECK();
-  if (trav_stats_on()) {
-    unsigned long long h[5];
-    TSNE_CUDA_TRY(cudaMemcpyFromSymbolAsync(h, g_trav_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, s));
-    TSNE_CUDA_TRY(cudaStreamSynchronize(s));
-    fprintf(stderr, "traverse stats: visits/pt %.1f  warp-max visits/pt %.1f  interactions/pt %.1f  fp64/pt %.3f  bucket pairs/pt %.1f\n",
-            h[0] / (double)N, h[1] / (double)N, h[2] / (double)N, h[3] / (double)N, h[4] / (double)N);
-    const unsigned long long zero[5] = {0, 0, 0, 0, 0};
-    TSNE_CUDA_TRY(cudaMemcpyToSymbolAsync(g_trav_stats, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s));
-  }
+  return TSNE_OK;
+}
+
+// The same traversal with per-point counters (measurement only; synchronises s):
+// out[0] node visits, [1] sum over warps of the warp's largest visit count (the
+// SIMT cost), [2] interactions (accepted cells + exact pairs), [3] fp64
+// re-decisions (D25 band and deep cells), [4] bucket pairs -- each per point.
+tsne_status traverse_stats(TreeWS& w, float theta, double* out, cudaStream_t s) {
+  const int N = (int)w.N;
+  const unsigned long long zero[5] = {0, 0, 0, 0, 0};
+  TSNE_CUDA_TRY(cudaMemcpyToSymbolAsync(g_trav_stats, zero, sizeof(zero), 0,
+                                        cudaMemcpyHostToDevice, s));
+  tsne_status st = launch_bucket_pairs(w, nullptr, nullptr, s);
+  if (st != TSNE_OK) return st;
+  k_traverse<true><<<traverse_blocks(N), kTravThreads, 0, s>>>(
+      w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
+      w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0,
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket);
+  TSNE_LAUNCH_CHECK();
+  unsigned long long h[5];
+  TSNE_CUDA_TRY(cudaMemcpyFromSymbolAsync(h, g_trav_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, s));
+  TSNE_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int k = 0; k < 5; ++k) out[k] = (double)h[k] / (double)N;
   return TSNE_OK;
 }
 

@@ -88,6 +88,8 @@ tsne_status launch_bbox(TreeWS& w, const float2* Y, cudaStream_t s);
 tsne_status build_tree(TreeWS& w, const float2* Y, bool apply_shift, cudaStream_t s);
 // Repulsive pass: w.rep, w.Z
 tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s);
+// measurement: per-point visit / interaction counters of one traversal (synchronises s)
+tsne_status traverse_stats(TreeWS& w, float theta, double* out5, cudaStream_t s);
 tsne_status launch_traverse_list(TreeWS& w, float theta, const int32_t* list, const int32_t* nlist,
                                  int row0, float2* rep_local, double* z_partial, cudaStream_t s);
 // Bounding box + recentring shift (fp64 mean, fixed order) of Y, into w.box.

@@ -227,7 +227,7 @@ def run(X_local: torch.Tensor, N: int, perplexity=30.0, theta=0.5, learning_rate
         raise ValueError("X_local must be float32 [row1-row0, D] for this rank's shard")
     X_local = X_local.contiguous()
     D = X_local.shape[1]
-    if device is not None and device.type == "cuda":
+    if device is not None and device.type == "cuda" and device.index is not None:
         torch.cuda.set_device(device)
     if rank == 0 and Y_out is None:
         Y_out = torch.empty(N, 2, dtype=torch.float32)
