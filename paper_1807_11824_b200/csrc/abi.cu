@@ -70,10 +70,7 @@ static size_t opt_plan(void* base, int64_t N, int64_t nnz, OptPlan& p) {
 }
 
 // Zeroes the last-block-done counters of a freshly carved tree workspace.
-static tsne_status init_tree_ws(TreeWS& w, cudaStream_t s) {
-  TSNE_CUDA_TRY(cudaMemsetAsync(w.counter, 0, 8 * sizeof(unsigned), s));
-  return TSNE_OK;
-}
+static tsne_status init_tree_ws(TreeWS& w, cudaStream_t s) { return tree_ws_init(w, s); }
 
 // A private stream ordered after/before `s` (graphs cannot be captured on the
 // legacy default stream).

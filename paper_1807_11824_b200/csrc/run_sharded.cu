@@ -369,7 +369,7 @@ tsne_status tsne_run_sharded(const float* X_local, int64_t N_local, int64_t N, i
     Carver c(p.ws);
     carve_shard(c, w, N);
   }
-  TSNE_CUDA_TRY(cudaMemsetAsync(w.tree.counter, 0, 8 * sizeof(unsigned), s));
+  if ((st = tree_ws_init(w.tree, s)) != TSNE_OK) return st;
   Sched sc{cfg.exag_iters, exaggeration, cfg.mom0, cfg.mom1, learning_rate, cfg.min_gain};
   const bool graphs = cfg.use_graphs != 0;
   for (int32_t t = 0; t < n_iter; ++t) {

@@ -53,8 +53,9 @@ tsne_status shard_forces(ShardWS& w, const float2* Y, int64_t N, int64_t row0, i
   // and applied on the fly by the tree build and by the update of the owned
   // rows (tsne_shard_update), so the attractive pass may read Y concurrently
   TreeWS& t = w.tree;
-  TSNE_CUDA_TRY(cudaMemsetAsync(t.counter, 0, 8 * sizeof(unsigned), s));
-  tsne_status st = recentre ? launch_bbox_mean(t, Y, s) : launch_bbox(t, Y, s);
+  tsne_status st = tree_ws_init(t, s);      // the workspace may be fresh (caller-owned)
+  if (st != TSNE_OK) return st;
+  st = recentre ? launch_bbox_mean(t, Y, s) : launch_bbox(t, Y, s);
   if (st != TSNE_OK) return st;
   if ((st = build_tree(t, Y, /*apply_shift=*/true, s)) != TSNE_OK) return st;
   const int n = (int)N;

@@ -223,8 +223,8 @@ __device__ __forceinline__ uint64_t spread_bits(uint32_t x32) {
 // q = min(2^L-1, max(0, floor((y - lo) * s))) in fp64 without contraction (D8, D9)
 __device__ __forceinline__ uint32_t quantise(float y, double lo, double s) {
   double f = floor(__dmul_rn(__dsub_rn((double)y, lo), s));
-  f = f < 0.0 ? 0.0 : f;
-  f = f > (double)((1u << kLevels) - 1u) ? (double)((1u << kLevels) - 1u) : f;
+  f = f >= 0.0 ? f : 0.0;                                           // (NaN -> 0)
+  f = f <= (double)((1u << kLevels) - 1u) ? f : (double)((1u << kLevels) - 1u);
   return (uint32_t)f;
 }
 
@@ -248,6 +248,11 @@ __global__ void k_keys(const float2* __restrict__ Y, int N, const BoxInfo* __res
   uint32_t qy = quantise(y.y, b.loy, b.s);
   keys[i] = (spread_bits(qx) << 1) | spread_bits(qy);   // quadrant digit = 2 bx + by
   vals[i] = i;
+}
+
+tsne_status tree_ws_init(TreeWS& w, cudaStream_t s) {
+  TSNE_CUDA_TRY(cudaMemsetAsync(w.counter, 0, 8 * sizeof(unsigned), s));
+  return TSNE_OK;
 }
 
 // ---------------------------------------------------------------- gather

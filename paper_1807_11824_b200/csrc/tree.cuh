@@ -79,6 +79,8 @@ struct TreeWS {
 
 // Carve (or size) the tree workspace for N points.
 void carve_tree(Carver& c, TreeWS& w, int64_t N);
+// Zeroes the last-block-done counters of a freshly carved tree workspace.
+tsne_status tree_ws_init(TreeWS& w, cudaStream_t s);
 size_t tree_cub_bytes(int64_t N, size_t* sort_b, size_t* scan_b, size_t* scan2_b);
 
 // Bounding box + root box of Y (shift = 0), written to w.box.

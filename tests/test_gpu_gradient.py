@@ -181,3 +181,27 @@ def test_hand_worked_goldens(T, name):
     dY, Z = gpu_grad(T, rp, col, val, Y, g["theta"], 1.0)
     f0 = -dY[0].astype(np.float64) * Z / 4.0
     np.testing.assert_allclose(f0, g["bh"]["f0"], rtol=2e-6)
+
+
+@pytest.mark.parametrize("case", ["identical_12000", "collapsed_clusters", "dense_cells"])
+def test_dense_cells_and_coincident_points(T, orc, case):
+    # Embeddings whose Morton keys pile up: thousands of coincident points (one
+    # level-24 bucket, D9), clusters collapsed to 1e-5 (deep chains of one-child
+    # cells), many dense cells of a few hundred points, plus a background.
+    rng = np.random.default_rng(11)
+    if case == "identical_12000":         # one bucket of 12000 coincident points + background
+        Y = np.concatenate([np.full((12000, 2), 0.25), rng.normal(0, 10, (8000, 2))])
+    elif case == "collapsed_clusters":    # buckets of ~9000 and ~3000 (merge / CTA paths)
+        c = [rng.normal(m, 1e-5, (n, 2)) for m, n in (((5, 5), 9000), ((-7, 2), 3000),
+                                                       ((1, -8), 600))]
+        Y = np.concatenate(c + [rng.normal(0, 10, (7400, 2))])
+    else:                                 # many buckets of a few hundred points
+        Y = np.concatenate([rng.normal(rng.uniform(-20, 20, 2), 0.02, (300, 2))
+                            for _ in range(60)] + [rng.normal(0, 10, (2000, 2))])
+    Y = Y[rng.permutation(len(Y))].astype(np.float32)
+    N = len(Y)
+    rp, col, v32, _ = synth.random_csr(N, 10, seed=5)
+    g, Z = gpu_grad(T, rp, col, v32, Y, 0.5, 12.0)
+    go, Zo = orc.gradient_bh(rp, col, v32, Y, 0.5, 12.0)
+    assert abs(Z - Zo) <= 1e-6 * Zo
+    assert rel(g, go) <= 1e-4
