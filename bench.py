@@ -261,6 +261,10 @@ def run_ours(args, rank, world):
     torch.cuda.synchronize()
     stages["p_ms"] = a.elapsed_time(b)
     nnz = int(col.numel())
+    # rows of d2 for the oracle's calibration timing (cpu_baseline.e2e_extrapolated)
+    cal_rows = np.random.default_rng(3).choice(N, min(N, 20000), replace=False)
+    d2_sample = d2[torch.as_tensor(cal_rows, device=d2.device)].cpu().numpy() \
+        if (rank == 0 and world == 1 and not args.no_cpu) else None
     del idx, d2
     quality = None
     if e2e is not None and "_Y" in e2e:
@@ -341,11 +345,14 @@ def run_ours(args, rank, world):
 
     # roofline of the dominant kernel
     hbm, which = peaks()
-    # k_attract_tma, algorithmic bytes per launch: col + val (8 B/nnz), row_ptr
+    # k_attract_tma, algorithmic bytes per launch in the 16-bit column format (f1):
+    # column delta + value (6 B/nnz), escaped columns (4 B each), packed row_ptr
     # (8 B/row), y_i (8 B/row), A out (8 B/row); the y_j gathers hit L2 (Y = 10 MB)
-    bytes_attr = 8 * nnz + 8 * (N + 1) + 16 * N
+    nfar = prof.get("attract_escaped_columns", 0)
+    bytes_attr = 6 * nnz + 4 * nfar + 8 * (N + 1) + 16 * N
+    bytes_attr_int32 = 8 * nnz + 8 * (N + 1) + 16 * N       # the int32-column CSR (round 1)
     bytes_upd = 64 * N             # k_update: A, f, y, v, gains in; y', v, gains out
-    stage_kern = {"attract_ms": "k_attract_tma", "traverse_ms": "k_traverse",
+    stage_kern = {"attract_ms": "k_attract_tma_c16", "traverse_ms": "k_traverse",
                   "tree_ms": "tree build (10 kernels)", "update_ms": "k_update"}
     kern = max(stage_kern, key=lambda k: prof[k])
     traffic = None
@@ -360,7 +367,8 @@ def run_ours(args, rank, world):
         ach = bytes_attr / (prof[kern] / 1e3) / 1e9
         roof.update({"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                      "frac": ach / hbm, "traffic": traffic, "peak_source": which,
-                     "algorithmic_bytes": bytes_attr})
+                     "algorithmic_bytes": bytes_attr, "escaped_columns": nfar,
+                     "bytes_vs_int32_csr": bytes_attr / bytes_attr_int32})
     else:
         # k_traverse is issue bound: its roofline is the SM issue rate,
         # 148 SMs x 4 schedulers x 1 warp-instruction per clock at the measured SM clock;
@@ -383,11 +391,14 @@ def run_ours(args, rank, world):
                      "traffic": traffic, "peak_source": "148 SMs x 4 issue/clk x measured SM clock",
                      "warp_instructions_per_launch": inst})
         ach_attr = bytes_attr / (prof["attract_ms"] / 1e3) / 1e9
-        roof["hbm_kernel"] = {"kernel": "k_attract_tma", "kernel_ms": prof["attract_ms"],
+        roof["hbm_kernel"] = {"kernel": "k_attract_tma (16-bit columns)",
+                              "kernel_ms": prof["attract_ms"],
                               "bound": "hbm", "achieved": ach_attr, "peak": hbm, "unit": "GB/s",
                               "frac": ach_attr / hbm,
-                              "traffic": tj.get("k_attract_tma") if traffic is not None else None,
-                              "algorithmic_bytes": bytes_attr}
+                              "traffic": (tj.get("k_attract_tma_c16")
+                                          if cfg.name == "C5-imagenet-resnet-shaped" else None),
+                              "algorithmic_bytes": bytes_attr, "escaped_columns": nfar,
+                              "bytes_vs_int32_csr": bytes_attr / bytes_attr_int32}
     roof["update_hbm_gbs"] = bytes_upd / (prof["update_ms"] / 1e3) / 1e9
     # the traversal in its own terms: node visits and interactions per
     # second (counters of one traversal of the profiled embedding, tsne_profile_iterations),
@@ -463,6 +474,28 @@ def run_ours(args, rank, world):
                                 "kind": "oracle",
                                 "sample": f"{ns} full-size fp64 oracle iteration(s) at N={N} "
                                           f"(synthetic clustered Y, {round(nnz / N)} nnz/row)"}
+        # the oracle end to end, extrapolated: brute-force kNN from
+        # sampled query rows x N / rows, calibration from sampled rows of the GPU's
+        # d2, 1000 iterations at the per-iteration time above; the symmetrisation
+        # (one sort of 2NK edges) is not included, so this is a lower bound
+        import oracle
+        Xh = synth.make_x(cfg, n=N, device=dev).cpu().numpy()
+        qrows = np.random.default_rng(4).choice(N, args.cpu_knn_rows, replace=False)
+        t0 = time.perf_counter()
+        oracle.knn(Xh, K, rows=qrows)
+        knn_s = (time.perf_counter() - t0) * N / len(qrows)
+        del Xh
+        t0 = time.perf_counter()
+        oracle.calibrate(d2_sample, cfg.perplexity)
+        cal_s = (time.perf_counter() - t0) * N / len(d2_sample)
+        it_s = 1000 * sum(times) / ns
+        tot = knn_s + cal_s + it_s
+        line["cpu_baseline"]["e2e_extrapolated"] = {
+            "seconds": tot, "knn_s": knn_s, "calibration_s": cal_s, "iterations_1000_s": it_s,
+            "sample": f"kNN: {len(qrows)} query rows x N/{len(qrows)}; calibration: "
+                      f"{len(d2_sample)} rows x N/{len(d2_sample)}; symmetrisation excluded",
+            "gpu_e2e_seconds": e2e["seconds"] if e2e else None,
+            "ratio_cpu_over_gpu": tot / e2e["seconds"] if e2e else None}
     if e2e is not None:
         e2e.pop("_Y", None)
         line["e2e"] = e2e
@@ -483,6 +516,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--cpu-knn-rows", type=int, default=64)
     ap.add_argument("--e2e-iters", type=int, default=1000)
     ap.add_argument("--late-t", type=int, default=700,
                     help="also time --steps iterations from this iteration (late phase); 0 = off")

@@ -205,3 +205,17 @@ def test_dense_cells_and_coincident_points(T, orc, case):
     go, Zo = orc.gradient_bh(rp, col, v32, Y, 0.5, 12.0)
     assert abs(Z - Zo) <= 1e-6 * Zo
     assert rel(g, go) <= 1e-4
+
+
+def test_error_monotone_in_theta_gpu(T):
+    # S:L271 (error monotone in theta) on the GPU path at N = 20000, against the
+    # exact gradient (theta = 0 reaches every leaf)
+    rp, col, v32, _ = synth.random_csr(20000, 10, seed=9)
+    Y = synth.fixed_y("clustered", 20000, seed=4)
+    g0, Z0 = gpu_grad(T, rp, col, v32, Y, 0.0, 1.0)
+    errs = []
+    for th in (0.1, 0.3, 0.5, 0.8, 1.2):
+        g, Z = gpu_grad(T, rp, col, v32, Y, th, 1.0)
+        errs.append(rel(g, g0))
+    assert all(a < b for a, b in zip(errs, errs[1:])), errs
+    assert errs[0] < 1e-3 and errs[-1] < 0.5
