@@ -345,14 +345,11 @@ def run_ours(args, rank, world):
 
     # roofline of the dominant kernel
     hbm, which = peaks()
-    # k_attract_tma, algorithmic bytes per launch in the 16-bit column format (f1):
-    # column delta + value (6 B/nnz), escaped columns (4 B each), packed row_ptr
+    # k_attract_tma, algorithmic bytes per launch: col + val (8 B/nnz), row_ptr
     # (8 B/row), y_i (8 B/row), A out (8 B/row); the y_j gathers hit L2 (Y = 10 MB)
-    nfar = prof.get("attract_escaped_columns", 0)
-    bytes_attr = 6 * nnz + 4 * nfar + 8 * (N + 1) + 16 * N
-    bytes_attr_int32 = 8 * nnz + 8 * (N + 1) + 16 * N       # the int32-column CSR (round 1)
+    bytes_attr = 8 * nnz + 8 * (N + 1) + 16 * N
     bytes_upd = 64 * N             # k_update: A, f, y, v, gains in; y', v, gains out
-    stage_kern = {"attract_ms": "k_attract_tma_c16", "traverse_ms": "k_traverse",
+    stage_kern = {"attract_ms": "k_attract_tma", "traverse_ms": "k_traverse",
                   "tree_ms": "tree build (10 kernels)", "update_ms": "k_update"}
     kern = max(stage_kern, key=lambda k: prof[k])
     traffic = None
@@ -367,8 +364,7 @@ def run_ours(args, rank, world):
         ach = bytes_attr / (prof[kern] / 1e3) / 1e9
         roof.update({"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                      "frac": ach / hbm, "traffic": traffic, "peak_source": which,
-                     "algorithmic_bytes": bytes_attr, "escaped_columns": nfar,
-                     "bytes_vs_int32_csr": bytes_attr / bytes_attr_int32})
+                     "algorithmic_bytes": bytes_attr})
     else:
         # k_traverse is issue bound: its roofline is the SM issue rate,
         # 148 SMs x 4 schedulers x 1 warp-instruction per clock at the measured SM clock;
@@ -391,14 +387,12 @@ def run_ours(args, rank, world):
                      "traffic": traffic, "peak_source": "148 SMs x 4 issue/clk x measured SM clock",
                      "warp_instructions_per_launch": inst})
         ach_attr = bytes_attr / (prof["attract_ms"] / 1e3) / 1e9
-        roof["hbm_kernel"] = {"kernel": "k_attract_tma (16-bit columns)",
-                              "kernel_ms": prof["attract_ms"],
+        roof["hbm_kernel"] = {"kernel": "k_attract_tma", "kernel_ms": prof["attract_ms"],
                               "bound": "hbm", "achieved": ach_attr, "peak": hbm, "unit": "GB/s",
                               "frac": ach_attr / hbm,
-                              "traffic": (tj.get("k_attract_tma_c16")
+                              "traffic": (tj.get("k_attract_tma")
                                           if cfg.name == "C5-imagenet-resnet-shaped" else None),
-                              "algorithmic_bytes": bytes_attr, "escaped_columns": nfar,
-                              "bytes_vs_int32_csr": bytes_attr / bytes_attr_int32}
+                              "algorithmic_bytes": bytes_attr}
     roof["update_hbm_gbs"] = bytes_upd / (prof["update_ms"] / 1e3) / 1e9
     # the traversal in its own terms: node visits and interactions per
     # second (counters of one traversal of the profiled embedding, tsne_profile_iterations),

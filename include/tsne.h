@@ -253,9 +253,7 @@ void tsne_optimize_release(void* ws);
  * (overlapped) iterations, and reports mean CUDA-event times on `stream`:
  *   stage_ms[0] tree build (H1-H4), [1] traversal (H5-H6), [2] attractive
  *   sums (H7), [3] update (H8), [4] one overlapped iteration (the attractive
- *   pass runs on a side stream concurrently with [0] and [1]); [5] (not a
- *   time) the number of escaped columns of the 16-bit column format the
- *   attractive pass streamed (columns more than 32767 labels from their row).
+ *   pass runs on a side stream concurrently with [0] and [1]).
  * kernels_per_iter (HOST out, nullable): kernel launches per iteration
  * (counted from a captured graph of one iteration).
  * trav_stats (HOST out, 5 doubles, nullable): counters of one extra traversal
@@ -264,7 +262,7 @@ void tsne_optimize_release(void* ws);
  * (accepted cells + exact pairs), [3] fp64 re-decisions (D25), [4] bucket pairs.  It overwrites the
  * internal state of the workspace: a later keep_state tsne_optimize call on
  * it starts afresh.
- * stage_ms (HOST out, 6 doubles).  Synchronises stream. */
+ * stage_ms (HOST out, 5 doubles).  Synchronises stream. */
 tsne_status tsne_profile_iterations(const int64_t* row_ptr, const int32_t* col, const float* val,
                                     int64_t N, float* Y, float* v, float* gains, int32_t t0,
                                     int32_t reps, float theta, float learning_rate,

@@ -283,7 +283,7 @@ def profile_iteration(opt: Optimizer, reps: int = 5, stream=None) -> dict:
     """Per-stage mean CUDA-event times (tsne_profile_iterations; advances the
     optimiser state by 2 * reps iterations like Optimizer.step)."""
     s = opt.state
-    ms = (C.c_double * 6)()
+    ms = (C.c_double * 5)()
     ts = (C.c_double * 5)()
     kern = C.c_int32()
     st = C.c_void_p(stream) if stream is not None else _stream()
@@ -295,7 +295,6 @@ def profile_iteration(opt: Optimizer, reps: int = 5, stream=None) -> dict:
     s.t += 2 * int(reps)
     return {"tree_ms": ms[0], "traverse_ms": ms[1], "attract_ms": ms[2], "update_ms": ms[3],
             "iteration_overlapped_ms": ms[4], "kernels_per_iteration": kern.value,
-            "attract_escaped_columns": int(ms[5]),
             "traverse_per_point": {"visits": ts[0], "warp_max_visits": ts[1],
                                    "interactions": ts[2], "fp64_decisions": ts[3],
                                    "bucket_pairs": ts[4]}}

@@ -129,93 +129,6 @@ __device__ __forceinline__ void row_block(const int32_t* __restrict__ cr,
   for (int u = 0; u < E; ++u) win_accum(yi, y[u], p[u], ax, ay);
 }
 
-// The same for the 16-bit column format (f1): entry q holds d = j - i, or
-// kEsc when |j - i| > 32767, whose column is the next entry of the row's
-// escape list `far` (in row order: the rank of the escape among the row's
-// escapes, from ballots).  ESC = false: the row has no escape.
-constexpr int kEsc = -32768;
-
-template <int E, bool ESC>
-__device__ __forceinline__ void row_block16(const int16_t* __restrict__ cr,
-                                            const float* __restrict__ vr, int n_rem, int self,
-                                            const int32_t* __restrict__ far, int& nesc,
-                                            float2 yi, uint32_t sbase,
-                                            const float2* __restrict__ Y, int wlo, int wn,
-                                            int lane, float& ax, float& ay) {
-  float p[E];
-  float2 y[E];
-  if (ESC) {
-    int c[E];
-#pragma unroll
-    for (int u = 0; u < E; ++u) {
-      const int q = lane + 32 * u;
-      int d = 0;
-      p[u] = 0.f;
-      if (u < E - 1 || q < n_rem) {
-        d = cr[q];
-        p[u] = vr[q];
-      }
-      const bool esc = d == kEsc;
-      const unsigned b = __ballot_sync(0xffffffffu, esc);
-      c[u] = esc ? __ldg(far + nesc + __popc(b & ((1u << lane) - 1u))) : self + d;
-      nesc += __popc(b);
-    }
-#pragma unroll
-    for (int u = 0; u < E; ++u) y[u] = win_y(sbase, Y, c[u], wlo, wn);
-  } else {
-    // no escape in the row: window offset and global address straight from d
-    const int iw = self - wlo;
-    const float2* Yi = Y + self;
-    int d[E];
-#pragma unroll
-    for (int u = 0; u < E; ++u) {
-      const int q = lane + 32 * u;
-      d[u] = 0;
-      p[u] = 0.f;
-      if (u < E - 1 || q < n_rem) {
-        d[u] = cr[q];
-        p[u] = vr[q];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < E; ++u) {
-      const unsigned o = (unsigned)(iw + d[u]);
-      const unsigned oc = min(o, (unsigned)(wn - 1));
-      float2 v;
-      asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(sbase + oc * 8u));
-      asm("{\n\t.reg .pred p;\n\tsetp.ge.u32 p, %2, %3;\n\t@p ld.global.nc.v2.f32 {%0, %1}, [%4];\n\t}"
-          : "+f"(v.x), "+f"(v.y)
-          : "r"(o), "r"((unsigned)wn), "l"(Yi + d[u]));
-      y[u] = v;
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < E; ++u) win_accum(yi, y[u], p[u], ax, ay);
-}
-
-template <bool ESC>
-__device__ __forceinline__ void row_blocks16(const int16_t* __restrict__ cr,
-                                             const float* __restrict__ vr, int n, int self,
-                                             const int32_t* __restrict__ far, float2 yi,
-                                             uint32_t sbase, const float2* __restrict__ Y,
-                                             int wlo, int wn, int lane, float& ax, float& ay) {
-  int nesc = 0;
-  int b = 0;
-  for (; n - b > 8 * 32; b += 8 * 32)
-    row_block16<8, ESC>(cr + b, vr + b, n - b, self, far, nesc, yi, sbase, Y, wlo, wn, lane, ax, ay);
-  switch ((n - b + 31) >> 5) {
-#define TSNE_RB16(e)                                                                          \
-  case e:                                                                                    \
-    row_block16<e, ESC>(cr + b, vr + b, n - b, self, far, nesc, yi, sbase, Y, wlo, wn, lane, \
-                        ax, ay);                                                             \
-    break;
-    TSNE_RB16(1) TSNE_RB16(2) TSNE_RB16(3) TSNE_RB16(4)
-    TSNE_RB16(5) TSNE_RB16(6) TSNE_RB16(7) TSNE_RB16(8)
-#undef TSNE_RB16
-    default: break;
-  }
-}
-
 // spin wait (no suspend-time hint: the pipeline's waits are short and a
 // sleeping producer would throttle the stream)
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* b, uint32_t parity) {
@@ -251,26 +164,19 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 
 // MODE 0: out[l] = A_l.  MODE 1 (tsne_gradient): out[l] = 4 (alpha A_l - f_l / Z).
 // Rows l in [0, n_rows) of the (local) CSR are global points row0 + l of Y.
-// CT = int32_t: plain CSR (row_ptr, col).  CT = int16_t: the 16-bit format of
-// the optimiser's internal CSR (f1): row_ptr[r] = (escape start of row r) << 32
-// | (first entry of row r), col = 16-bit deltas, far = escaped columns.
-template <int MODE, class CT>
+template <int MODE>
 __global__ void __launch_bounds__(kAtThreads, 1)
-k_attract_tma(const int64_t* __restrict__ row_ptr, const CT* __restrict__ col,
-              const float* __restrict__ val, const int32_t* __restrict__ far,
-              const float2* __restrict__ Y, int Ny, int row0,
+k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+              const float* __restrict__ val, const float2* __restrict__ Y, int Ny, int row0,
               int n_rows, float2* __restrict__ out, const float2* __restrict__ rep,
               const double* __restrict__ Z, float alpha) {
-  constexpr bool C16 = sizeof(CT) == 2;
-  constexpr int64_t kAl = C16 ? 8 : 4;               // entries per 16 bytes of col
-  auto lo = [](int64_t x) -> int64_t { return C16 ? (x & 0xffffffffll) : x; };
   extern __shared__ __align__(128) unsigned char at_smem[];
   __shared__ AtMeta s_meta[kAtStages];
   __shared__ __align__(16) int64_t s_rpring[kAtRpSlots][kAtChunk + 1];
   __shared__ __align__(8) uint64_t s_full[kAtStages], s_empty[kAtStages], s_win;
   float2* s_y = reinterpret_cast<float2*>(at_smem);
-  unsigned char* s_colb = at_smem + sizeof(float2) * kAtWin;   // kAtCap x 4 bytes per stage
-  float* s_val = reinterpret_cast<float*>(s_colb + (size_t)kAtStages * kAtCap * 4);
+  int32_t* s_col = reinterpret_cast<int32_t*>(at_smem + sizeof(float2) * kAtWin);
+  float* s_val = reinterpret_cast<float*>(s_col + kAtStages * kAtCap);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // this CTA's rows [lr0, lr1): whole chunks of kAtChunk rows
   const int nch_all = (n_rows + kAtChunk - 1) / kAtChunk;
@@ -294,7 +200,7 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const CT* __restrict__ col,
 
   if (wid == kAtConsumers) {
     // ------------------------------------------------------------ producer
-    const int64_t nnz4 = lo(row_ptr[n_rows]) & ~(kAl - 1);
+    const int64_t nnz4 = row_ptr[n_rows] & ~int64_t(3);
     if (lane == 0) {
       mbar_arrive_tx(&s_win, (uint32_t)(wn * sizeof(float2)));
       bulk_g2s(sbase, Y + wlo, (uint32_t)(wn * sizeof(float2)), &s_win);
@@ -322,10 +228,10 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const CT* __restrict__ col,
       int64_t a_lo = 0, a_hi = 0;
       if (!sentinel) {
         if (lane <= nr) m.rp[lane] = rpb[lane];
-        const int64_t e_lo = lo(rpb[0]), e_hi = lo(rpb[nr]);
-        a_lo = e_lo & ~(kAl - 1);
-        a_hi = min((e_hi + kAl - 1) & ~(kAl - 1), nnz4);
-        if (e_hi + kAl - 1 - a_lo > kAtCap) a_hi = a_lo;      // does not fit: read from global
+        const int64_t e_lo = rpb[0], e_hi = rpb[nr];
+        a_lo = e_lo & ~int64_t(3);
+        a_hi = min((e_hi + 3) & ~int64_t(3), nnz4);
+        if (e_hi + 3 - a_lo > kAtCap) a_hi = a_lo;            // does not fit: read from global
       }
       if (lane == 0) {
         m.a_lo = a_lo;
@@ -336,10 +242,9 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const CT* __restrict__ col,
       __syncwarp();
       if (lane == 0) {
         const uint32_t cnt = (a_hi > a_lo) ? (uint32_t)(a_hi - a_lo) : 0u;
-        mbar_arrive_tx(&s_full[s], cnt * (uint32_t)(sizeof(CT) + 4));
+        mbar_arrive_tx(&s_full[s], cnt * 8u);
         if (cnt) {
-          bulk_g2s(smem_u32(s_colb + (size_t)s * kAtCap * 4), col + a_lo,
-                   cnt * (uint32_t)sizeof(CT), &s_full[s]);
+          bulk_g2s(smem_u32(s_col + s * kAtCap), col + a_lo, cnt * 4u, &s_full[s]);
           bulk_g2s(smem_u32(s_val + s * kAtCap), val + a_lo, cnt * 4u, &s_full[s]);
         }
       }
@@ -356,7 +261,7 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const CT* __restrict__ col,
         // largest nr <= kAtBatch with rows [b0, b0 + nr) fitting a stage (a prefix: rp grows)
         const int l = lane + 1;
         const bool ok = l <= kAtBatch && b0 + l <= cn &&
-                        lo(rpc[b0 + l]) + kAl - 1 - (lo(rpc[b0]) & ~(kAl - 1)) <= kAtCap;
+                        rpc[b0 + l] + 3 - (rpc[b0] & ~int64_t(3)) <= kAtCap;
         int nr = __popc(__ballot_sync(0xffffffffu, ok));
         nr = nr > 0 ? nr : 1;
         issue(cr0 + b0, nr, rpc + b0, false);
@@ -379,31 +284,15 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const CT* __restrict__ col,
     for (int br = wr; br < m.nrows; br += kAtRows) {
       const int l = m.r0 + br;
       const int i = row0 + l;
-      const int64_t e0 = lo(m.rp[br]), e1 = lo(m.rp[br + 1]);
+      const int64_t e0 = m.rp[br], e1 = m.rp[br + 1];
       const int64_t a_lo = m.a_lo, a_hi = m.a_hi;
-      const CT* cs = reinterpret_cast<const CT*>(s_colb + (size_t)s * kAtCap * 4);
+      const int32_t* cs = s_col + s * kAtCap;
       const float* vs = s_val + s * kAtCap;
       const float2 yi = win_y(sbase, Y, i, wlo, wn);
       float ax = 0.f, ay = 0.f;
       const int n = (int)(e1 - e0);
-      if (C16) {
-        const int f0 = (int)((uint64_t)m.rp[br] >> 32);
-        const bool esc = ((uint64_t)m.rp[br + 1] >> 32) != (uint64_t)f0;
-        // (separate calls for shared and global operands: one pointer chosen
-        // between the two would make every load a generic one)
-        if (e0 >= a_lo && e1 <= a_hi) {
-          const int16_t* cr = reinterpret_cast<const int16_t*>(cs) + (e0 - a_lo);
-          const float* vr = vs + (e0 - a_lo);
-          if (esc) row_blocks16<true>(cr, vr, n, i, far + f0, yi, sbase, Y, wlo, wn, lane, ax, ay);
-          else row_blocks16<false>(cr, vr, n, i, far, yi, sbase, Y, wlo, wn, lane, ax, ay);
-        } else if (n <= kAtLong) {
-          const int16_t* cr = reinterpret_cast<const int16_t*>(col) + e0;
-          const float* vr = val + e0;
-          if (esc) row_blocks16<true>(cr, vr, n, i, far + f0, yi, sbase, Y, wlo, wn, lane, ax, ay);
-          else row_blocks16<false>(cr, vr, n, i, far, yi, sbase, Y, wlo, wn, lane, ax, ay);
-        }
-      } else if (e0 >= a_lo && e1 <= a_hi) {      // the row is staged (the common case)
-        const int32_t* cr = reinterpret_cast<const int32_t*>(cs) + (e0 - a_lo);
+      if (e0 >= a_lo && e1 <= a_hi) {             // the row is staged (the common case)
+        const int32_t* cr = cs + (e0 - a_lo);
         const float* vr = vs + (e0 - a_lo);
         // blocks of up to 8 x 32 entries: every gather of a block is issued
         // before any arithmetic, so a row pays the L2 latency of its columns
@@ -423,9 +312,8 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const CT* __restrict__ col,
           default: break;
         }
       } else if (n <= kAtLong) {
-        const int32_t* cg = reinterpret_cast<const int32_t*>(col);
         for (int q = lane; q < n; q += 32)
-          win_accum(yi, win_y(sbase, Y, __ldcs(cg + e0 + q), wlo, wn), __ldcs(val + e0 + q), ax,
+          win_accum(yi, win_y(sbase, Y, __ldcs(col + e0 + q), wlo, wn), __ldcs(val + e0 + q), ax,
                     ay);
       }
       ax = warp_sum(ax);
@@ -529,52 +417,30 @@ k_attract_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ 
 constexpr int kAtGridAlone = kNumSMs;
 constexpr int kAtGridShared = TSNE_AT_GRID_SHARED;
 
-template <int MODE, class CT>
-static tsne_status launch_pipeline(const int64_t* row_ptr, const CT* col, const float* val,
-                                   const int32_t* far, const float2* Y, int64_t Ny, int64_t row0,
-                                   int64_t n_rows, float2* out, const float2* rep, const double* Z,
-                                   float alpha, cudaStream_t s, int grid) {
-  static bool attr = false;                    // not a stream operation (graph-capture safe)
-  if (!attr) {
-    TSNE_CUDA_TRY(cudaFuncSetAttribute(k_attract_tma<MODE, CT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAtSmem));
-    attr = true;
-  }
-  const int64_t nch = (n_rows + kAtChunk - 1) / kAtChunk;
-  const int blocks = (int)(nch < grid ? nch : grid);
-  k_attract_tma<MODE, CT><<<blocks, kAtThreads, kAtSmem, s>>>(row_ptr, col, val, far, Y, (int)Ny,
-                                                               (int)row0, (int)n_rows, out, rep, Z,
-                                                               alpha);
-  TSNE_LAUNCH_CHECK();
-  return TSNE_OK;
-}
-
-static tsne_status launch_long(int MODE, const int64_t* row_ptr, const int32_t* col,
-                               const float* val, const float2* Y, int64_t row0, int64_t n_rows,
-                               float2* out, const float2* rep, const double* Z, float alpha,
-                               cudaStream_t s) {
-  const int64_t lb = (n_rows + kLongThreads - 1) / kLongThreads;
-  const int lblocks = (int)(lb < 2 * kNumSMs ? lb : 2 * kNumSMs);
-  if (MODE == 0)
-    k_attract_long<0><<<lblocks, kLongThreads, 0, s>>>(row_ptr, col, val, Y, (int)row0,
-                                                       (int)n_rows, out, rep, Z, alpha);
-  else
-    k_attract_long<1><<<lblocks, kLongThreads, 0, s>>>(row_ptr, col, val, Y, (int)row0,
-                                                       (int)n_rows, out, rep, Z, alpha);
-  TSNE_LAUNCH_CHECK();
-  return TSNE_OK;
-}
-
 template <int MODE>
 static tsne_status launch_win(const int64_t* row_ptr, const int32_t* col, const float* val,
                               const float2* Y, int64_t Ny, int64_t row0, int64_t n_rows,
                               float2* out, const float2* rep, const double* Z, float alpha,
                               cudaStream_t s, int grid) {
   if (n_rows <= 0) return TSNE_OK;
-  tsne_status st = launch_pipeline<MODE, int32_t>(row_ptr, col, val, nullptr, Y, Ny, row0,
-                                                  n_rows, out, rep, Z, alpha, s, grid);
-  if (st != TSNE_OK) return st;
-  return launch_long(MODE, row_ptr, col, val, Y, row0, n_rows, out, rep, Z, alpha, s);
+  static bool attr = false;                    // not a stream operation (graph-capture safe)
+  if (!attr) {
+    TSNE_CUDA_TRY(cudaFuncSetAttribute(k_attract_tma<MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAtSmem));
+    attr = true;
+  }
+  const int64_t nch = (n_rows + kAtChunk - 1) / kAtChunk;
+  const int blocks = (int)(nch < grid ? nch : grid);
+  k_attract_tma<MODE><<<blocks, kAtThreads, kAtSmem, s>>>(row_ptr, col, val, Y, (int)Ny,
+                                                           (int)row0, (int)n_rows, out, rep, Z,
+                                                           alpha);
+  TSNE_LAUNCH_CHECK();
+  const int64_t lb = (n_rows + kLongThreads - 1) / kLongThreads;
+  const int lblocks = (int)(lb < 2 * kNumSMs ? lb : 2 * kNumSMs);
+  k_attract_long<MODE><<<lblocks, kLongThreads, 0, s>>>(row_ptr, col, val, Y, (int)row0,
+                                                        (int)n_rows, out, rep, Z, alpha);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
 }
 
 __device__ __forceinline__ float sgnf(float x) { return (float)((x > 0.f) - (x < 0.f)); }
@@ -709,16 +575,11 @@ tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, cons
 }
 
 tsne_status launch_attract_sum(const int64_t* row_ptr, const int32_t* col, const float* val,
-                               const float2* Y, int64_t N, int64_t nnz, float2* A, cudaStream_t s,
-                               const int64_t* rpf, const int16_t* c16, const int32_t* far) {
+                               const float2* Y, int64_t N, int64_t nnz, float2* A, cudaStream_t s) {
   // rows of more than ~200 nonzeros (K = 150 workloads): the pass outweighs the tree build
   // it runs beside, so it keeps every SM (C4: 1.73 ms on 148 CTAs, 2.04 ms on 120)
   const int grid = nnz > 200 * N ? kAtGridAlone : kAtGridShared;
-  if (!c16) return launch_win<0>(row_ptr, col, val, Y, N, 0, N, A, nullptr, nullptr, 1.f, s, grid);
-  tsne_status st = launch_pipeline<0, int16_t>(rpf, c16, val, far, Y, N, 0, N, A, nullptr, nullptr,
-                                               1.f, s, grid);
-  if (st != TSNE_OK) return st;
-  return launch_long(0, row_ptr, col, val, Y, 0, N, A, nullptr, nullptr, 1.f, s);
+  return launch_win<0>(row_ptr, col, val, Y, N, 0, N, A, nullptr, nullptr, 1.f, s, grid);
 }
 
 tsne_status launch_update(const float2* Yin, const float2* A, int64_t N, TreeWS& w, OptWS& o,

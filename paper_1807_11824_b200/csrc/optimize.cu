@@ -33,12 +33,8 @@ void carve_opt(Carver& c, OptWS& o, int64_t N, int64_t nnz) {
   for (int h = 0; h < 2; ++h) {
     o.rp[h] = c.take<int64_t>(N + 1);
     o.col[h] = c.take<int32_t>(nnz + 4);
-    o.val[h] = c.take<float>(nnz + 8);
-    o.c16[h] = c.take<int16_t>(nnz + 16);
-    o.far[h] = c.take<int32_t>(nnz + 4);
-    o.rpf[h] = c.take<int64_t>(N + 1);
+    o.val[h] = c.take<float>(nnz + 4);
   }
-  o.fcnt = c.take<int64_t>(N + 1);
   o.len = c.take<int64_t>(N + 1);
   size_t sb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, sb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(N + 1));
@@ -54,13 +50,13 @@ __global__ void k_set_state(int32_t* t_dev, int32_t t0, int32_t* flag) {
 // One iteration: the attractive sums run on a side stream
 // concurrently with the tree build and the traversal (they only need Y);
 // the update joins both.
-static tsne_status one_iteration(int h, int64_t N, float2* Yin, float2* Yout, float2* V,
-                                 float2* G, float theta, const Sched& sc, TreeWS& w, OptWS& o,
+static tsne_status one_iteration(const int64_t* row_ptr, const int32_t* col, const float* val,
+                                 int64_t N, float2* Yin, float2* Yout, float2* V, float2* G,
+                                 float theta, const Sched& sc, TreeWS& w, OptWS& o,
                                  cudaStream_t s) {
   TSNE_CUDA_TRY(cudaEventRecord(o.ev_fork, s));
   TSNE_CUDA_TRY(cudaStreamWaitEvent(o.side, o.ev_fork, 0));
-  tsne_status st = launch_attract_sum(o.rp[h], o.col[h], o.val[h], Yin, N, o.nnz, o.A, o.side,
-                                      o.rpf[h], o.c16[h], o.far[h]);
+  tsne_status st = launch_attract_sum(row_ptr, col, val, Yin, N, o.nnz, o.A, o.side);
   if (st != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaEventRecord(o.ev_join, o.side));
   if ((st = build_tree(w, Yin, /*apply_shift=*/true, s)) != TSNE_OK) return st;
@@ -144,62 +140,6 @@ __global__ void k_scatter_out(int N, const int32_t* __restrict__ lab, const floa
   Gu[o] = G[k];
 }
 
-// ---------------------------------------------------------------- 16-bit columns (f1)
-// After the locality relabelling most columns lie within +-32767 labels of
-// their row: the attractive pass streams them as 16-bit deltas (6 bytes per
-// nonzero with the fp32 value instead of 8); the others are escapes whose
-// column is kept in `far` (row order).
-constexpr int kEscMark = -32768;
-
-__global__ void k_c16_count(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int N,
-                            int64_t* __restrict__ fcnt) {
-  const int lane = threadIdx.x & 31;
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r > N) return;
-  if (r == N) { if (lane == 0) fcnt[N] = 0; return; }
-  int c = 0;
-  for (int64_t e = rp[r] + lane; e < rp[r + 1]; e += 32) {
-    const int d = col[e] - r;
-    c += (d < -32767 || d > 32767);
-  }
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if (lane == 0) fcnt[r] = c;
-}
-
-__global__ void k_c16_write(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int N,
-                            const int64_t* __restrict__ fpos, int16_t* __restrict__ c16,
-                            int32_t* __restrict__ far, int64_t* __restrict__ rpf) {
-  const int lane = threadIdx.x & 31;
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r > N) return;
-  if (lane == 0) rpf[r] = (fpos[r] << 32) | rp[r];
-  if (r == N) return;
-  int64_t f = fpos[r];
-  const int64_t e0 = rp[r], e1 = rp[r + 1];
-  for (int64_t eb = e0; eb < e1; eb += 32) {         // warp-uniform trip count
-    const int64_t e = eb + lane;
-    const bool in = e < e1;
-    const int c = in ? col[e] : r;
-    const int d = c - r;
-    const bool esc = in && (d < -32767 || d > 32767);
-    const unsigned b = __ballot_sync(0xffffffffu, esc);
-    if (in) c16[e] = esc ? (int16_t)kEscMark : (int16_t)d;
-    if (esc) far[f + __popc(b & ((1u << lane) - 1u))] = c;
-    f += __popc(b);
-  }
-}
-
-static tsne_status encode_c16(int h, int N, OptWS& o, cudaStream_t s) {
-  const int blocks = (int)(((int64_t)(N + 1) * 32 + 255) / 256);
-  k_c16_count<<<blocks, 256, 0, s>>>(o.rp[h], o.col[h], N, o.fcnt);
-  TSNE_LAUNCH_CHECK();
-  size_t sb = o.scan_tmp_bytes;
-  TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveSum(o.scan_tmp, sb, o.fcnt, o.len, N + 1, s));
-  k_c16_write<<<blocks, 256, 0, s>>>(o.rp[h], o.col[h], N, o.len, o.c16[h], o.far[h], o.rpf[h]);
-  TSNE_LAUNCH_CHECK();
-  return TSNE_OK;
-}
-
 // Relabel (src P, src state, src lab) -> (P half `dst`, o.Ya/o.V/o.G, o.lab).
 static tsne_status relabel(const int32_t* perm, int N, const int64_t* rp, const int32_t* col,
                            const float* val, const float2* Ys, const float2* Vs, const float2* Gs,
@@ -219,7 +159,7 @@ static tsne_status relabel(const int32_t* perm, int N, const int64_t* rp, const 
   TSNE_CUDA_TRY(cudaMemcpyAsync(o.V, Vn, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
   TSNE_CUDA_TRY(cudaMemcpyAsync(o.G, Gn, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
   TSNE_CUDA_TRY(cudaMemcpyAsync(o.lab, o.lab2, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s));
-  return encode_c16(dst, N, o, s);
+  return TSNE_OK;
 }
 
 // ---------------------------------------------------------------- locality order
@@ -471,8 +411,10 @@ struct Graph {
 static tsne_status capture_pair(Graph& gr, int h, int64_t N, float theta, const Sched& sc,
                                 TreeWS& w, OptWS& o, cudaStream_t s) {
   TSNE_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  tsne_status s1 = one_iteration(h, N, o.Ya, o.Yb, o.V, o.G, theta, sc, w, o, s);
-  tsne_status s2 = (s1 == TSNE_OK) ? one_iteration(h, N, o.Yb, o.Ya, o.V, o.G, theta, sc, w, o, s)
+  tsne_status s1 = one_iteration(o.rp[h], o.col[h], o.val[h], N, o.Ya, o.Yb, o.V, o.G, theta, sc,
+                                 w, o, s);
+  tsne_status s2 = (s1 == TSNE_OK) ? one_iteration(o.rp[h], o.col[h], o.val[h], N, o.Yb, o.Ya,
+                                                   o.V, o.G, theta, sc, w, o, s)
                                    : s1;
   cudaError_t ce = cudaStreamEndCapture(s, &gr.g);
   if (s1 != TSNE_OK) return s1;
@@ -640,7 +582,8 @@ tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const flo
     for (; c < chunk; ++c) {
       float2* a = (c % 2 == 0) ? o.Ya : o.Yb;
       float2* b = (c % 2 == 0) ? o.Yb : o.Ya;
-      if ((st = one_iteration(h, N, a, b, o.V, o.G, theta, sc, w, o, s)) != TSNE_OK)
+      if ((st = one_iteration(o.rp[h], o.col[h], o.val[h], N, a, b, o.V, o.G, theta, sc, w, o,
+                              s)) != TSNE_OK)
         return st;
     }
     if (chunk % 2)
@@ -691,7 +634,7 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
   if (kernels) {  // count kernel nodes of one captured (never launched) iteration
     cudaGraph_t g = nullptr;
     TSNE_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    st = one_iteration(0, N, o.Ya, o.Yb, o.V, o.G, theta, sc, w, o, s);
+    st = one_iteration(o.rp[0], o.col[0], o.val[0], N, o.Ya, o.Yb, o.V, o.G, theta, sc, w, o, s);
     cudaError_t ce = cudaStreamEndCapture(s, &g);
     if (st != TSNE_OK) { if (g) cudaGraphDestroy(g); return st; }
     TSNE_CUDA_TRY(ce);
@@ -720,9 +663,7 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
     cudaEventRecord(e[1], s);
     if (st == TSNE_OK) st = launch_traverse(w, theta, s);
     cudaEventRecord(e[2], s);
-    if (st == TSNE_OK)
-      st = launch_attract_sum(o.rp[0], o.col[0], o.val[0], a, N, o.nnz, o.A, s, o.rpf[0], o.c16[0],
-                              o.far[0]);
+    if (st == TSNE_OK) st = launch_attract_sum(o.rp[0], o.col[0], o.val[0], a, N, o.nnz, o.A, s);
     cudaEventRecord(e[3], s);
     if (st == TSNE_OK) st = launch_update(a, o.A, N, w, o, sc, b, o.V, o.G, s);
     cudaEventRecord(e[4], s);
@@ -737,7 +678,7 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
   double overlapped = 0.0;
   for (int r = 0; r < reps && st == TSNE_OK; ++r) {
     cudaEventRecord(e[0], s);
-    st = one_iteration(0, N, a, b, o.V, o.G, theta, sc, w, o, s);
+    st = one_iteration(o.rp[0], o.col[0], o.val[0], N, a, b, o.V, o.G, theta, sc, w, o, s);
     cudaEventRecord(e[1], s);
     cudaEventSynchronize(e[1]);
     float ms = 0.f;
@@ -749,12 +690,6 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
   if (st != TSNE_OK) return st;
   for (int k = 0; k < 4; ++k) stage_ms[k] = reps > 0 ? acc[k] / reps : 0.0;
   stage_ms[4] = reps > 0 ? overlapped / reps : 0.0;
-  {   // escaped columns of the 16-bit format of the P half the stages used
-    int64_t last = 0;
-    TSNE_CUDA_TRY(cudaMemcpyAsync(&last, o.rpf[0] + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    TSNE_CUDA_TRY(cudaStreamSynchronize(s));
-    stage_ms[5] = (double)((uint64_t)last >> 32);
-  }
   if (trav_stats) {   // counters of one more traversal of the current embedding
     if ((st = build_tree(w, a, true, s)) != TSNE_OK) return st;
     if ((st = traverse_stats(w, theta, trav_stats, s)) != TSNE_OK) return st;

@@ -31,13 +31,6 @@ struct OptWS {
   int64_t* rp[2] = {nullptr, nullptr};
   int32_t* col[2] = {nullptr, nullptr};
   float* val[2] = {nullptr, nullptr};
-  // the 16-bit column format of each half for the attractive pass (f1):
-  // c16 = j - i (or kEsc), far = escaped columns in CSR order, rpf[r] =
-  // (escapes before row r) << 32 | rp[r]
-  int16_t* c16[2] = {nullptr, nullptr};
-  int32_t* far[2] = {nullptr, nullptr};
-  int64_t* rpf[2] = {nullptr, nullptr};
-  int64_t* fcnt = nullptr;               // N+1 escapes per row -> exclusive scan
   int64_t* len = nullptr;                // N+1 row lengths -> scanned row_ptr
   void* scan_tmp = nullptr;
   size_t scan_tmp_bytes = 0;
@@ -49,9 +42,7 @@ tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, cons
                                 const float2* Y, int64_t N, const float2* rep, const double* Z,
                                 float alpha, float2* dY, cudaStream_t s);
 tsne_status launch_attract_sum(const int64_t* row_ptr, const int32_t* col, const float* val,
-                               const float2* Y, int64_t N, int64_t nnz, float2* A, cudaStream_t s,
-                               const int64_t* rpf = nullptr, const int16_t* c16 = nullptr,
-                               const int32_t* far = nullptr);
+                               const float2* Y, int64_t N, int64_t nnz, float2* A, cudaStream_t s);
 tsne_status launch_update(const float2* Yin, const float2* A, int64_t N, TreeWS& w, OptWS& o,
                           const Sched& sc, float2* Yout, float2* V, float2* G, cudaStream_t s);
 
