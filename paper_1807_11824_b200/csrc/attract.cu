@@ -88,6 +88,22 @@ __device__ __forceinline__ float2 win_y(uint32_t sbase, const float2* __restrict
   return v;
 }
 
+// (a, b) summed over the warp with 6 shuffles instead of 10: the first step
+// exchanges a against b between the half-warps, so each half then reduces one
+// value; fixed order, lane 0 ends with both sums (deterministic)
+__device__ __forceinline__ void warp_sum2(float& a, float& b) {
+  const unsigned lane = threadIdx.x & 31u;
+  const bool hi = lane >= 16u;
+  const float send = hi ? a : b;
+  const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+  float v = hi ? b + recv : a + recv;          // lanes < 16: a-sums, lanes >= 16: b-sums
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const float vb = __shfl_sync(0xffffffffu, v, 16);
+  a = v;
+  b = vb;
+}
+
 __device__ __forceinline__ void win_accum(float2 yi, float2 yj, float p, float& ax, float& ay) {
   const float dx = yi.x - yj.x, dy = yi.y - yj.y;
   const float w = rcp_approx_f(fmaf(dy, dy, fmaf(dx, dx, 1.f)));   // 1/(1+d^2), d^2 >= 0
@@ -187,6 +203,7 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
   wlo = min(wlo, Ny - kAtWin);
   wlo = max(wlo, 0) & ~1;                      // 16-byte aligned source
   const int wn = min(kAtWin, Ny - wlo) & ~1;   // 16-byte multiple
+  const bool own_in_win = row0 + lr0 >= wlo && row0 + lr1 <= wlo + wn;
   const uint32_t sbase = smem_u32(s_y);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kAtStages; ++s) {
@@ -288,7 +305,13 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
       const int64_t a_lo = m.a_lo, a_hi = m.a_hi;
       const int32_t* cs = s_col + s * kAtCap;
       const float* vs = s_val + s * kAtCap;
-      const float2 yi = win_y(sbase, Y, i, wlo, wn);
+      float2 yi;                                  // the row's own point: in the window
+      if (own_in_win) {                           // whenever the window covers the CTA's rows
+        asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(yi.x), "=f"(yi.y)
+            : "r"(sbase + (unsigned)(i - wlo) * 8u));
+      } else {
+        yi = win_y(sbase, Y, i, wlo, wn);
+      }
       float ax = 0.f, ay = 0.f;
       const int n = (int)(e1 - e0);
       if (e0 >= a_lo && e1 <= a_hi) {             // the row is staged (the common case)
@@ -316,8 +339,7 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
           win_accum(yi, win_y(sbase, Y, __ldcs(col + e0 + q), wlo, wn), __ldcs(val + e0 + q), ax,
                     ay);
       }
-      ax = warp_sum(ax);
-      ay = warp_sum(ay);
+      warp_sum2(ax, ay);
       if (lane == 0 && n <= kAtLong) {          // longer rows: k_attract_long
         if (MODE == 0) {
           out[l] = make_float2(ax, ay);
