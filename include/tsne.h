@@ -344,6 +344,57 @@ tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, 
                         const tsne_config* cfg, float* Y_out, tsne_run_info* info);
 
 /* ------------------------------------------------------------------------
+ * Approximate kNN by IVF-PQ: the paper's own line-1
+ * algorithm, FAISS's inverted file with product quantisation (Alg. 1,
+ * P:L151; Sec. III-B): |C| = sqrt(N) coarse centroids trained by
+ * k-means, residuals r = x - q1(x) product-quantised into m
+ * sub-vectors of 256 codewords (8-bit codes), and a search that scans the
+ * inverted lists of the tau nearest centroids by the asymmetric distance
+ * ||x - q(y)||^2 (look-up tables).  This build re-ranks the K' best
+ * candidates of each query (kprime below) by their exact fp64 distance,
+ * so d2 holds exact distances of approximately found neighbours (D19).
+ * Deterministic training (D27): the training sample is the points
+ * floor(k N / ntrain), initial centroids the sample rows floor(c ntrain / k),
+ * a fixed number of Lloyd iterations, empty clusters keep their centroid,
+ * ties by index; the seed field is reserved.
+ *   nlist           0 -> round(sqrt(N))
+ *   m               0 -> min(96, ceil(D / 8)); dsub = ceil(D / m) <= 64, the
+ *                   vectors zero-padded to Dp = m dsub dimensions
+ *   kmeans_iters    Lloyd iterations of both quantisers (10)
+ *   train_per_list  ntrain = min(N, nlist * train_per_list) (64)
+ *   kprime          candidates re-ranked per query, 0 -> K + max(64, 5K);
+ *                   rounded up to 32, at most 480
+ * The index is one caller-owned DEVICE buffer of tsne_ivfpq_index_size bytes
+ * (256-byte aligned); tsne_ivfpq_layout gives its parts (byte offsets):
+ *   out[0..3] nlist, m, dsub, Dp; out[4] centroids fp32 [nlist x Dp];
+ *   out[5] codebooks fp32 [m x 256 x dsub]; out[6] codes u8 [N x m] in list
+ *   order; out[7] list offsets int32 [nlist + 1]; out[8] list entries
+ *   (point ids) int32 [N]; out[9] T tables fp32 [nlist x m x 256]
+ *   (T[L][j][k] = |cb_jk|^2 + 2 <c_L,j, cb_jk>); out[10] ntrain.
+ * tsne_ivfpq_search: queries = the N indexed points themselves (the kNN graph
+ * of t-SNE), self excluded; tau in [1, min(nlist, 64)]; lists are probed in
+ * distance order until tau lists are done and at least K' candidates were
+ * seen.  idx [N x K] int32 (-1 if fewer than K were found), d2 [N x K] fp64,
+ * each row ascending by (d2, idx).  X fp32 [N x D] DEVICE.  Errors: TSNE_ERR_ARG,
+ * TSNE_ERR_WORKSPACE, TSNE_ERR_CUDA (also cuBLAS failures).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t nlist, m, kmeans_iters, train_per_list, kprime;
+  uint64_t seed;
+} tsne_ivfpq_params;
+void tsne_ivfpq_params_default(tsne_ivfpq_params* p);
+size_t tsne_ivfpq_index_size(int64_t N, int32_t D, const tsne_ivfpq_params* p);
+tsne_status tsne_ivfpq_layout(int64_t N, int32_t D, const tsne_ivfpq_params* p,
+                              int64_t* out /* HOST, 11 */);
+size_t tsne_ivfpq_workspace_size(int64_t N, int32_t D, int32_t K, const tsne_ivfpq_params* p);
+tsne_status tsne_ivfpq_build(const float* X, int64_t N, int32_t D, const tsne_ivfpq_params* p,
+                             void* index, size_t index_bytes, void* ws, size_t ws_bytes,
+                             tsne_stream_t stream);
+tsne_status tsne_ivfpq_search(const float* X, int64_t N, int32_t D, const tsne_ivfpq_params* p,
+                              const void* index, int32_t K, int32_t tau, int32_t* idx,
+                              double* d2, void* ws, size_t ws_bytes, tsne_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * Algorithm 1 end to end on `world` GPUs, one process per GPU (
  * the paper is single-GPU; its problem statement P:L147-148).  The
  * library owns the NCCL communicator, built from `nccl_unique_id`

@@ -69,6 +69,9 @@ def lib():
                                       i32, i32, f64, f64, f64, i32, f64, f64, f64]
         L.oracle_nn_preservation.argtypes = [P(i32), i32, i64, P(f64), i32]
         L.oracle_nn_preservation.restype = f64
+        L.oracle_ivfpq_search.argtypes = [P(f32), i64, i32, i32, i32, i32, i32, P(f32), P(f32),
+                                          P(i32), P(C.c_uint8), i32, i32, i32, i32, P(i32),
+                                          P(f64)]
         L.oracle_nn_preservation_rows.argtypes = [P(i32), i32, i64, P(f64), i32, P(i64), i64]
         L.oracle_nn_preservation_rows.restype = f64
         L.oracle_run.argtypes = [P(f32), i64, i32, f64, f64, f64, i32, f64, i32, f64, f64, f64,
@@ -288,6 +291,30 @@ def optimize(row_ptr, col, val32, Y, v=None, gains=None, t0=0, n_iter=1, theta=0
     if rc != 0:
         raise ValueError("oracle_optimize rc=%d" % rc)
     return Y, v, gains
+
+
+def ivfpq_search(X, cent, cb, list_of, codes, K, tau, Kc, Pmax=64):
+    """O13 IVF-PQ search given an index: cent [nlist, Dp], cb [m, 256, dsub],
+    list_of [N] (coarse list of each point), codes [N, m] uint8 (by point).
+    Returns idx int32 [N, K] (-1: not found), d2 float64 [N, K] (exact)."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    N, D = X.shape
+    cent = np.ascontiguousarray(cent, dtype=np.float32)
+    cb = np.ascontiguousarray(cb, dtype=np.float32)
+    nlist, Dp = cent.shape
+    m, _, dsub = cb.shape
+    list_of = np.ascontiguousarray(list_of, dtype=np.int32)
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    idx = np.empty((N, K), np.int32)
+    d2 = np.empty((N, K), np.float64)
+    rc = lib().oracle_ivfpq_search(_P(X, C.c_float), N, D, Dp, nlist, m, dsub,
+                                   _P(cent, C.c_float), _P(cb, C.c_float),
+                                   _P(list_of, C.c_int32), _P(codes, C.c_uint8), int(K),
+                                   int(tau), int(Kc), int(Pmax), _P(idx, C.c_int32),
+                                   _P(d2, C.c_double))
+    if rc != 0:
+        raise ValueError("oracle_ivfpq_search rc=%d" % rc)
+    return idx, d2
 
 
 def nn_preservation(idx_x, Y64, k=10, rows=None):

@@ -116,6 +116,99 @@ double oracle_sqdist(const float* X, int32_t D, int64_t i, int64_t j) {
 }
 
 /* ======================================================================
+ * O13  Approximate kNN by IVF-PQ (Alg. 1 line 1),
+ * search given an index (the training is the GPU's; its deterministic
+ * k-means is checked by properties, D27):
+ *   q1(y) = c_{list(y)} (coarse centroid), q2 = product quantisation of the
+ *   residual y - q1(y): sub-vector j (dims [j dsub, (j+1) dsub) of the
+ *   zero-padded Dp = m dsub vector) is codeword cb[j][code_j(y)];
+ *   q(y) = q1(y) + q2(y - q1(y))   (the paper's "q(y) = q1(y) + q2(y - q1(y))").
+ * For query x_i: the centroids in order of ||x - c||^2 (fp64, ties by index);
+ * the lists are scanned in that order until tau lists are done and at least
+ * Kc candidates (points other than i) were seen, or Pmax lists; each candidate
+ * y by the asymmetric distance ||x - q(y)||^2, written out directly in fp64
+ * (the definition, not the look-up-table expansion); the Kc smallest by
+ * (distance, index); then their exact distances ||x_i - x_j||^2 (fp64, the
+ * original D dimensions) and the K smallest by (d2, index).  idx = -1 / d2 =
+ * +inf where fewer than K candidates were found.
+ * ====================================================================== */
+int oracle_ivfpq_search(const float* X, int64_t N, int32_t D, int32_t Dp, int32_t nlist,
+                        int32_t m, int32_t dsub, const float* cent, const float* cb,
+                        const int32_t* list_of, const uint8_t* codes, int32_t K, int32_t tau,
+                        int32_t Kc, int32_t Pmax, int32_t* idx, double* d2) {
+  if (N < 2 || K < 1 || Kc < K || tau < 1 || tau > nlist || m * dsub != Dp || Dp < D)
+    return ORACLE_ERR_ARG;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t i = 0; i < N; ++i) {
+    double* cd = (double*)malloc(sizeof(double) * (size_t)nlist);
+    int32_t* co = (int32_t*)malloc(sizeof(int32_t) * (size_t)nlist);
+    int32_t* cj = (int32_t*)malloc(sizeof(int32_t) * (size_t)Kc);
+    double* ca = (double*)malloc(sizeof(double) * (size_t)Kc);
+    const float* x = X + (size_t)i * D;
+    /* coarse distances and the probe order */
+    for (int32_t c = 0; c < nlist; ++c) {
+      double s = 0.0;
+      for (int32_t e = 0; e < Dp; ++e) {
+        double t = (e < D ? (double)x[e] : 0.0) - (double)cent[(size_t)c * Dp + e];
+        s += t * t;
+      }
+      cd[c] = s;
+      co[c] = c;
+    }
+    for (int32_t a = 1; a < nlist; ++a) {           /* insertion sort by (distance, index) */
+      int32_t v = co[a];
+      int32_t b = a;
+      while (b > 0 && key_less(cd[v], v, cd[co[b - 1]], co[b - 1])) { co[b] = co[b - 1]; --b; }
+      co[b] = v;
+    }
+    /* scan the lists; keep the Kc smallest asymmetric distances */
+    int32_t have = 0;
+    int64_t seen = 0;
+    int32_t P = nlist < Pmax ? nlist : Pmax;
+    for (int32_t p = 0; p < P; ++p) {
+      if (p >= tau && seen >= Kc) break;
+      int32_t L = co[p];
+      for (int64_t y = 0; y < N; ++y) {
+        if (list_of[y] != L || y == i) continue;
+        ++seen;
+        double s = 0.0;
+        for (int32_t e = 0; e < Dp; ++e) {
+          int32_t j = e / dsub;
+          double q = (double)cent[(size_t)L * Dp + e] +
+                     (double)cb[((size_t)j * 256 + codes[(size_t)y * m + j]) * dsub + (e - j * dsub)];
+          double t = (e < D ? (double)x[e] : 0.0) - q;
+          s += t * t;
+        }
+        if (have == Kc && !key_less(s, (int32_t)y, ca[Kc - 1], cj[Kc - 1])) continue;
+        int32_t pos = have < Kc ? have : Kc - 1;
+        while (pos > 0 && key_less(s, (int32_t)y, ca[pos - 1], cj[pos - 1])) {
+          ca[pos] = ca[pos - 1]; cj[pos] = cj[pos - 1]; --pos;
+        }
+        ca[pos] = s; cj[pos] = (int32_t)y;
+        if (have < Kc) ++have;
+      }
+    }
+    /* exact distances of the candidates, the K smallest by (d2, index) */
+    int32_t* oi = idx + (size_t)i * K;
+    double* od = d2 + (size_t)i * K;
+    int32_t got = 0;
+    for (int32_t c = 0; c < have; ++c) {
+      double s = oracle_sqdist(X, D, i, cj[c]);
+      if (got == K && !key_less(s, cj[c], od[K - 1], oi[K - 1])) continue;
+      int32_t pos = got < K ? got : K - 1;
+      while (pos > 0 && key_less(s, cj[c], od[pos - 1], oi[pos - 1])) {
+        od[pos] = od[pos - 1]; oi[pos] = oi[pos - 1]; --pos;
+      }
+      od[pos] = s; oi[pos] = cj[c];
+      if (got < K) ++got;
+    }
+    for (int32_t c = got; c < K; ++c) { oi[c] = -1; od[c] = 1.0 / 0.0; }
+    free(cd); free(co); free(cj); free(ca);
+  }
+  return ORACLE_OK;
+}
+
+/* ======================================================================
  * O2  Conditional affinities p_{j|i} (Eq. 1), restricted to the K
  * neighbours (D2), bandwidth chosen so that the Shannon entropy in nats
  * equals ln(perplexity) (D3; the paper never states the rule).

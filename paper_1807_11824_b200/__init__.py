@@ -35,6 +35,11 @@ class Config(C.Structure):
                 ("keep_state", C.c_int32)]
 
 
+class IvfParams(C.Structure):
+    _fields_ = [("nlist", C.c_int32), ("m", C.c_int32), ("kmeans_iters", C.c_int32),
+                ("train_per_list", C.c_int32), ("kprime", C.c_int32), ("seed", C.c_uint64)]
+
+
 class KnnInfo(C.Structure):
     _fields_ = [("rows_uncertified", C.c_int64), ("candidates", C.c_int32),
                 ("gemm_path", C.c_int32)]
@@ -54,7 +59,9 @@ EXPORTS = ["tsne_last_error", "tsne_abi_version", "tsne_config_default",
            "tsne_run_ex", "tsne_profile_iterations", "tsne_shard_workspace_size",
            "tsne_shard_forces", "tsne_shard_attract", "tsne_shard_update", "tsne_recentre",
            "tsne_kl_workspace_size", "tsne_kl", "tsne_nccl_unique_id", "tsne_run_workspace_size",
-           "tsne_run_sharded"]
+           "tsne_run_sharded", "tsne_ivfpq_params_default", "tsne_ivfpq_index_size",
+           "tsne_ivfpq_layout", "tsne_ivfpq_workspace_size", "tsne_ivfpq_build",
+           "tsne_ivfpq_search"]
 
 
 def lib():
@@ -110,7 +117,18 @@ def lib():
     L.tsne_run_workspace_size.restype = sz
     L.tsne_run_sharded.argtypes = [vp, i64, i64, i32, f32, f32, f32, i32, f32, C.POINTER(Config),
                                    vp, i32, i32, vp, C.POINTER(RunInfo)]
-    for name in ["tsne_nccl_unique_id", "tsne_run_sharded", "tsne_knn", "tsne_knn_rows", "tsne_compute_p", "tsne_gradient", "tsne_optimize", "tsne_init_y",
+    L.tsne_ivfpq_params_default.argtypes = [C.POINTER(IvfParams)]
+    L.tsne_ivfpq_params_default.restype = None
+    L.tsne_ivfpq_index_size.argtypes = [i64, i32, C.POINTER(IvfParams)]
+    L.tsne_ivfpq_index_size.restype = sz
+    L.tsne_ivfpq_layout.argtypes = [i64, i32, C.POINTER(IvfParams), C.POINTER(i64)]
+    L.tsne_ivfpq_workspace_size.argtypes = [i64, i32, i32, C.POINTER(IvfParams)]
+    L.tsne_ivfpq_workspace_size.restype = sz
+    L.tsne_ivfpq_build.argtypes = [vp, i64, i32, C.POINTER(IvfParams), vp, sz, vp, sz, vp]
+    L.tsne_ivfpq_search.argtypes = [vp, i64, i32, C.POINTER(IvfParams), vp, i32, i32, vp, vp, vp,
+                                    sz, vp]
+    for name in ["tsne_ivfpq_layout", "tsne_ivfpq_build", "tsne_ivfpq_search",
+                 "tsne_nccl_unique_id", "tsne_run_sharded", "tsne_knn", "tsne_knn_rows", "tsne_compute_p", "tsne_gradient", "tsne_optimize", "tsne_init_y",
                  "tsne_run", "tsne_run_ex", "tsne_profile_iterations", "tsne_shard_forces",
                  "tsne_shard_attract", "tsne_shard_update", "tsne_recentre", "tsne_kl"]:
         getattr(L, name).restype = C.c_int
@@ -173,6 +191,65 @@ def knn(X: torch.Tensor, K: int, rows=None):
                                    ws.numel(), C.byref(info), _stream()), "tsne_knn_rows")
     return idx, d2, {"rows_uncertified": info.rows_uncertified, "candidates": info.candidates,
                      "gemm_path": {2: "tcgen05-sym", 1: "tcgen05", 0: "none"}[info.gemm_path]}
+
+
+# ---------------------------------------------------------------- f2 IVF-PQ
+def ivfpq_params(**kw) -> IvfParams:
+    p = IvfParams()
+    lib().tsne_ivfpq_params_default(C.byref(p))
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+class IvfPQ:
+    """IVF-PQ index of the rows of X (tsne_ivfpq_build) and its kNN search
+    (tsne_ivfpq_search): queries are the indexed points, self excluded."""
+
+    def __init__(self, X: torch.Tensor, **params):
+        X = _dev(X, torch.float32, "X")
+        self.N, self.D = X.shape
+        self.params = ivfpq_params(**params)
+        nb = lib().tsne_ivfpq_index_size(self.N, self.D, C.byref(self.params))
+        self.index = _ws(nb, X.device)
+        ws = _ws(lib().tsne_ivfpq_workspace_size(self.N, self.D, 0, C.byref(self.params)),
+                 X.device)
+        _check(lib().tsne_ivfpq_build(_ptr(X), self.N, self.D, C.byref(self.params),
+                                      _ptr(self.index), self.index.numel(), _ptr(ws), ws.numel(),
+                                      _stream()), "tsne_ivfpq_build")
+        lay = (C.c_int64 * 11)()
+        _check(lib().tsne_ivfpq_layout(self.N, self.D, C.byref(self.params), lay),
+               "tsne_ivfpq_layout")
+        self.nlist, self.m, self.dsub, self.Dp = lay[0], lay[1], lay[2], lay[3]
+        self._off = list(lay)
+
+    def parts(self) -> dict:
+        """Views of the index parts (tsne_ivfpq_layout): centroids, codebooks,
+        codes (list order), list offsets, list entries, T tables."""
+        b = self.index
+        o = self._off
+
+        def view(off, n, dt):
+            itemsize = torch.empty(0, dtype=dt).element_size()
+            return b[off: off + n * itemsize].view(dt)
+        return {"centroids": view(o[4], self.nlist * self.Dp, torch.float32).view(self.nlist, self.Dp),
+                "codebooks": view(o[5], self.m * 256 * self.dsub, torch.float32).view(self.m, 256, self.dsub),
+                "codes": view(o[6], self.N * self.m, torch.uint8).view(self.N, self.m),
+                "list_offsets": view(o[7], self.nlist + 1, torch.int32),
+                "list_ids": view(o[8], self.N, torch.int32),
+                "T": view(o[9], self.nlist * self.m * 256, torch.float32).view(self.nlist, self.m, 256),
+                "ntrain": o[10]}
+
+    def search(self, X: torch.Tensor, K: int, tau: int):
+        X = _dev(X, torch.float32, "X")
+        idx = torch.empty(self.N, K, dtype=torch.int32, device=X.device)
+        d2 = torch.empty(self.N, K, dtype=torch.float64, device=X.device)
+        ws = _ws(lib().tsne_ivfpq_workspace_size(self.N, self.D, K, C.byref(self.params)),
+                 X.device)
+        _check(lib().tsne_ivfpq_search(_ptr(X), self.N, self.D, C.byref(self.params),
+                                       _ptr(self.index), int(K), int(tau), _ptr(idx), _ptr(d2),
+                                       _ptr(ws), ws.numel(), _stream()), "tsne_ivfpq_search")
+        return idx, d2
 
 
 # ---------------------------------------------------------------- U2 + U3

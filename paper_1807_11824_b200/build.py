@@ -52,7 +52,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
     if force or jobs or _stale(LIB, objs):
-        run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda"])
+        run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda", "-lcublas",
+             "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
     return LIB
 
 
