@@ -215,6 +215,10 @@ typedef struct {
                            to modify row_ptr/col/val in between.  A run split
                            into such calls is bitwise identical to one call.
                            Host resources are freed by tsne_optimize_release. */
+  int32_t knn_tau;      /* tsne_run_ex only (0): 0 = exact kNN (tsne_knn);
+                           > 0 = approximate kNN by IVF-PQ with tau probes and
+                           default index parameters (tsne_ivfpq_*, the paper's
+                           FAISS path).                             */
 } tsne_config;
 
 /* Fills the defaults listed above. */

@@ -32,7 +32,7 @@ class Config(C.Structure):
     _fields_ = [("K", C.c_int32), ("exag_iters", C.c_int32), ("mom0", C.c_float),
                 ("mom1", C.c_float), ("min_gain", C.c_float), ("seed", C.c_uint64),
                 ("Y_init", C.c_void_p), ("use_graphs", C.c_int32), ("relabel_every", C.c_int32),
-                ("keep_state", C.c_int32)]
+                ("keep_state", C.c_int32), ("knn_tau", C.c_int32)]
 
 
 class IvfParams(C.Structure):
@@ -386,9 +386,11 @@ def init_y(N: int, seed: int = 42, device="cuda") -> torch.Tensor:
 # ---------------------------------------------------------------- Algorithm 1
 def run(X: torch.Tensor, perplexity=30.0, theta=0.5, learning_rate=200.0, n_iter=1000,
         exaggeration=12.0, Y_out: torch.Tensor | None = None, Y_init: torch.Tensor | None = None,
-        seed: int = 42, K: int = 0, exag_iters: int = 250, use_graphs=True, relabel_every=64):
+        seed: int = 42, K: int = 0, exag_iters: int = 250, use_graphs=True, relabel_every=64,
+        knn_tau: int = 0):
     """End to end (tsne_run_ex).  X may live on the host (pinned for speed) or
-    the device; Y_out (optional) likewise.  Returns (Y_out, info dict)."""
+    the device; Y_out (optional) likewise.  knn_tau > 0: the kNN by IVF-PQ with
+    tau probes instead of the exact search.  Returns (Y_out, info dict)."""
     if X.dtype != torch.float32:
         raise TsneError("X must be float32")
     X = X.contiguous()
@@ -401,7 +403,8 @@ def run(X: torch.Tensor, perplexity=30.0, theta=0.5, learning_rate=200.0, n_iter
         yi = _dev(Y_init, torch.float32, "Y_init")
     cfg = default_config(K=int(K), exag_iters=exag_iters, seed=seed,
                          Y_init=(yi.data_ptr() if yi is not None else None),
-                         use_graphs=1 if use_graphs else 0, relabel_every=int(relabel_every))
+                         use_graphs=1 if use_graphs else 0, relabel_every=int(relabel_every),
+                         knn_tau=int(knn_tau))
     info = RunInfo()
     if X.is_cuda or Y_out.is_cuda:
         torch.cuda.current_stream().synchronize()   # tsne_run_ex runs on its own stream

@@ -118,6 +118,7 @@ void tsne_config_default(tsne_config* cfg) {
   cfg->use_graphs = 1;
   cfg->relabel_every = 64;
   cfg->keep_state = 0;
+  cfg->knn_tau = 0;
 }
 
 // ---------------------------------------------------------------- gradient
@@ -570,6 +571,12 @@ tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, 
   plan.take<int32_t>(1);
   size_t ws_need = kb > pb ? kb : pb;
   ws_need = ws_need > ob ? ws_need : ob;
+  size_t ivf_idx = 0, ivf_ws = 0;
+  if (cfg.knn_tau > 0) {               // IVF-PQ: the index, then its workspace
+    ivf_idx = (tsne_ivfpq_index_size(N, D, nullptr) + 255) & ~size_t(255);
+    ivf_ws = tsne_ivfpq_workspace_size(N, D, K, nullptr);
+    ws_need = ws_need > ivf_idx + ivf_ws ? ws_need : ivf_idx + ivf_ws;
+  }
   plan.take<char>(ws_need);
   void* mem = nullptr;
   const bool timing = getenv("TSNE_RUN_TIMING") != nullptr;
@@ -615,7 +622,14 @@ tsne_status tsne_run_ex(const float* X, int64_t N, int32_t D, float perplexity, 
     set_error("X contains non-finite values");
     st = TSNE_ERR_ARG;
   }
-  if (st == TSNE_OK) {
+  if (st == TSNE_OK && cfg.knn_tau > 0) {
+    char* ib = static_cast<char*>(ws);
+    st = tsne_ivfpq_build(Xuse, N, D, nullptr, ib, ivf_idx, ib + ivf_idx, ivf_ws,
+                          (tsne_stream_t)s);
+    if (st == TSNE_OK)
+      st = tsne_ivfpq_search(Xuse, N, D, nullptr, ib, K, cfg.knn_tau, idx, d2, ib + ivf_idx,
+                             ivf_ws, (tsne_stream_t)s);
+  } else if (st == TSNE_OK) {
     KnnWS kw; Carver kc(ws); carve_knn(kc, kw, N, D, K);
     st = run_knn(Xuse, N, D, K, 0, N, idx, d2, kw, &kinfo, s);
   }

@@ -101,3 +101,19 @@ def test_recall_against_exact_knn(T):
             rec = r
     assert all(a <= b + 1e-9 for a, b in zip(rec, rec[1:])), rec
     assert rec[2] >= 0.8, rec          # defaults: m = min(96, D/8), K' = K + 5K
+
+
+def test_run_with_ivfpq_knn(T, orc):
+    # tsne_run_ex with the approximate kNN (knn_tau): the embedding's quality
+    # against the exact-kNN pipeline on the same data (exact-Z KL of P_exact)
+    X = synth.make_x("C2", n=8000)
+    Xh = X.pin_memory()
+    Ya, ia = T.run(Xh, perplexity=30.0, n_iter=500, knn_tau=16)
+    Ye, ie = T.run(Xh, perplexity=30.0, n_iter=500)
+    assert torch.isfinite(Ya).all() and ia["nnz"] > 0
+    idx, d2 = orc.knn(X.numpy(), 90)
+    rp, col, v64, v32, *_ = orc.compute_p(idx, d2, 30.0)
+    kla = orc.kl(rp, col, v32, Ya.numpy().astype(np.float64))
+    kle = orc.kl(rp, col, v32, Ye.numpy().astype(np.float64))
+    print("KL (exact P) of the IVF-PQ run %.4f vs exact-kNN run %.4f" % (kla, kle))
+    assert kla < 1.15 * kle
