@@ -52,7 +52,14 @@ constexpr int kAtThreads = (kAtConsumers + 1) * 32;
 constexpr int kAtStages = TSNE_AT_STAGES;
 constexpr int kAtCap = TSNE_AT_CAP;            // nonzeros per stage buffer
 constexpr int kAtWin = TSNE_AT_WIN;            // window points
-constexpr int kAtBatch = 2 * kAtRows;          // rows per batch: up to 2 per consumer warp
+#ifndef TSNE_AT_BATCH
+#define TSNE_AT_BATCH (2 * TSNE_AT_ROWS)
+#endif
+constexpr int kAtBatch = TSNE_AT_BATCH;        // rows per batch: up to 2 per consumer warp
+#ifndef TSNE_AT_EMAX
+#define TSNE_AT_EMAX 8
+#endif
+constexpr int kAtEmax = TSNE_AT_EMAX;          // 32-entry groups of a row loaded together
 constexpr int kAtLong = 2048;                  // longer rows: k_attract_long
 constexpr int kAtChunk = 56;                   // rows per row_ptr prefetch chunk (~2 batches)
 constexpr int kAtLook = 3;                     // row_ptr prefetch distance (chunks)
@@ -237,15 +244,28 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
         }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
+    // row_ptr of local row r from the ring (a chunk's slot holds kAtChunk + 1
+    // entries; the end of the CTA's range at a chunk boundary is the last
+    // entry of the previous chunk)
+    auto rpv = [&](int r) -> int64_t {
+      const int c = r / kAtChunk, o = r - c * kAtChunk;
+      if (r == lr1 && o == 0) return s_rpring[(c - 1) % kAtRpSlots][kAtChunk];
+      return s_rpring[c % kAtRpSlots][o];
+    };
     int k = 0;                                  // batch sequence number
-    auto issue = [&](int r0, int nr, const int64_t* rpb, bool sentinel) {
+    auto issue = [&](int r0, int nr, bool sentinel) {
       const int s = k % kAtStages;
+#ifdef TSNE_AT_SPIN
+      if (k >= kAtStages) mbar_wait_spin(&s_empty[s], ((k / kAtStages) - 1) & 1);
+#else
       if (k >= kAtStages) mbar_wait_sleep(&s_empty[s], ((k / kAtStages) - 1) & 1);
+#endif
       AtMeta& m = s_meta[s];
       int64_t a_lo = 0, a_hi = 0;
       if (!sentinel) {
-        if (lane <= nr) m.rp[lane] = rpb[lane];
-        const int64_t e_lo = rpb[0], e_hi = rpb[nr];
+        const int64_t v = rpv(r0 + min(lane, nr));
+        if (lane <= nr) m.rp[lane] = v;
+        const int64_t e_lo = __shfl_sync(0xffffffffu, v, 0), e_hi = __shfl_sync(0xffffffffu, v, nr);
         a_lo = e_lo & ~int64_t(3);
         a_hi = min((e_hi + 3) & ~int64_t(3), nnz4);
         if (e_hi + 3 - a_lo > kAtCap) a_hi = a_lo;            // does not fit: read from global
@@ -267,25 +287,26 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
       }
       ++k;
     };
+    // Batches are cut across chunk boundaries (a batch of at most kAtBatch <
+    // kAtChunk rows spans at most two chunks), so rows of ~230 nonzeros (C4:
+    // 17 per stage) do not leave a short batch at the end of every chunk.
     for (int j = 0; j < kAtLook; ++j) fetch_rp(c0 + j);
-    for (int c = c0; c < c1; ++c) {
-      fetch_rp(c + kAtLook);
-      asm volatile("cp.async.wait_group %0;" ::"n"(kAtLook) : "memory");
+    int fetched = c0 + kAtLook;                 // next chunk to fetch
+    for (int row = lr0; row < lr1;) {
+      const int c = row / kAtChunk;
+      while (fetched <= c + kAtLook) fetch_rp(fetched++);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kAtLook - 1) : "memory");   // chunks <= c + 1
       __syncwarp();
-      const int64_t* rpc = s_rpring[c % kAtRpSlots];
-      const int cr0 = c * kAtChunk, cn = min(kAtChunk, n_rows - cr0);
-      for (int b0 = 0; b0 < cn;) {
-        // largest nr <= kAtBatch with rows [b0, b0 + nr) fitting a stage (a prefix: rp grows)
-        const int l = lane + 1;
-        const bool ok = l <= kAtBatch && b0 + l <= cn &&
-                        rpc[b0 + l] + 3 - (rpc[b0] & ~int64_t(3)) <= kAtCap;
-        int nr = __popc(__ballot_sync(0xffffffffu, ok));
-        nr = nr > 0 ? nr : 1;
-        issue(cr0 + b0, nr, rpc + b0, false);
-        b0 += nr;
-      }
+      // largest nr <= kAtBatch with rows [row, row + nr) fitting a stage (a prefix: rp grows)
+      const int l = lane + 1;
+      const int64_t base = rpv(row) & ~int64_t(3);
+      const bool ok = l <= kAtBatch && row + l <= lr1 && rpv(min(row + l, lr1)) + 3 - base <= kAtCap;
+      int nr = __popc(__ballot_sync(0xffffffffu, ok));
+      nr = nr > 0 ? nr : 1;
+      issue(row, nr, false);
+      row += nr;
     }
-    for (int g = 0; g < kAtGroups; ++g) issue(0, 0, nullptr, true);   // one end marker per group
+    for (int g = 0; g < kAtGroups; ++g) issue(0, 0, true);   // one end marker per group
     asm volatile("cp.async.wait_all;" ::: "memory");
     return;
   }
@@ -321,17 +342,17 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
         // before any arithmetic, so a row pays the L2 latency of its columns
         // outside the window about once, not once per 32 entries
         int b = 0;
-        for (; n - b > 8 * 32; b += 8 * 32)
-          row_block<8>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay);
+        for (; n - b > kAtEmax * 32; b += kAtEmax * 32)
+          row_block<kAtEmax>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay);
         switch ((n - b + 31) >> 5) {
-          case 1: row_block<1>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
-          case 2: row_block<2>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
-          case 3: row_block<3>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
-          case 4: row_block<4>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
-          case 5: row_block<5>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
-          case 6: row_block<6>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
-          case 7: row_block<7>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
-          case 8: row_block<8>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay); break;
+#define TSNE_RB(e)                                                                           \
+  case e:                                                                                   \
+    if (e <= kAtEmax)                                                                       \
+      row_block<(e <= kAtEmax ? e : 1)>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn,    \
+                                        lane, ax, ay);                                      \
+    break;
+          TSNE_RB(1) TSNE_RB(2) TSNE_RB(3) TSNE_RB(4) TSNE_RB(5) TSNE_RB(6) TSNE_RB(7) TSNE_RB(8)
+#undef TSNE_RB
           default: break;
         }
       } else if (n <= kAtLong) {

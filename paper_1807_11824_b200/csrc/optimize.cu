@@ -60,15 +60,12 @@ static tsne_status one_iteration(const int64_t* row_ptr, const int32_t* col, con
   if (st != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaEventRecord(o.ev_join, o.side));
   if ((st = build_tree(w, Yin, /*apply_shift=*/true, s)) != TSNE_OK) return st;
-#ifdef TSNE_JOIN_AFTER_TRAVERSE
+  // the traversal starts when the tree is built, beside the attractive pass's
+  // tail if that is still running (joining before the traversal was measured
+  // equal at C5 and 1.3x slower at C4, whose attractive pass outlasts tree +
+  // traversal)
   if ((st = launch_traverse(w, theta, s)) != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaStreamWaitEvent(s, o.ev_join, 0));
-#else
-  // the traversal waits for the attractive pass: it then has every SM (the
-  // latency-bound tree build is what runs beside the attractive pass)
-  TSNE_CUDA_TRY(cudaStreamWaitEvent(s, o.ev_join, 0));
-  if ((st = launch_traverse(w, theta, s)) != TSNE_OK) return st;
-#endif
   return launch_update(Yin, o.A, N, w, o, sc, Yout, V, G, s);
 }
 
