@@ -589,6 +589,17 @@ tsne_status run_iterations(const int64_t* row_ptr, const int32_t* col, const flo
     since += chunk;
     if (since == period) {
       since = 0;
+      if (done < n_iter) {
+        // non-finite sentinel (set by k_update), checked at every checkpoint so
+        // a diverging run stops within relabel_every iterations
+        int32_t bad = 0;
+        TSNE_CUDA_TRY(cudaMemcpyAsync(&bad, o.flag, sizeof(bad), cudaMemcpyDeviceToHost, s));
+        TSNE_CUDA_TRY(cudaStreamSynchronize(s));
+        if (bad) {
+          set_error("non-finite embedding during iterations [%d, %d)", t0, t0 + done);
+          return TSNE_ERR_NONFINITE;
+        }
+      }
       // a relabel checkpoint (also at the end of a call whose state is kept)
       if ((done < n_iter || keep_state) && t0 + done >= kMortonFrom && w.perm &&
           morton_improves(o.rp[h], o.col[h], w.perm, N, o, s)) {
