@@ -412,7 +412,10 @@ tsne_status tsne_ivfpq_search(const float* X, int64_t N, int32_t D, const tsne_i
  *           on the other ranks).
  * Steps: X all-gathered; kNN of the own query rows against all N points
  * (row sweep + fp64 re-rank, bit-identical to tsne_knn rows); the kNN lists
- * all-gathered; P built on every rank; per iteration the attractive sums and
+ * all-gathered; P built on every rank; the points relabelled by the diffusion
+ * locality order of P (identical on every rank), after which rank r iterates
+ * on the contiguous label range [r S, (r+1) S) (its rows' neighbours then
+ * fall in the attractive pass's window); per iteration the attractive sums and
  * the traversal of the own points, an all-gather of the Z partials (added in
  * rank order: every rank uses the identical Z), the update of the own rows,
  * an all-gather of the Y shards (CUDA graphs, one per schedule phase).

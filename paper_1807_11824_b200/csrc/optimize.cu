@@ -312,6 +312,57 @@ static tsne_status diffusion_order(const int64_t* row_ptr, const int32_t* col, c
   return build_tree(w, u, /*apply_shift=*/false, s);      // w.perm = the order
 }
 
+// ---------------------------------------------------------------- for the multi-GPU run
+// The diffusion locality order of P (as above) into perm[N], on scratch u (2N).
+tsne_status diffusion_perm(const int64_t* row_ptr, const int32_t* col, const float* val,
+                           int64_t N, TreeWS& w, float2* u, int32_t* perm, cudaStream_t s) {
+  float2* u2 = u + N;
+  tsne_status st = launch_init_y(N, 0x6c6f63616c697479ull, u, s);
+  if (st != TSNE_OK) return st;
+  const int blocks = (int)((N * 32 + 255) / 256);
+  for (int k = 0; k < kDiffuseSteps; ++k) {
+    k_diffuse<<<blocks, 256, 0, s>>>(row_ptr, col, val, u, (int)N, u2);
+    TSNE_LAUNCH_CHECK();
+    float2* t = u; u = u2; u2 = t;
+  }
+  if ((st = launch_bbox(w, u, s)) != TSNE_OK) return st;
+  if ((st = build_tree(w, u, /*apply_shift=*/false, s)) != TSNE_OK) return st;
+  TSNE_CUDA_TRY(cudaMemcpyAsync(perm, w.perm, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s));
+  return TSNE_OK;
+}
+
+__global__ void k_perm_lens(const int32_t* __restrict__ perm, int N, const int64_t* __restrict__ rp,
+                            int32_t* __restrict__ inv, int64_t* __restrict__ len) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > N) return;
+  if (k == N) { len[N] = 0; return; }
+  const int o = perm[k];
+  inv[o] = k;
+  len[k] = rp[o + 1] - rp[o];
+}
+
+// P relabelled by perm (new label k <- old label perm[k]) into (rp2, col2, val2);
+// inv [N], len [N+1] and the scan scratch are caller scratch
+tsne_status permute_csr(const int32_t* perm, int64_t N, const int64_t* rp, const int32_t* col,
+                        const float* val, int32_t* inv, int64_t* len, void* scan_tmp,
+                        size_t scan_bytes, int64_t* rp2, int32_t* col2, float* val2,
+                        cudaStream_t s) {
+  k_perm_lens<<<(int)((N + 256) / 256), 256, 0, s>>>(perm, (int)N, rp, inv, len);
+  TSNE_LAUNCH_CHECK();
+  size_t sb = scan_bytes;
+  TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scan_tmp, sb, len, rp2, N + 1, s));
+  k_relabel_rows<<<(int)((N * 32 + 255) / 256), 256, 0, s>>>(perm, (int)N, rp, col, val, inv, rp2,
+                                                             col2, val2);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
+size_t permute_csr_scan_bytes(int64_t N) {
+  size_t sb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, sb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(N + 1));
+  return sb;
+}
+
 // Enter the internal label space: the diffusion order early in the run, the
 // Morton order of the caller's Y later (or the caller's order if !morton).
 static tsne_status enter(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t N,

@@ -63,4 +63,14 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
 
 tsne_status launch_init_y(int64_t N, uint64_t seed, float2* Y, cudaStream_t s);
 
+// multi-GPU run: the diffusion locality order of P (perm[N], scratch u[2N]) and
+// P relabelled by a permutation (new label k <- old perm[k])
+tsne_status diffusion_perm(const int64_t* row_ptr, const int32_t* col, const float* val,
+                           int64_t N, TreeWS& w, float2* u, int32_t* perm, cudaStream_t s);
+tsne_status permute_csr(const int32_t* perm, int64_t N, const int64_t* rp, const int32_t* col,
+                        const float* val, int32_t* inv, int64_t* len, void* scan_tmp,
+                        size_t scan_bytes, int64_t* rp2, int32_t* col2, float* val2,
+                        cudaStream_t s);
+size_t permute_csr_scan_bytes(int64_t N);
+
 }  // namespace tsne

@@ -2,11 +2,13 @@
 // (the paper is single-GPU), with the communicator owned
 // by the library: tsne_nccl_unique_id / tsne_run_sharded / tsne_run_workspace_size.
 //
-// Per rank r (rows [r S, min(N, (r+1) S)), S = ceil(N / G)):
+// Per rank r (rows [r S, min(N, (r+1) S)) of the locality labels, S = ceil(N / G)):
 //   1. X: own rows -> device (H2D if host), NCCL all-gather -> X on every rank
 //   2. kNN of the own query rows against all N points (run_knn, row sweep)
 //   3. NCCL all-gather of the kNN lists; P built redundantly (needs every row
-//      for the symmetrisation, ~40 ms at C5); the own CSR rows kept
+//      for the symmetrisation, ~40 ms at C5); the locality labels (the
+//      diffusion order of P, identical on every rank) and P relabelled by them;
+//      the own rows (a contiguous label range) kept
 //   4. per iteration: attractive sums of the own rows (side stream) ||
 //      quadtree over the full Y (redundant) + traversal of the own points;
 //      all-gather of the Z partials (rank order: every rank adds them in the
@@ -77,6 +79,18 @@ const NcclApi* nccl() {
     }                                                                                    \
   } while (0)
 
+__global__ void k_gather_y(const int32_t* __restrict__ perm, const float2* __restrict__ src,
+                           int N, float2* __restrict__ dst) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < N) dst[k] = src[perm[k]];
+}
+
+__global__ void k_scatter_y(const int32_t* __restrict__ perm, const float2* __restrict__ src,
+                            int N, float2* __restrict__ dst) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < N) dst[perm[k]] = src[k];
+}
+
 // rows [r0, r1) of the global CSR as a local CSR (offsets rebased)
 __global__ void k_rebase(const int64_t* __restrict__ rp, int64_t r0, int64_t n,
                          int64_t* __restrict__ out) {
@@ -107,6 +121,17 @@ struct RankPlan {
   double* zpart;           // 2
   double* zparts;          // 2 G
   int32_t* flag;           // 1 (+ non-finite X flag)
+  // locality labels (the diffusion order of P): rank r owns a
+  // contiguous range of labels, so its rows' neighbours fall in its window
+  int32_t* perm;           // N  label -> point
+  int32_t* inv;            // N
+  int64_t* len;            // N + 1
+  float2* u;               // 2N scratch (diffusion coordinates, Y by point)
+  int64_t* rp2;            // N + 1   P in labels
+  int32_t* col2;           // cap
+  float* val2;             // cap
+  void* scan_tmp;
+  size_t scan_bytes;
   void* ws;                // max(kNN, P) scratch, then the shard workspace
   size_t ws_bytes;
 };
@@ -138,6 +163,15 @@ size_t plan(RankPlan& p, void* base, int64_t N, int32_t D, int32_t K, int G) {
   p.zpart = c.take<double>(2);
   p.zparts = c.take<double>(2 * G);
   p.flag = c.take<int32_t>(2);
+  p.perm = c.take<int32_t>(N);
+  p.inv = c.take<int32_t>(N);
+  p.len = c.take<int64_t>(N + 1);
+  p.u = c.take<float2>(2 * N);
+  p.rp2 = c.take<int64_t>(N + 1);
+  p.col2 = c.take<int32_t>(p.cap + 4);
+  p.val2 = c.take<float>(p.cap + 4);
+  p.scan_bytes = permute_csr_scan_bytes(N);
+  p.scan_tmp = c.take<char>(p.scan_bytes);
   size_t kb, pb, sb;
   { KnnWS w; Carver q(nullptr); carve_knn(q, w, N, D, K); kb = q.bytes(); }
   { PWS w; Carver q(nullptr); carve_p(q, w, N, K); pb = q.bytes(); }
@@ -341,34 +375,43 @@ tsne_status tsne_run_sharded(const float* X_local, int64_t N_local, int64_t N, i
                             &ndeg, s)) != TSNE_OK)
       return st;
   }
-  int64_t e0 = 0, e1 = 0;
-  TSNE_CUDA_TRY(cudaMemcpyAsync(&e0, p.rp + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  TSNE_CUDA_TRY(cudaMemcpyAsync(&e1, p.rp + r0 + n_loc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  TSNE_CUDA_TRY(cudaStreamSynchronize(s));
-  k_rebase<<<(int)((n_loc + 256) / 256), 256, 0, s>>>(p.rp, r0, n_loc, p.rp_l);
-  TSNE_LAUNCH_CHECK();
-  if (e1 > e0) {                    // 16-byte aligned copies of the own rows (bulk-copy streams)
-    TSNE_CUDA_TRY(cudaMemcpyAsync(p.col_l, p.col + e0, sizeof(int32_t) * (e1 - e0),
-                                  cudaMemcpyDeviceToDevice, s));
-    TSNE_CUDA_TRY(cudaMemcpyAsync(p.val_l, p.val + e0, sizeof(float) * (e1 - e0),
-                                  cudaMemcpyDeviceToDevice, s));
-  }
-  TSNE_CUDA_TRY(cudaEventRecord(r.ev[3], s));
-  // 4. iterations
-  TSNE_CUDA_TRY(cudaMemsetAsync(p.Yfull, 0, sizeof(float2) * world * S, s));
-  if (cfg.Y_init) {
-    TSNE_CUDA_TRY(cudaMemcpyAsync(p.Yfull, cfg.Y_init, sizeof(float2) * N, cudaMemcpyDefault, s));
-  } else if ((st = launch_init_y(N, cfg.seed, p.Yfull, s)) != TSNE_OK) {
-    return st;
-  }
-  TSNE_CUDA_TRY(cudaMemsetAsync(p.V, 0, sizeof(float2) * S, s));
-  if ((st = fill_ones(reinterpret_cast<float*>(p.Gn), 2 * S, s)) != TSNE_OK) return st;
-  TSNE_CUDA_TRY(cudaMemsetAsync(p.flag, 0, sizeof(int32_t), s));
   ShardWS w;
   {
     Carver c(p.ws);
     carve_shard(c, w, N);
   }
+  if ((st = tree_ws_init(w.tree, s)) != TSNE_OK) return st;
+  // locality labels: the diffusion order of P, computed identically on every
+  // rank (P and the code are identical); the ranks then own label ranges
+  if ((st = diffusion_perm(p.rp, p.col, p.val, N, w.tree, p.u, p.perm, s)) != TSNE_OK) return st;
+  if ((st = permute_csr(p.perm, N, p.rp, p.col, p.val, p.inv, p.len, p.scan_tmp, p.scan_bytes,
+                        p.rp2, p.col2, p.val2, s)) != TSNE_OK)
+    return st;
+  int64_t e0 = 0, e1 = 0;
+  TSNE_CUDA_TRY(cudaMemcpyAsync(&e0, p.rp2 + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  TSNE_CUDA_TRY(cudaMemcpyAsync(&e1, p.rp2 + r0 + n_loc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  TSNE_CUDA_TRY(cudaStreamSynchronize(s));
+  k_rebase<<<(int)((n_loc + 256) / 256), 256, 0, s>>>(p.rp2, r0, n_loc, p.rp_l);
+  TSNE_LAUNCH_CHECK();
+  if (e1 > e0) {                    // 16-byte aligned copies of the own rows (bulk-copy streams)
+    TSNE_CUDA_TRY(cudaMemcpyAsync(p.col_l, p.col2 + e0, sizeof(int32_t) * (e1 - e0),
+                                  cudaMemcpyDeviceToDevice, s));
+    TSNE_CUDA_TRY(cudaMemcpyAsync(p.val_l, p.val2 + e0, sizeof(float) * (e1 - e0),
+                                  cudaMemcpyDeviceToDevice, s));
+  }
+  TSNE_CUDA_TRY(cudaEventRecord(r.ev[3], s));
+  // 4. iterations
+  TSNE_CUDA_TRY(cudaMemsetAsync(p.Yfull, 0, sizeof(float2) * world * S, s));
+  if (cfg.Y_init) {                 // Y0 by point, then in labels
+    TSNE_CUDA_TRY(cudaMemcpyAsync(p.u, cfg.Y_init, sizeof(float2) * N, cudaMemcpyDefault, s));
+  } else if ((st = launch_init_y(N, cfg.seed, p.u, s)) != TSNE_OK) {
+    return st;
+  }
+  k_gather_y<<<(int)((N + 255) / 256), 256, 0, s>>>(p.perm, p.u, (int)N, p.Yfull);
+  TSNE_LAUNCH_CHECK();
+  TSNE_CUDA_TRY(cudaMemsetAsync(p.V, 0, sizeof(float2) * S, s));
+  if ((st = fill_ones(reinterpret_cast<float*>(p.Gn), 2 * S, s)) != TSNE_OK) return st;
+  TSNE_CUDA_TRY(cudaMemsetAsync(p.flag, 0, sizeof(int32_t), s));
   if ((st = tree_ws_init(w.tree, s)) != TSNE_OK) return st;
   Sched sc{cfg.exag_iters, exaggeration, cfg.mom0, cfg.mom1, learning_rate, cfg.min_gain};
   const bool graphs = cfg.use_graphs != 0;
@@ -393,9 +436,12 @@ tsne_status tsne_run_sharded(const float* X_local, int64_t N_local, int64_t N, i
   TSNE_CUDA_TRY(cudaMemcpyAsync(&flag, p.flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   TSNE_CUDA_TRY(cudaEventRecord(r.ev[4], s));
   // 5. result
-  if (rank == 0)
-    TSNE_CUDA_TRY(cudaMemcpyAsync(Y_out, p.Yfull, sizeof(float2) * N,
+  if (rank == 0) {                  // back to the caller's point order
+    k_scatter_y<<<(int)((N + 255) / 256), 256, 0, s>>>(p.perm, p.Yfull, (int)N, p.u);
+    TSNE_LAUNCH_CHECK();
+    TSNE_CUDA_TRY(cudaMemcpyAsync(Y_out, p.u, sizeof(float2) * N,
                                   y_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+  }
   TSNE_CUDA_TRY(cudaEventRecord(r.ev[5], s));
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
