@@ -350,7 +350,7 @@ tsne_status permute_csr(const int32_t* perm, int64_t N, const int64_t* rp, const
   k_perm_lens<<<(int)((N + 256) / 256), 256, 0, s>>>(perm, (int)N, rp, inv, len);
   TSNE_LAUNCH_CHECK();
   size_t sb = scan_bytes;
-  TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scan_tmp, sb, len, rp2, N + 1, s));
+  TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scan_tmp, sb, len, rp2, (int)(N + 1), s));
   k_relabel_rows<<<(int)((N * 32 + 255) / 256), 256, 0, s>>>(perm, (int)N, rp, col, val, inv, rp2,
                                                              col2, val2);
   TSNE_LAUNCH_CHECK();
