@@ -4,37 +4,90 @@
 // and the update of the points it owns, rows [row0, row1).  The exchange --
 // the Z partials and the all-gather of the updated Y shards -- is done by the
 // caller over NCCL (torch.distributed), between the two calls below.
-#include <cub/device/device_scan.cuh>
-
 #include "shard.cuh"
 
 namespace tsne {
 
 void carve_shard(Carver& c, ShardWS& w, int64_t N) {
   carve_tree(c, w.tree, N);
-  w.flags = c.take<int32_t>(N + 1);
-  w.pos = c.take<int32_t>(N + 1);
+  w.flags = c.take<int32_t>(N / 1024 + 2);   // per-block owned counts -> offsets
+  w.pos = c.take<int32_t>(1);                // number of owned points
   w.list = c.take<int32_t>(N);
-  size_t sb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, sb, (int32_t*)nullptr, (int32_t*)nullptr, (int)(N + 1));
-  w.scan_tmp = c.take<char>(sb);
-  w.scan_tmp_bytes = sb;
 }
 
-__global__ void k_owned_flags(const int32_t* __restrict__ perm, int N, int row0, int row1,
-                              int32_t* __restrict__ flags) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k > N) return;
-  if (k == N) { flags[N] = 0; return; }
+// The sorted positions k whose point perm[k] is owned ([row0, row1)), in
+// sorted order: per-block counts (warp ballots), an exclusive scan of the
+// block counts (one CTA), then every owned position written at its rank.
+constexpr int kOwnThreads = 1024;
+
+__device__ __forceinline__ bool owned_at(const int32_t* perm, int k, int N, int row0, int row1) {
+  if (k >= N) return false;
   const int p = perm[k];
-  flags[k] = (p >= row0 && p < row1) ? 1 : 0;
+  return p >= row0 && p < row1;
 }
 
-__global__ void k_owned_list(const int32_t* __restrict__ flags, const int32_t* __restrict__ pos,
-                             int N, int32_t* __restrict__ list) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= N) return;
-  if (flags[k]) list[pos[k]] = k;
+__global__ void __launch_bounds__(kOwnThreads)
+k_owned_count(const int32_t* __restrict__ perm, int N, int row0, int row1,
+              int32_t* __restrict__ bcount) {
+  __shared__ int s_w[kOwnThreads / 32];
+  const int k = blockIdx.x * kOwnThreads + threadIdx.x;
+  const unsigned b = __ballot_sync(0xffffffffu, owned_at(perm, k, N, row0, row1));
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < kOwnThreads / 32; ++w) t += s_w[w];
+    bcount[blockIdx.x] = t;
+  }
+}
+
+// exclusive scan of nb block counts in place (one CTA), total into *ntot
+__global__ void __launch_bounds__(1024) k_owned_scan(int32_t* __restrict__ bcount, int nb,
+                                                     int32_t* __restrict__ ntot) {
+  __shared__ int s_w[32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int per = (nb + 1023) / 1024;
+  const int b0 = t * per, b1 = min(nb, b0 + per);
+  int tot = 0;
+  for (int b = b0; b < b1; ++b) tot += bcount[b];
+  int inc = tot;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += x;
+  }
+  if (lane == 31) s_w[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int v = s_w[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += x;
+    }
+    s_w[lane] = v;
+  }
+  __syncthreads();
+  int off = (wid ? s_w[wid - 1] : 0) + inc - tot;
+  for (int b = b0; b < b1; ++b) {
+    const int c = bcount[b];
+    bcount[b] = off;
+    off += c;
+  }
+  if (t == 1023) *ntot = s_w[31];
+}
+
+__global__ void __launch_bounds__(kOwnThreads)
+k_owned_write(const int32_t* __restrict__ perm, int N, int row0, int row1,
+              const int32_t* __restrict__ boff, int32_t* __restrict__ list) {
+  __shared__ int s_w[kOwnThreads / 32];
+  const int k = blockIdx.x * kOwnThreads + threadIdx.x;
+  const bool own = owned_at(perm, k, N, row0, row1);
+  const unsigned b = __ballot_sync(0xffffffffu, own);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_w[wid] = __popc(b);
+  __syncthreads();
+  int before = boff[blockIdx.x];
+  for (int w = 0; w < wid; ++w) before += s_w[w];
+  if (own) list[before + __popc(b & ((1u << lane) - 1u))] = k;
 }
 
 __global__ void k_recentre(float2* Y, int N, const BoxInfo* box) {
@@ -59,13 +112,14 @@ tsne_status shard_forces(ShardWS& w, const float2* Y, int64_t N, int64_t row0, i
   if (st != TSNE_OK) return st;
   if ((st = build_tree(t, Y, /*apply_shift=*/true, s)) != TSNE_OK) return st;
   const int n = (int)N;
-  k_owned_flags<<<(n + 256) / 256, 256, 0, s>>>(t.perm, n, (int)row0, (int)row1, w.flags);
+  const int nb = (n + kOwnThreads - 1) / kOwnThreads;
+  k_owned_count<<<nb, kOwnThreads, 0, s>>>(t.perm, n, (int)row0, (int)row1, w.flags);
   TSNE_LAUNCH_CHECK();
-  size_t sb = w.scan_tmp_bytes;
-  TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.scan_tmp, sb, w.flags, w.pos, n + 1, s));
-  k_owned_list<<<(n + 255) / 256, 256, 0, s>>>(w.flags, w.pos, n, w.list);
+  k_owned_scan<<<1, 1024, 0, s>>>(w.flags, nb, w.pos);
   TSNE_LAUNCH_CHECK();
-  return launch_traverse_list(t, theta, w.list, w.pos + n, (int)row0, rep_local, z_partial, s);
+  k_owned_write<<<nb, kOwnThreads, 0, s>>>(t.perm, n, (int)row0, (int)row1, w.flags, w.list);
+  TSNE_LAUNCH_CHECK();
+  return launch_traverse_list(t, theta, w.list, w.pos, (int)row0, rep_local, z_partial, s);
 }
 
 tsne_status shard_recentre(ShardWS& w, float2* Y, int64_t N, cudaStream_t s) {

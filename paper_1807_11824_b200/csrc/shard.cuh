@@ -7,8 +7,6 @@ namespace tsne {
 struct ShardWS {
   TreeWS tree;
   int32_t *flags = nullptr, *pos = nullptr, *list = nullptr;
-  void* scan_tmp = nullptr;
-  size_t scan_tmp_bytes = 0;
 };
 
 void carve_shard(Carver& c, ShardWS& w, int64_t N);
