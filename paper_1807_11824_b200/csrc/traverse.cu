@@ -63,10 +63,14 @@ k_bucket_pairs(const float4* __restrict__ nodes, const int32_t* __restrict__ nfi
                const float2* __restrict__ ys, const int32_t* __restrict__ leafnode, int N,
                const int32_t* __restrict__ list, const int32_t* __restrict__ nlist,
                const int32_t* __restrict__ has_bucket, BucketSum* __restrict__ out) {
-  const int tid = blockIdx.x * kBucketThreads + threadIdx.x;
-  const bool active = tid < (list ? *nlist : N);
-  const int k = active ? (list ? list[tid] : tid) : -1;
   if (!*has_bucket) return;                         // no bucket in this tree (k_traverse knows)
+  const int nact = list ? *nlist : N;
+  // grid-stride over chunks of kBucketThreads points (a small grid, so a tree
+  // without buckets costs one short launch)
+  for (int base = blockIdx.x * kBucketThreads; base < nact; base += gridDim.x * kBucketThreads) {
+  const int tid = base + threadIdx.x;
+  const bool active = tid < nact;
+  const int k = active ? (list ? list[tid] : tid) : -1;
   int s0 = -1, cnt = 0;
   float2 yi = make_float2(0.f, 0.f);
   if (active) {
@@ -118,6 +122,7 @@ k_bucket_pairs(const float4* __restrict__ nodes, const int32_t* __restrict__ nfi
     b.f = make_float2(fx, fy);
     b.z = z;
     out[k] = b;
+  }
   }
 }
 
@@ -370,7 +375,8 @@ static tsne_status launch_bucket_pairs(TreeWS& w, const int32_t* list, const int
                                        cudaStream_t s) {
   const int N = (int)w.N;
   // the fixed-point coordinates are dead after the tree build: reuse them
-  k_bucket_pairs<<<(N + kBucketThreads - 1) / kBucketThreads, kBucketThreads, 0, s>>>(
+  const int nb = (N + kBucketThreads - 1) / kBucketThreads;
+  k_bucket_pairs<<<nb < 16 * kNumSMs ? nb : 16 * kNumSMs, kBucketThreads, 0, s>>>(
       w.nodes, w.nfirst, w.ys, w.leafnode, N, list, nlist, w.has_bucket,
       reinterpret_cast<BucketSum*>(w.fq));
   TSNE_LAUNCH_CHECK();

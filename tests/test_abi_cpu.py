@@ -96,3 +96,31 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 for bad in ("import oracle", "from oracle", "tsne_oracle", "oracle_"):
                     assert bad not in txt, (f, bad)
+
+
+def test_new_entry_points_validate_without_device(L):
+    """tsne_run_sharded, tsne_ivfpq_* and tsne_optimize_release check their
+    arguments before any CUDA call (S:L111 style errors)."""
+    import paper_1807_11824_b200 as T
+    v = C.c_void_p(256)
+    uid = (C.c_uint8 * 128)()
+    info = T.RunInfo()
+    # N_local must be this rank's shard size: N = 100, world 3 -> S = 34, rank 2 owns 32 rows
+    rc = L.tsne_run_sharded(v, 34, 100, 8, 10.0, 0.5, 200.0, 10, 12.0, None, uid, 2, 3, None,
+                            C.byref(info))
+    assert rc == 1 and b"N_local must be 32" in L.tsne_last_error()
+    rc = L.tsne_run_sharded(v, 32, 100, 8, 10.0, 0.5, 200.0, 10, 12.0, None, uid, 3, 3, None,
+                            C.byref(info))
+    assert rc == 1 and b"rank" in L.tsne_last_error()
+    # IVF-PQ: index layout defaults (|C| = sqrt(N), m = min(96, ceil(D / 8))) and bad tau
+    p = T.ivfpq_params()
+    lay = (C.c_int64 * 11)()
+    assert L.tsne_ivfpq_layout(10000, 784, C.byref(p), lay) == 0
+    assert (lay[0], lay[1], lay[2], lay[3]) == (100, 96, 9, 864)
+    assert L.tsne_ivfpq_index_size(10000, 784, C.byref(p)) >= 10000 * 96 + 100 * 864 * 4
+    rc = L.tsne_ivfpq_search(v, 10000, 784, C.byref(p), v, 32, 101, v, v, v, 1 << 40, None)
+    assert rc == 1 and b"tau" in L.tsne_last_error()
+    rc = L.tsne_ivfpq_build(v, 10000, 784, C.byref(T.ivfpq_params(m=4)), v, 1 << 40, v, 1 << 40,
+                            None)
+    assert rc == 1 and b"dsub" in L.tsne_last_error()
+    L.tsne_optimize_release(v)          # unknown workspace: ignored
