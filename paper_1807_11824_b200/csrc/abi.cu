@@ -351,7 +351,8 @@ tsne_status tsne_shard_attract(const int64_t* row_ptr_local, const int32_t* col_
   if (st != TSNE_OK) return st;
   return launch_attract_sum_shard(row_ptr_local, col_local, val_local,
                                   reinterpret_cast<const float2*>(Y), N, row0, row1 - row0,
-                                  reinterpret_cast<float2*>(A_local), (cudaStream_t)stream);
+                                  reinterpret_cast<float2*>(A_local), nullptr,
+                                  (cudaStream_t)stream);
 }
 
 tsne_status tsne_shard_update(const float* A_local, int64_t N, int64_t row0, int64_t row1,

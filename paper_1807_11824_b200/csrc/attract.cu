@@ -21,58 +21,103 @@ constexpr int kAttrThreads = 256;
 constexpr int kAttrWarps = kAttrThreads / 32;
 
 // ---------------------------------------------------------------- H7
-// Attractive pass as a persistent TMA pipeline (one CTA per SM).  The CTA
-// owns a contiguous range of rows, cut into batches of at most kAtBatch rows
-// whose nonzeros fit a stage buffer.  A producer warp streams each batch's
-// col/val span (contiguous in the CSR) into a kAtStages-deep shared-memory
-// ring with cp.async.bulk + mbarriers (the bulk copies keep ~3 batches of the
-// 8-byte-per-nonzero stream in flight per SM without holding registers); the
-// embedding window Y[wlo, wlo + kAtWin) around the CTA's rows is staged once
-// the same way.  Two groups of kAtRows consumer warps take alternate batches
-// (latency hiding for the L2 gathers); warp w of a group computes rows w and
-// w + kAtRows of its batches: lanes take consecutive nonzeros from shared memory, gather y_j
-// from the window (columns outside it, rare once the labels are in a locality
-// order -- DESIGN.md 6.4-6.5 -- come from L2), and reduce with a fixed
-// butterfly (deterministic; the result does not depend on which path an
-// operand came from).  A batch whose span does not fit a stage buffer is read
-// from global memory directly; rows of more than kAtLong nonzeros go to
-// k_attract_long.  The sizes below are the measured best of the variants in
-// DESIGN.md 6.4 (overridable at compile time for such experiments).
-#ifndef TSNE_AT_ROWS
-#define TSNE_AT_ROWS 15
+// Attractive pass as a persistent TMA pipeline (one CTA per SM).
+// * CTA b owns the rows [f(b), f(b+1)), f(b) the first row starting at or
+//   after nonzero nnz*b/G, so every CTA streams the same number of nonzeros
+//   whatever the row-length distribution.
+// * The rows are cut into ITEMS: consecutive pieces of kAtItem nonzeros counted
+//   from the row's start (a row of n nonzeros is ceil(n / kAtItem) items, an
+//   empty row one empty item).  Up to kAtItems whole items whose nonzeros fit
+//   a stage buffer form a BATCH -- a batch may end inside a row, never inside
+//   an item.  The batches depend only on row_ptr and the grid: the optimiser
+//   and the shards cut them once per CSR (k_attract_plan, at every relabel);
+//   the one-shot entry points cut them inside the kernel (same cut).
+// * A producer warp streams each batch's col/val span (contiguous in the CSR)
+//   and its item list into a kAtStages-deep shared-memory ring with
+//   cp.async.bulk + mbarriers; the embedding window Y[wlo, wlo + kAtWin)
+//   around the CTA's rows is staged once the same way.
+// * Consumer warps (kAtGroups groups taking alternate batches) take the items
+//   of a batch one at a time from a shared counter -- dynamic, so a long row
+//   (a hub of the kNN graph: thousands of nonzeros) is spread over many warps
+//   and a warp that finished early takes more of the next batch.  Lanes take
+//   consecutive nonzeros of the item from shared memory, gather y_j from the
+//   window (columns outside it, rare once the labels are in a locality order
+//   -- come from L2 through a predicated load), and the
+//   warp reduces the item with a fixed butterfly into a per-item partial.
+// * A finaliser warp adds each row's partials in item order (a row continued
+//   from the previous batch starts from the carried sum) and writes the rows
+//   that ended.  The item cut depends only on the row, so every row is summed
+//   in the same order whatever the grid, the batch cuts or the CSR around it
+//   (deterministic; a shard's local CSR gives the single-GPU rows bit for bit).
+#ifndef TSNE_AT_GROUPS
 #define TSNE_AT_GROUPS 2
+#endif
+#ifndef TSNE_AT_WARPS
+#define TSNE_AT_WARPS 30
+#endif
+#ifndef TSNE_AT_STAGES
 #define TSNE_AT_STAGES 4
+#endif
+#ifndef TSNE_AT_CAP
 #define TSNE_AT_CAP 4096
-#define TSNE_AT_WIN 12288
 #endif
-constexpr int kAtRows = TSNE_AT_ROWS;          // consumer warps per group
+#ifndef TSNE_AT_ITEM
+#define TSNE_AT_ITEM 256
+#endif
 constexpr int kAtGroups = TSNE_AT_GROUPS;      // consumer groups take alternate batches
-constexpr int kAtConsumers = kAtRows * kAtGroups;
-constexpr int kAtThreads = (kAtConsumers + 1) * 32;
+constexpr int kAtConsumers = TSNE_AT_WARPS;    // consumer warps
+constexpr int kAtRows = kAtConsumers / kAtGroups;   // consumer warps per group
+constexpr int kAtThreads = (kAtConsumers + 2) * 32;   // + the producer and the finaliser warp
 constexpr int kAtStages = TSNE_AT_STAGES;
+constexpr int kAtMetas = 2 * kAtStages;        // batch metadata slots (outlive their stage)
 constexpr int kAtCap = TSNE_AT_CAP;            // nonzeros per stage buffer
-constexpr int kAtWin = TSNE_AT_WIN;            // window points
-#ifndef TSNE_AT_BATCH
-#define TSNE_AT_BATCH (2 * TSNE_AT_ROWS)
-#endif
-constexpr int kAtBatch = TSNE_AT_BATCH;        // rows per batch: up to 2 per consumer warp
-#ifndef TSNE_AT_EMAX
-#define TSNE_AT_EMAX 8
-#endif
-constexpr int kAtEmax = TSNE_AT_EMAX;          // 32-entry groups of a row loaded together
-constexpr int kAtLong = 2048;                  // longer rows: k_attract_long
-constexpr int kAtChunk = 56;                   // rows per row_ptr prefetch chunk (~2 batches)
+constexpr int kAtBudget = kAtCap - 8;          // a batch's nonzeros (the 16-byte aligned span fits)
+constexpr int kAtItem = TSNE_AT_ITEM;          // nonzeros per item
+constexpr int kAtEmax = kAtItem / 32;          // 32-entry groups of an item, loaded together
+constexpr int kAtItems = 32;                   // items per batch (one per producer lane)
+constexpr int kAtChunk = 56;                   // rows per row_ptr prefetch chunk
 constexpr int kAtLook = 3;                     // row_ptr prefetch distance (chunks)
 constexpr int kAtRpSlots = kAtLook + 1;
+constexpr int kAtHdrRing = 64;                 // prefetched batch headers (plan mode)
+static_assert(kAtConsumers % kAtGroups == 0, "equal consumer groups");
 static_assert(kAtStages % kAtGroups == 0, "a stage always serves the same consumer group");
-constexpr size_t kAtSmem = sizeof(float2) * kAtWin + (size_t)kAtStages * kAtCap * 8;
+static_assert(kAtItem % 32 == 0 && kAtEmax >= 1 && kAtEmax <= 8, "an item is 1-8 warp-wide groups");
+static_assert(kAtBudget / kAtItem >= 1, "a stage holds at least one item");
+static_assert(kAtCap < (1 << 13) && kAtItem < (1 << 9), "item descriptor fields");
+static_assert(kAtChunk >= kAtItems + 2, "a batch's rows lie in two row_ptr chunks");
 
-static_assert(kAtBatch < 32, "a batch is cut by one warp ballot");
-struct AtMeta {
-  int64_t rp[kAtBatch + 1];  // row_ptr of the batch's rows (local CSR)
-  int64_t a_lo, a_hi;        // staged nonzeros [a_lo, a_hi) (a_hi <= a_lo when not staged)
-  int32_t r0, nrows;         // first local row, rows in the batch
+struct AtBatchHdr {
+  int64_t a_lo;              // first staged nonzero (a multiple of 4)
+  int32_t cnt;               // nonzeros bulk-copied from a_lo (a multiple of 4)
+  int16_t n_items;           // -1: end marker
+  int16_t n_tail;            // the CSR's last (< 4) nonzeros, copied after them by plain loads
 };
+struct AtBatch {             // one batch of the plan; copied whole into a metadata slot
+  AtBatchHdr h;
+  int2 item[kAtItems];       // {local row, beg | len << 13 | last << 22} (beg: offset from a_lo)
+};
+static_assert(sizeof(AtBatchHdr) == 16 && sizeof(AtBatch) % 16 == 0, "bulk-copy granules");
+struct AtMeta {
+  AtBatch b;
+  float2 part[kAtItems];     // per-item partial sums (consumers -> finaliser)
+  int32_t next;              // next item to take (shared counter)
+  int32_t pad[3];
+};
+struct AtShared {            // the kernel's static shared memory
+  AtMeta meta[kAtMetas];
+  union {
+    int64_t rpring[kAtRpSlots][kAtChunk + 1];  // row_ptr ring (batches cut in the kernel)
+    AtBatchHdr hring[kAtHdrRing];              // header ring (plan mode)
+  };
+  uint64_t full[kAtStages], empty[kAtStages], done[kAtMetas], mfree[kAtMetas], win;
+  int32_t lr0, lr1, wlo, wn;
+};
+// the window takes what the 227 KB per-CTA limit leaves
+constexpr int kAtSmemLimit = 232448;
+constexpr int kAtWin =
+    (int)(((kAtSmemLimit - (int)sizeof(AtShared) - 64 - kAtStages * kAtCap * 8) / 8) & ~63);
+static_assert(kAtWin >= 4096, "window");
+constexpr size_t kAtSmem = sizeof(float2) * kAtWin + (size_t)kAtStages * kAtCap * 8;
 
 __device__ __forceinline__ float rcp_approx_f(float x) {
   float r;
@@ -119,10 +164,10 @@ __device__ __forceinline__ void win_accum(float2 yi, float2 yj, float p, float& 
   ay = fmaf(pw, dy, ay);
 }
 
-// E x 32 consecutive entries of a staged row (n_rem entries remain from cr):
-// lane takes entries lane + 32u; only the last group can be partial (its
-// absent entries are the point itself with p = 0).  All loads first, then
-// the arithmetic: the window / L2 gathers of the block are in flight together.
+// E x 32 consecutive entries of a staged item (n_rem entries from cr): lane
+// takes entries lane + 32u; only the last group can be partial (its absent
+// entries are the point itself with p = 0).  All loads first, then the
+// arithmetic: the window / L2 gathers of the item are in flight together.
 template <int E>
 __device__ __forceinline__ void row_block(const int32_t* __restrict__ cr,
                                           const float* __restrict__ vr, int n_rem, int self,
@@ -152,8 +197,7 @@ __device__ __forceinline__ void row_block(const int32_t* __restrict__ cr,
   for (int u = 0; u < E; ++u) win_accum(yi, y[u], p[u], ax, ay);
 }
 
-// spin wait (no suspend-time hint: the pipeline's waits are short and a
-// sleeping producer would throttle the stream)
+// spin wait (the consumers' waits are short)
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
@@ -185,305 +229,513 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
+// First rows r in [0, n] with rp[r] >= T0 and with rp[r] >= T1 (rp[n] >= T0,
+// T1), searched by the warp together: each round 32 lanes sample the
+// remaining interval of each search, so a search over N rows takes
+// ~log32(N) dependent loads.
+__device__ __forceinline__ void lower_bound2_warp(const int64_t* __restrict__ rp, int n, int64_t T0,
+                                                  int64_t T1, int lane, int& r0, int& r1) {
+  int lo[2] = {0, 0}, hi[2] = {n, n};          // each answer lies in [lo, hi]
+  const int64_t T[2] = {T0, T1};
+  while (lo[0] < hi[0] || lo[1] < hi[1]) {
+    int st[2];
+    bool g[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      st[h] = (hi[h] - lo[h] + 31) >> 5;
+      const int p = lo[h] + lane * st[h];
+      g[h] = lo[h] < hi[h] ? (p >= hi[h] || rp[p] >= T[h]) : true;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const unsigned b = __ballot_sync(0xffffffffu, g[h]);
+      if (lo[h] < hi[h]) {
+        if (b == 0u) {
+          lo[h] += 31 * st[h] + 1;
+        } else {
+          const int f = __ffs(b) - 1;
+          if (f == 0) {
+            hi[h] = lo[h];
+          } else {
+            hi[h] = min(hi[h], lo[h] + f * st[h]);
+            lo[h] += (f - 1) * st[h] + 1;
+          }
+        }
+      }
+    }
+  }
+  r0 = lo[0];
+  r1 = lo[1];
+}
+
+// The CTA's row range [lr0, lr1) of a grid of G CTAs over n_rows rows.
+__device__ __forceinline__ void at_range(const int64_t* __restrict__ row_ptr, int n_rows, int b,
+                                         int G, int lane, int& lr0, int& lr1) {
+  const int64_t nnz = row_ptr[n_rows];
+  lower_bound2_warp(row_ptr, n_rows, nnz * b / G, nnz * (b + 1) / G, lane, lr0, lr1);
+  if (b == 0) lr0 = 0;
+  if (b + 1 == G) lr1 = n_rows;
+}
+
+// row_ptr of rows [lr0, lr1] through a ring of kAtChunk-row chunks in shared
+// memory, fetched kAtLook chunks ahead with cp.async (one warp)
+struct RpRing {
+  int64_t (*ring)[kAtChunk + 1];
+  const int64_t* row_ptr;
+  int lr0, lr1, nch, fetched;
+  __device__ __forceinline__ void fetch(int c, int lane) {
+    if (c < nch)
+      for (int q = lane; q <= kAtChunk; q += 32) {
+        const int r = min(lr0 + c * kAtChunk + q, lr1);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                         smem_u32(&ring[c % kAtRpSlots][q])),
+                     "l"(row_ptr + r)
+                     : "memory");
+      }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  __device__ __forceinline__ void start(int lane) {
+    nch = (lr1 - lr0 + kAtChunk - 1) / kAtChunk;
+    for (int j = 0; j < kAtLook; ++j) fetch(j, lane);
+    fetched = kAtLook;
+  }
+  // rows r .. r + 32 readable (chunks <= chunk(r) + 1 have landed)
+  __device__ __forceinline__ void ready(int r, int lane) {
+    const int c = (r - lr0) / kAtChunk;
+    while (fetched <= c + kAtLook) fetch(fetched++, lane);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kAtLook - 1) : "memory");
+    __syncwarp();
+  }
+  // (a chunk's slot holds kAtChunk + 1 entries; the end of the range at a
+  // chunk boundary is the last entry of the previous chunk)
+  __device__ __forceinline__ int64_t operator()(int r) const {
+    const int o = r - lr0, c = o / kAtChunk, q = o - c * kAtChunk;
+    if (c == nch) return ring[(c - 1) % kAtRpSlots][kAtChunk];
+    return ring[c % kAtRpSlots][q];
+  }
+};
+
+// Cuts the next batch at (r, e) -- e the next nonzero of row r, an item
+// boundary -- (one warp): whole rows while they fit (items and nonzeros), then
+// whole items of the row that does not.  Writes the item descriptors and
+// returns the header; advances (r, e).
+__device__ __forceinline__ AtBatchHdr pack_batch(const RpRing& rp, int lane, int lr1, int64_t nnz4,
+                                                 int& r, int64_t& e, int2* __restrict__ items) {
+  const int rj = r + lane;                      // lane j looks at row r + j
+  const bool in = rj < lr1;
+  int64_t sj = 0, tj = 0;                       // its nonzeros [sj, tj)
+  int itj = 0;                                  // and items
+  if (in) {
+    sj = lane == 0 ? e : rp(rj);
+    tj = rp(rj + 1);
+    itj = max(1, (int)((tj - sj + kAtItem - 1) / kAtItem));
+  }
+  int I = itj;                                  // inclusive prefix of the item counts
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, I, o);
+    if (lane >= o) I += v;
+  }
+  const bool fits = in && I <= kAtItems && tj - e <= kAtBudget;   // a prefix of the lanes
+  const int f = __popc(__ballot_sync(0xffffffffu, fits));
+  const int i_before = f > 0 ? __shfl_sync(0xffffffffu, I, f - 1) : 0;
+  const int64_t t_before = f > 0 ? __shfl_sync(0xffffffffu, tj, f - 1) : e;
+  int q = 0;                                    // whole items of row r + f
+  int64_t sf = 0;
+  if (f < 32) {
+    sf = __shfl_sync(0xffffffffu, sj, f);
+    if (r + f < lr1)
+      q = (int)min((int64_t)(kAtItems - i_before), (kAtBudget - (sf - e)) / kAtItem);
+  }
+  const int64_t e_hi = q > 0 ? sf + (int64_t)q * kAtItem : t_before;
+  const int64_t a_lo = e & ~int64_t(3);
+  const int64_t a_hi = min((e_hi + 3) & ~int64_t(3), nnz4);
+  if (lane < f)
+    for (int u = 0; u < itj; ++u) {
+      const int64_t b = sj + (int64_t)u * kAtItem;
+      const int len = (int)min((int64_t)kAtItem, tj - b);
+      items[I - itj + u] = make_int2(rj, (int)(b - a_lo) | (len << 13) | ((u == itj - 1) << 22));
+    }
+  if (lane < q)                                 // never the row's last item
+    items[i_before + lane] =
+        make_int2(r + f, (int)(sf + (int64_t)lane * kAtItem - a_lo) | (kAtItem << 13));
+  AtBatchHdr h;
+  h.a_lo = a_lo;
+  h.cnt = a_hi > a_lo ? (int32_t)(a_hi - a_lo) : 0;
+  h.n_items = (int16_t)(i_before + q);
+  h.n_tail = (int16_t)max((int64_t)0, e_hi - max(nnz4, a_lo));
+  r += f;
+  e = e_hi;
+  return h;
+}
+
+// Batches of CTA b are stored from plan_off(lr0(b), row_ptr[lr0(b)], b).  Every
+// batch but a CTA's last holds kAtItems items or more than kAtBudget - kAtItem
+// nonzeros, and a range holds at most nnz/kAtItem + rows items, so the regions
+// [plan_off(b), plan_off(b + 1)) never overflow.
+__host__ __device__ __forceinline__ int64_t plan_off(int64_t lr, int64_t E, int64_t b) {
+  return lr / kAtItems + E / (kAtBudget - kAtItem) + E / ((int64_t)kAtItem * kAtItems) + 5 * b;
+}
+
+// One warp per pipeline CTA: its row range and its batches (the same cut as
+// the in-kernel packing).  cta[b] = {lr0, lr1, first batch, batches}.
+__global__ void __launch_bounds__(32) k_attract_plan(const int64_t* __restrict__ row_ptr,
+                                                      int n_rows, AtBatch* __restrict__ batches,
+                                                      int4* __restrict__ cta) {
+  __shared__ __align__(16) int64_t ring[kAtRpSlots][kAtChunk + 1];
+  const int lane = threadIdx.x, b = blockIdx.x, G = gridDim.x;
+  int lr0, lr1;
+  at_range(row_ptr, n_rows, b, G, lane, lr0, lr1);
+  const int64_t nnz4 = row_ptr[n_rows] & ~int64_t(3);
+  const int64_t e0 = row_ptr[lr0];
+  const int64_t off0 = plan_off(lr0, e0, b), off1 = plan_off(lr1, row_ptr[lr1], b + 1);
+  RpRing rp{ring, row_ptr, lr0, lr1, 0, 0};
+  rp.start(lane);
+  int r = lr0, k = 0;
+  int64_t e = e0;
+  while (r < lr1) {
+    rp.ready(r, lane);
+    if (off0 + k >= off1) __trap();             // cannot happen (plan_off's bound)
+    AtBatch& B = batches[off0 + k];
+    const AtBatchHdr h = pack_batch(rp, lane, lr1, nnz4, r, e, B.item);
+    if (lane == 0) B.h = h;
+    ++k;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (lane == 0) cta[b] = make_int4(lr0, lr1, (int)off0, k);
+}
+
+template <int MODE>
+__device__ __forceinline__ void at_write(float2* __restrict__ out, const float2* __restrict__ rep,
+                                         const double* __restrict__ Z, float alpha, int l,
+                                         float2 a) {
+  if (MODE == 0) {
+    out[l] = a;
+  } else {
+    const float invZ = (float)Z[1];
+    const float2 f = rep[l];
+    out[l] = make_float2(4.f * (alpha * a.x - f.x * invZ), 4.f * (alpha * a.y - f.y * invZ));
+  }
+}
+
 // MODE 0: out[l] = A_l.  MODE 1 (tsne_gradient): out[l] = 4 (alpha A_l - f_l / Z).
 // Rows l in [0, n_rows) of the (local) CSR are global points row0 + l of Y.
-template <int MODE>
+// PLAN: the batches come from k_attract_plan (batches, cta), else the producer
+// cuts them.
+template <int MODE, bool PLAN>
 __global__ void __launch_bounds__(kAtThreads, 1)
 k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
               const float* __restrict__ val, const float2* __restrict__ Y, int Ny, int row0,
-              int n_rows, float2* __restrict__ out, const float2* __restrict__ rep,
+              int n_rows, const AtBatch* __restrict__ batches, const int4* __restrict__ cta,
+              float2* __restrict__ out, const float2* __restrict__ rep,
               const double* __restrict__ Z, float alpha) {
   extern __shared__ __align__(128) unsigned char at_smem[];
-  __shared__ AtMeta s_meta[kAtStages];
-  __shared__ __align__(16) int64_t s_rpring[kAtRpSlots][kAtChunk + 1];
-  __shared__ __align__(8) uint64_t s_full[kAtStages], s_empty[kAtStages], s_win;
+  __shared__ __align__(16) AtShared sh;
   float2* s_y = reinterpret_cast<float2*>(at_smem);
   int32_t* s_col = reinterpret_cast<int32_t*>(at_smem + sizeof(float2) * kAtWin);
   float* s_val = reinterpret_cast<float*>(s_col + kAtStages * kAtCap);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // this CTA's rows [lr0, lr1): whole chunks of kAtChunk rows
-  const int nch_all = (n_rows + kAtChunk - 1) / kAtChunk;
-  const int c0 = (int)((int64_t)nch_all * blockIdx.x / gridDim.x);
-  const int c1 = (int)((int64_t)nch_all * (blockIdx.x + 1) / gridDim.x);
-  const int lr0 = c0 * kAtChunk, lr1 = min(c1 * kAtChunk, n_rows);
-  int wlo = row0 + (lr0 + lr1) / 2 - kAtWin / 2;
-  wlo = min(wlo, Ny - kAtWin);
-  wlo = max(wlo, 0) & ~1;                      // 16-byte aligned source
-  const int wn = min(kAtWin, Ny - wlo) & ~1;   // 16-byte multiple
-  const bool own_in_win = row0 + lr0 >= wlo && row0 + lr1 <= wlo + wn;
   const uint32_t sbase = smem_u32(s_y);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kAtStages; ++s) {
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_empty[s], kAtRows);
+      mbar_init(&sh.full[s], 1);
+      mbar_init(&sh.empty[s], kAtRows);
     }
-    mbar_init(&s_win, 1);
+    for (int s = 0; s < kAtMetas; ++s) {
+      mbar_init(&sh.done[s], kAtRows);
+      mbar_init(&sh.mfree[s], 1);
+    }
+    mbar_init(&sh.win, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
+  if (wid == kAtConsumers + 1) {
+    // ----------------------------------------------------------- finaliser
+    // Batch kk is done: add each row's partials in item order (a row continued
+    // from the previous batch starts from the carried sum), write the rows
+    // that ended, free the batch's metadata slot.
+    float2 carry = make_float2(0.f, 0.f);
+    for (int kk = 0;; ++kk) {
+      const int ms = kk % kAtMetas;
+      mbar_wait_sleep(&sh.done[ms], (kk / kAtMetas) & 1);
+      const AtMeta& m = sh.meta[ms];
+      const int ni = m.b.h.n_items;
+      if (ni < 0) break;                        // the first end marker: every batch is done
+      int row = -1;
+      bool head = false;
+      if (lane < ni) {
+        row = m.b.item[lane].x;
+        head = lane == 0 || m.b.item[lane - 1].x != row;
+      }
+      float2 acc = make_float2(0.f, 0.f);
+      bool open = false;                        // the row continues in the next batch
+      if (head) {
+        if (lane == 0) acc = carry;
+        for (int t = lane;; ++t) {
+          const float2 p = m.part[t];
+          acc.x += p.x;
+          acc.y += p.y;
+          if ((m.b.item[t].y >> 22) & 1) {
+            at_write<MODE>(out, rep, Z, alpha, row, acc);
+            break;
+          }
+          if (t == ni - 1) {
+            open = true;
+            break;
+          }
+        }
+      }
+      const unsigned ob = __ballot_sync(0xffffffffu, open);
+      carry = make_float2(0.f, 0.f);
+      if (ob) {
+        const int src = __ffs(ob) - 1;
+        carry.x = __shfl_sync(0xffffffffu, acc.x, src);
+        carry.y = __shfl_sync(0xffffffffu, acc.y, src);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.mfree[ms]);
+    }
+    return;
+  }
+
   if (wid == kAtConsumers) {
     // ------------------------------------------------------------ producer
     const int64_t nnz4 = row_ptr[n_rows] & ~int64_t(3);
-    if (lane == 0) {
-      mbar_arrive_tx(&s_win, (uint32_t)(wn * sizeof(float2)));
-      bulk_g2s(sbase, Y + wlo, (uint32_t)(wn * sizeof(float2)), &s_win);
+    int lr0, lr1, b0 = 0, nb = 0;               // this CTA's rows: an equal share of the nonzeros
+    if (PLAN) {
+      const int4 ci = cta[blockIdx.x];
+      lr0 = ci.x;
+      lr1 = ci.y;
+      b0 = ci.z;
+      nb = ci.w;
+    } else {
+      at_range(row_ptr, n_rows, blockIdx.x, gridDim.x, lane, lr0, lr1);
     }
-    // row_ptr of chunk c + kAtLook is fetched with cp.async into a small ring
-    // while chunk c is cut into batches, so the producer never waits on a
-    // global load.  A batch is at most kAtBatch rows whose nonzeros fit a stage
-    // (a longer single row is read from global memory by its consumer).
-    auto fetch_rp = [&](int c) {
-      if (c < c1)
-        for (int q = lane; q <= kAtChunk; q += 32) {
-          const int r = min(c * kAtChunk + q, n_rows);
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                           smem_u32(&s_rpring[c % kAtRpSlots][q])),
-                       "l"(row_ptr + r)
-                       : "memory");
-        }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    // row_ptr of local row r from the ring (a chunk's slot holds kAtChunk + 1
-    // entries; the end of the CTA's range at a chunk boundary is the last
-    // entry of the previous chunk)
-    auto rpv = [&](int r) -> int64_t {
-      const int c = r / kAtChunk, o = r - c * kAtChunk;
-      if (r == lr1 && o == 0) return s_rpring[(c - 1) % kAtRpSlots][kAtChunk];
-      return s_rpring[c % kAtRpSlots][o];
-    };
+    int wlo = row0 + (lr0 + lr1) / 2 - kAtWin / 2;
+    wlo = min(wlo, Ny - kAtWin);
+    wlo = max(wlo, 0) & ~1;                      // 16-byte aligned source
+    const int wn = min(kAtWin, Ny - wlo) & ~1;   // 16-byte multiple
+    if (lane == 0) {
+      sh.lr0 = lr0;
+      sh.lr1 = lr1;
+      sh.wlo = wlo;
+      sh.wn = wn;
+      mbar_arrive_tx(&sh.win, (uint32_t)(wn * sizeof(float2)));   // releases lr0 .. wn
+      bulk_g2s(sbase, Y + wlo, (uint32_t)(wn * sizeof(float2)), &sh.win);
+    }
     int k = 0;                                  // batch sequence number
-    auto issue = [&](int r0, int nr, bool sentinel) {
-      const int s = k % kAtStages;
-#ifdef TSNE_AT_SPIN
-      if (k >= kAtStages) mbar_wait_spin(&s_empty[s], ((k / kAtStages) - 1) & 1);
-#else
-      if (k >= kAtStages) mbar_wait_sleep(&s_empty[s], ((k / kAtStages) - 1) & 1);
-#endif
-      AtMeta& m = s_meta[s];
-      int64_t a_lo = 0, a_hi = 0;
-      if (!sentinel) {
-        const int64_t v = rpv(r0 + min(lane, nr));
-        if (lane <= nr) m.rp[lane] = v;
-        const int64_t e_lo = __shfl_sync(0xffffffffu, v, 0), e_hi = __shfl_sync(0xffffffffu, v, nr);
-        a_lo = e_lo & ~int64_t(3);
-        a_hi = min((e_hi + 3) & ~int64_t(3), nnz4);
-        if (e_hi + 3 - a_lo > kAtCap) a_hi = a_lo;            // does not fit: read from global
+    // batch k takes stage k % kAtStages once its consumers are done with batch
+    // k - kAtStages, and metadata slot k % kAtMetas once the finaliser is done
+    // with batch k - kAtMetas
+    auto take_slot = [&]() -> AtMeta& {
+      if (k >= kAtStages) mbar_wait_sleep(&sh.empty[k % kAtStages], ((k / kAtStages) - 1) & 1);
+      if (k >= kAtMetas) mbar_wait_sleep(&sh.mfree[k % kAtMetas], ((k / kAtMetas) - 1) & 1);
+      return sh.meta[k % kAtMetas];
+    };
+    // the stage's col/val: a bulk copy of [a_lo, a_lo + cnt) and the CSR's
+    // last < 4 nonzeros by plain loads (released by lane 0's arrive)
+    auto tail = [&](const AtBatchHdr& h, int s) {
+      if (lane < h.n_tail) {
+        const int64_t x = h.a_lo + h.cnt + lane;
+        s_col[s * kAtCap + h.cnt + lane] = col[x];
+        s_val[s * kAtCap + h.cnt + lane] = val[x];
       }
-      if (lane == 0) {
-        m.a_lo = a_lo;
-        m.a_hi = a_hi;
-        m.r0 = r0;
-        m.nrows = sentinel ? -1 : nr;
+    };
+    auto stream = [&](const AtBatchHdr& h, int s, uint32_t extra) {
+      mbar_arrive_tx(&sh.full[s], (uint32_t)h.cnt * 8u + extra);
+      if (h.cnt) {
+        bulk_g2s(smem_u32(s_col + s * kAtCap), col + h.a_lo, (uint32_t)h.cnt * 4u, &sh.full[s]);
+        bulk_g2s(smem_u32(s_val + s * kAtCap), val + h.a_lo, (uint32_t)h.cnt * 4u, &sh.full[s]);
       }
-      __syncwarp();
-      if (lane == 0) {
-        const uint32_t cnt = (a_hi > a_lo) ? (uint32_t)(a_hi - a_lo) : 0u;
-        mbar_arrive_tx(&s_full[s], cnt * 8u);
-        if (cnt) {
-          bulk_g2s(smem_u32(s_col + s * kAtCap), col + a_lo, cnt * 4u, &s_full[s]);
-          bulk_g2s(smem_u32(s_val + s * kAtCap), val + a_lo, cnt * 4u, &s_full[s]);
+    };
+    if (PLAN) {
+      // headers prefetched 32 batches ahead; the item lists come with the data
+      auto fetch_h = [&](int k0) {
+        if (k0 + lane < nb)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                           smem_u32(&sh.hring[(k0 + lane) % kAtHdrRing])),
+                       "l"(&batches[b0 + k0 + lane].h)
+                       : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      fetch_h(0);
+      for (; k < nb;) {
+        if (k % 32 == 0) {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+          __syncwarp();
+          fetch_h(k + 32);
         }
+        const AtBatchHdr h = sh.hring[k % kAtHdrRing];
+        AtMeta& m = take_slot();
+        const int s = k % kAtStages;
+        tail(h, s);
+        if (lane == 0) m.next = 0;
+        __syncwarp();
+        if (lane == 0) {
+          stream(h, s, (uint32_t)sizeof(AtBatch));
+          bulk_g2s(smem_u32(&m.b), &batches[b0 + k], (uint32_t)sizeof(AtBatch), &sh.full[s]);
+        }
+        ++k;
+      }
+    } else {
+      RpRing rp{sh.rpring, row_ptr, lr0, lr1, 0, 0};
+      rp.start(lane);
+      int r = lr0;                              // current row
+      int64_t e = row_ptr[lr0];                 // its next nonzero (an item boundary)
+      while (r < lr1) {
+        rp.ready(r, lane);
+        AtMeta& m = take_slot();
+        const int s = k % kAtStages;
+        const AtBatchHdr h = pack_batch(rp, lane, lr1, nnz4, r, e, m.b.item);
+        tail(h, s);
+        if (lane == 0) {
+          m.b.h = h;
+          m.next = 0;
+        }
+        __syncwarp();
+        if (lane == 0) stream(h, s, 0u);
+        ++k;
+      }
+    }
+    for (int g = 0; g < kAtGroups; ++g) {       // one end marker per group
+      AtMeta& m = take_slot();
+      if (lane == 0) {
+        m.b.h.n_items = -1;
+        mbar_arrive(&sh.full[k % kAtStages]);
       }
       ++k;
-    };
-    // Batches are cut across chunk boundaries (a batch of at most kAtBatch <
-    // kAtChunk rows spans at most two chunks), so rows of ~230 nonzeros (C4:
-    // 17 per stage) do not leave a short batch at the end of every chunk.
-    for (int j = 0; j < kAtLook; ++j) fetch_rp(c0 + j);
-    int fetched = c0 + kAtLook;                 // next chunk to fetch
-    for (int row = lr0; row < lr1;) {
-      const int c = row / kAtChunk;
-      while (fetched <= c + kAtLook) fetch_rp(fetched++);
-      asm volatile("cp.async.wait_group %0;" ::"n"(kAtLook - 1) : "memory");   // chunks <= c + 1
-      __syncwarp();
-      // largest nr <= kAtBatch with rows [row, row + nr) fitting a stage (a prefix: rp grows)
-      const int l = lane + 1;
-      const int64_t base = rpv(row) & ~int64_t(3);
-      const bool ok = l <= kAtBatch && row + l <= lr1 && rpv(min(row + l, lr1)) + 3 - base <= kAtCap;
-      int nr = __popc(__ballot_sync(0xffffffffu, ok));
-      nr = nr > 0 ? nr : 1;
-      issue(row, nr, false);
-      row += nr;
     }
-    for (int g = 0; g < kAtGroups; ++g) issue(0, 0, true);   // one end marker per group
     asm volatile("cp.async.wait_all;" ::: "memory");
     return;
   }
 
   // -------------------------------------------------------------- consumers
-  mbar_wait_spin(&s_win, 0);
-  const int grp = wid / kAtRows, wr = wid % kAtRows;
+  mbar_wait_spin(&sh.win, 0);
+  const int wlo = sh.wlo, wn = sh.wn;
+  const bool own_in_win = row0 + sh.lr0 >= wlo && row0 + sh.lr1 <= wlo + wn;
+  const int grp = wid / kAtRows;
   for (int k = grp;; k += kAtGroups) {
-    const int s = k % kAtStages;
-    mbar_wait_spin(&s_full[s], (k / kAtStages) & 1);
-    const AtMeta& m = s_meta[s];
-    if (m.nrows < 0) break;                     // end marker
-    for (int br = wr; br < m.nrows; br += kAtRows) {
-      const int l = m.r0 + br;
-      const int i = row0 + l;
-      const int64_t e0 = m.rp[br], e1 = m.rp[br + 1];
-      const int64_t a_lo = m.a_lo, a_hi = m.a_hi;
-      const int32_t* cs = s_col + s * kAtCap;
-      const float* vs = s_val + s * kAtCap;
-      float2 yi;                                  // the row's own point: in the window
-      if (own_in_win) {                           // whenever the window covers the CTA's rows
+    const int s = k % kAtStages, ms = k % kAtMetas;
+    mbar_wait_spin(&sh.full[s], (k / kAtStages) & 1);
+    AtMeta& m = sh.meta[ms];
+    const int ni = m.b.h.n_items;
+    if (ni < 0) {                               // end marker (wakes the finaliser)
+      if (lane == 0) mbar_arrive(&sh.done[ms]);
+      break;
+    }
+    const int32_t* cs = s_col + s * kAtCap;
+    const float* vs = s_val + s * kAtCap;
+    int t = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(&m.next, 1) : 0, 0);
+    while (t < ni) {
+      const int2 d = m.b.item[t];
+      const int l = d.x, i = row0 + l;
+      const int beg = d.y & 0x1fff, len = (d.y >> 13) & 0x1ff;
+      float2 yi;                                // the row's own point
+      if (own_in_win) {                         // whenever the window covers the CTA's rows
         asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(yi.x), "=f"(yi.y)
             : "r"(sbase + (unsigned)(i - wlo) * 8u));
       } else {
         yi = win_y(sbase, Y, i, wlo, wn);
       }
       float ax = 0.f, ay = 0.f;
-      const int n = (int)(e1 - e0);
-      if (e0 >= a_lo && e1 <= a_hi) {             // the row is staged (the common case)
-        const int32_t* cr = cs + (e0 - a_lo);
-        const float* vr = vs + (e0 - a_lo);
-        // blocks of up to 8 x 32 entries: every gather of a block is issued
-        // before any arithmetic, so a row pays the L2 latency of its columns
-        // outside the window about once, not once per 32 entries
-        int b = 0;
-        for (; n - b > kAtEmax * 32; b += kAtEmax * 32)
-          row_block<kAtEmax>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn, lane, ax, ay);
-        switch ((n - b + 31) >> 5) {
+      const int32_t* cr = cs + beg;
+      const float* vr = vs + beg;
+      switch ((len + 31) >> 5) {
 #define TSNE_RB(e)                                                                           \
   case e:                                                                                   \
     if (e <= kAtEmax)                                                                       \
-      row_block<(e <= kAtEmax ? e : 1)>(cr + b, vr + b, n - b, i, yi, sbase, Y, wlo, wn,    \
-                                        lane, ax, ay);                                      \
+      row_block<(e <= kAtEmax ? e : 1)>(cr, vr, len, i, yi, sbase, Y, wlo, wn, lane, ax, ay); \
     break;
-          TSNE_RB(1) TSNE_RB(2) TSNE_RB(3) TSNE_RB(4) TSNE_RB(5) TSNE_RB(6) TSNE_RB(7) TSNE_RB(8)
+        TSNE_RB(1) TSNE_RB(2) TSNE_RB(3) TSNE_RB(4) TSNE_RB(5) TSNE_RB(6) TSNE_RB(7) TSNE_RB(8)
 #undef TSNE_RB
-          default: break;
-        }
-      } else if (n <= kAtLong) {
-        for (int q = lane; q < n; q += 32)
-          win_accum(yi, win_y(sbase, Y, __ldcs(col + e0 + q), wlo, wn), __ldcs(val + e0 + q), ax,
-                    ay);
+        default: break;
       }
       warp_sum2(ax, ay);
-      if (lane == 0 && n <= kAtLong) {          // longer rows: k_attract_long
-        if (MODE == 0) {
-          out[l] = make_float2(ax, ay);
-        } else {
-          const float invZ = (float)Z[1];
-          const float2 f = rep[l];
-          out[l] = make_float2(4.f * (alpha * ax - f.x * invZ), 4.f * (alpha * ay - f.y * invZ));
-        }
+      int tn = 0;
+      if (lane == 0) {
+        m.part[t] = make_float2(ax, ay);
+        tn = atomicAdd(&m.next, 1);
       }
+      t = __shfl_sync(0xffffffffu, tn, 0);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&s_empty[s]);
-  }
-}
-
-// Rows longer than kAtLong nonzeros (hubs of the kNN graph: a point that is a
-// neighbour of thousands of others) would serialise one warp of the
-// pipeline; a whole CTA takes each of them instead.  CTA b scans rows
-// [b*n/G, (b+1)*n/G) and processes the long ones: threads stride the row, the
-// sum is reduced in a fixed order (deterministic).
-constexpr int kLongThreads = 512;
-
-template <int MODE>
-__global__ void __launch_bounds__(kLongThreads)
-k_attract_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-               const float* __restrict__ val, const float2* __restrict__ Y, int row0, int n_rows,
-               float2* __restrict__ out, const float2* __restrict__ rep,
-               const double* __restrict__ Z, float alpha) {
-  __shared__ float2 s_red[kLongThreads / 32];
-  __shared__ unsigned s_ball[kLongThreads / 32];
-  const int r0 = (int)((int64_t)n_rows * blockIdx.x / gridDim.x);
-  const int r1 = (int)((int64_t)n_rows * (blockIdx.x + 1) / gridDim.x);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int base = r0; base < r1; base += kLongThreads) {
-    const int r = base + (int)threadIdx.x;
-    const bool lng = r < r1 && row_ptr[r + 1] - row_ptr[r] > kAtLong;
-    const unsigned ball = __ballot_sync(0xffffffffu, lng);
-    if (lane == 0) s_ball[wid] = ball;
-    __syncthreads();
-    for (int w = 0; w < kLongThreads / 32; ++w) {
-      unsigned b = s_ball[w];
-      while (b) {                                       // block-uniform loop
-        const int l = base + w * 32 + __ffs(b) - 1;
-        b &= b - 1;
-        const float2 yi = Y[row0 + l];
-        float ax = 0.f, ay = 0.f;
-        const int64_t eb = row_ptr[l], ee = row_ptr[l + 1];
-        for (int64_t e = eb + threadIdx.x; e < ee; e += 4 * kLongThreads) {   // 4 in flight
-          int c[4];
-          float p[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int64_t f = e + u * kLongThreads;
-            c[u] = row0 + l;                           // absent: the point itself, p = 0
-            p[u] = 0.f;
-            if (f < ee) {
-              c[u] = __ldcs(col + f);
-              p[u] = __ldcs(val + f);
-            }
-          }
-          float2 yj[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) yj[u] = __ldg(Y + c[u]);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) win_accum(yi, yj[u], p[u], ax, ay);
-        }
-        ax = warp_sum(ax);
-        ay = warp_sum(ay);
-        if (lane == 0) s_red[wid] = make_float2(ax, ay);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          float sx = 0.f, sy = 0.f;
-          for (int q = 0; q < kLongThreads / 32; ++q) { sx += s_red[q].x; sy += s_red[q].y; }
-          if (MODE == 0) {
-            out[l] = make_float2(sx, sy);
-          } else {
-            const float invZ = (float)Z[1];
-            const float2 f = rep[l];
-            out[l] = make_float2(4.f * (alpha * sx - f.x * invZ), 4.f * (alpha * sy - f.y * invZ));
-          }
-        }
-        __syncthreads();
-      }
+    if (lane == 0) {
+      mbar_arrive(&sh.empty[s]);
+      mbar_arrive(&sh.done[ms]);
     }
-    __syncthreads();
   }
 }
 
-// CTAs of the pipeline: all SMs when it runs alone (tsne_gradient); 120 when it
-// runs concurrently with the tree build on a side stream (optimiser, shards):
-// the 28 SMs it leaves free take the latency-bound tree kernels, which cannot
-// share an SM with a pipeline CTA (measured at C5: iteration 1.33 -> 1.25 ms,
-// the pass alone 0.43 -> 0.53 ms).
+// CTAs of the pipeline: all SMs when it runs alone (tsne_gradient) or when the
+// pass outlasts tree + traversal (more than 200 nonzeros per row); otherwise
+// 120 on a side stream concurrently with the tree build: the 28 SMs it leaves
+// free take the latency-bound tree kernels, which cannot share an SM with a
+// pipeline CTA (measured at C5: iteration 1.33 -> 1.25 ms, the pass alone
+// 0.43 -> 0.53 ms).
 #ifndef TSNE_AT_GRID_SHARED
 #define TSNE_AT_GRID_SHARED 120
 #endif
 constexpr int kAtGridAlone = kNumSMs;
 constexpr int kAtGridShared = TSNE_AT_GRID_SHARED;
 
+static int at_blocks(int64_t n_rows, int grid) {
+  const int64_t nch = (n_rows + kAtChunk - 1) / kAtChunk;
+  return (int)(nch < grid ? (nch > 0 ? nch : 1) : grid);
+}
+
+int attract_grid_sum(int64_t N, int64_t nnz) {
+  return at_blocks(N, nnz > 200 * N ? kAtGridAlone : kAtGridShared);
+}
+int attract_grid_shard(int64_t n_local) { return at_blocks(n_local, kAtGridShared); }
+
+void carve_attract_plan(Carver& c, AtPlan& p, int64_t n_rows, int64_t nnz_cap, int grid) {
+  p.grid = grid;
+  p.batches = c.take<AtBatch>((size_t)plan_off(n_rows, nnz_cap, grid) + 1);
+  p.cta = c.take<int4>(grid);
+}
+
+tsne_status attract_plan_build(const AtPlan& p, const int64_t* row_ptr, int64_t n_rows,
+                               cudaStream_t s) {
+  if (n_rows <= 0) return TSNE_OK;
+  k_attract_plan<<<p.grid, 32, 0, s>>>(row_ptr, (int)n_rows, static_cast<AtBatch*>(p.batches),
+                                       p.cta);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
+template <int MODE, bool PLAN>
+static tsne_status launch_win_t(const int64_t* row_ptr, const int32_t* col, const float* val,
+                                const float2* Y, int64_t Ny, int64_t row0, int64_t n_rows,
+                                const AtPlan* plan, float2* out, const float2* rep,
+                                const double* Z, float alpha, cudaStream_t s, int blocks) {
+  static bool attr = false;                    // not a stream operation (graph-capture safe)
+  if (!attr) {
+    TSNE_CUDA_TRY(cudaFuncSetAttribute(k_attract_tma<MODE, PLAN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAtSmem));
+    attr = true;
+  }
+  k_attract_tma<MODE, PLAN><<<blocks, kAtThreads, kAtSmem, s>>>(
+      row_ptr, col, val, Y, (int)Ny, (int)row0, (int)n_rows,
+      PLAN ? static_cast<const AtBatch*>(plan->batches) : nullptr, PLAN ? plan->cta : nullptr,
+      out, rep, Z, alpha);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
+// plan: the batches of this CSR cut by attract_plan_build (its grid), or null
+// (the kernel cuts them; grid CTAs at most)
 template <int MODE>
 static tsne_status launch_win(const int64_t* row_ptr, const int32_t* col, const float* val,
                               const float2* Y, int64_t Ny, int64_t row0, int64_t n_rows,
                               float2* out, const float2* rep, const double* Z, float alpha,
-                              cudaStream_t s, int grid) {
+                              const AtPlan* plan, cudaStream_t s, int grid) {
   if (n_rows <= 0) return TSNE_OK;
-  static bool attr = false;                    // not a stream operation (graph-capture safe)
-  if (!attr) {
-    TSNE_CUDA_TRY(cudaFuncSetAttribute(k_attract_tma<MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAtSmem));
-    attr = true;
-  }
-  const int64_t nch = (n_rows + kAtChunk - 1) / kAtChunk;
-  const int blocks = (int)(nch < grid ? nch : grid);
-  k_attract_tma<MODE><<<blocks, kAtThreads, kAtSmem, s>>>(row_ptr, col, val, Y, (int)Ny,
-                                                           (int)row0, (int)n_rows, out, rep, Z,
-                                                           alpha);
-  TSNE_LAUNCH_CHECK();
-  const int64_t lb = (n_rows + kLongThreads - 1) / kLongThreads;
-  const int lblocks = (int)(lb < 2 * kNumSMs ? lb : 2 * kNumSMs);
-  k_attract_long<MODE><<<lblocks, kLongThreads, 0, s>>>(row_ptr, col, val, Y, (int)row0,
-                                                        (int)n_rows, out, rep, Z, alpha);
-  TSNE_LAUNCH_CHECK();
-  return TSNE_OK;
+  if (plan)
+    return launch_win_t<MODE, true>(row_ptr, col, val, Y, Ny, row0, n_rows, plan, out, rep, Z,
+                                    alpha, s, plan->grid);
+  return launch_win_t<MODE, false>(row_ptr, col, val, Y, Ny, row0, n_rows, nullptr, out, rep, Z,
+                                   alpha, s, at_blocks(n_rows, grid));
 }
 
 __device__ __forceinline__ float sgnf(float x) { return (float)((x > 0.f) - (x < 0.f)); }
@@ -614,15 +866,16 @@ int update_blocks(int64_t N) {
 tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, const float* val,
                                 const float2* Y, int64_t N, const float2* rep, const double* Z,
                                 float alpha, float2* dY, cudaStream_t s) {
-  return launch_win<1>(row_ptr, col, val, Y, N, 0, N, dY, rep, Z, alpha, s, kAtGridAlone);
+  return launch_win<1>(row_ptr, col, val, Y, N, 0, N, dY, rep, Z, alpha, nullptr, s, kAtGridAlone);
 }
 
 tsne_status launch_attract_sum(const int64_t* row_ptr, const int32_t* col, const float* val,
-                               const float2* Y, int64_t N, int64_t nnz, float2* A, cudaStream_t s) {
+                               const float2* Y, int64_t N, int64_t nnz, float2* A,
+                               const AtPlan* plan, cudaStream_t s) {
   // rows of more than ~200 nonzeros (K = 150 workloads): the pass outweighs the tree build
-  // it runs beside, so it keeps every SM (C4: 1.73 ms on 148 CTAs, 2.04 ms on 120)
-  const int grid = nnz > 200 * N ? kAtGridAlone : kAtGridShared;
-  return launch_win<0>(row_ptr, col, val, Y, N, 0, N, A, nullptr, nullptr, 1.f, s, grid);
+  // it runs beside, so it keeps every SM (attract_grid_sum)
+  return launch_win<0>(row_ptr, col, val, Y, N, 0, N, A, nullptr, nullptr, 1.f, plan, s,
+                       attract_grid_sum(N, nnz));
 }
 
 tsne_status launch_update(const float2* Yin, const float2* A, int64_t N, TreeWS& w, OptWS& o,
@@ -675,8 +928,8 @@ k_update_shard(const float2* __restrict__ A, const float2* __restrict__ Y, int r
 
 tsne_status launch_attract_sum_shard(const int64_t* row_ptr, const int32_t* col, const float* val,
                                      const float2* Y, int64_t N, int64_t row0, int64_t n_local,
-                                     float2* A, cudaStream_t s) {
-  return launch_win<0>(row_ptr, col, val, Y, N, row0, n_local, A, nullptr, nullptr, 1.f, s,
+                                     float2* A, const AtPlan* plan, cudaStream_t s) {
+  return launch_win<0>(row_ptr, col, val, Y, N, row0, n_local, A, nullptr, nullptr, 1.f, plan, s,
                        kAtGridShared);
 }
 

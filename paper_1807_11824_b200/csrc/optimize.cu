@@ -34,6 +34,7 @@ void carve_opt(Carver& c, OptWS& o, int64_t N, int64_t nnz) {
     o.rp[h] = c.take<int64_t>(N + 1);
     o.col[h] = c.take<int32_t>(nnz + 4);
     o.val[h] = c.take<float>(nnz + 4);
+    carve_attract_plan(c, o.plan[h], N, nnz, attract_grid_sum(N, nnz));
   }
   o.len = c.take<int64_t>(N + 1);
   size_t sb = 0;
@@ -47,6 +48,11 @@ __global__ void k_set_state(int32_t* t_dev, int32_t t0, int32_t* flag) {
   *flag = 0;
 }
 
+// the batch plan of P half h (cut by relabel(), the only writer of o.rp[h])
+static const AtPlan* plan_of(const OptWS& o, const int64_t* row_ptr) {
+  return row_ptr == o.rp[0] ? &o.plan[0] : row_ptr == o.rp[1] ? &o.plan[1] : nullptr;
+}
+
 // One iteration: the attractive sums run on a side stream
 // concurrently with the tree build and the traversal (they only need Y);
 // the update joins both.
@@ -56,7 +62,8 @@ static tsne_status one_iteration(const int64_t* row_ptr, const int32_t* col, con
                                  cudaStream_t s) {
   TSNE_CUDA_TRY(cudaEventRecord(o.ev_fork, s));
   TSNE_CUDA_TRY(cudaStreamWaitEvent(o.side, o.ev_fork, 0));
-  tsne_status st = launch_attract_sum(row_ptr, col, val, Yin, N, o.nnz, o.A, o.side);
+  tsne_status st = launch_attract_sum(row_ptr, col, val, Yin, N, o.nnz, o.A, plan_of(o, row_ptr),
+                                      o.side);
   if (st != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaEventRecord(o.ev_join, o.side));
   if ((st = build_tree(w, Yin, /*apply_shift=*/true, s)) != TSNE_OK) return st;
@@ -152,6 +159,8 @@ static tsne_status relabel(const int32_t* perm, int N, const int64_t* rp, const 
   k_relabel_rows<<<(int)(((int64_t)N * 32 + 255) / 256), 256, 0, s>>>(
       perm, N, rp, col, val, o.inv, o.rp[dst], o.col[dst], o.val[dst]);
   TSNE_LAUNCH_CHECK();
+  tsne_status st = attract_plan_build(o.plan[dst], o.rp[dst], N, s);
+  if (st != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaMemcpyAsync(o.Ya, Yn, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
   TSNE_CUDA_TRY(cudaMemcpyAsync(o.V, Vn, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
   TSNE_CUDA_TRY(cudaMemcpyAsync(o.G, Gn, sizeof(float2) * N, cudaMemcpyDeviceToDevice, s));
@@ -722,7 +731,8 @@ tsne_status profile_iterations(const int64_t* row_ptr, const int32_t* col, const
     cudaEventRecord(e[1], s);
     if (st == TSNE_OK) st = launch_traverse(w, theta, s);
     cudaEventRecord(e[2], s);
-    if (st == TSNE_OK) st = launch_attract_sum(o.rp[0], o.col[0], o.val[0], a, N, o.nnz, o.A, s);
+    if (st == TSNE_OK)
+      st = launch_attract_sum(o.rp[0], o.col[0], o.val[0], a, N, o.nnz, o.A, &o.plan[0], s);
     cudaEventRecord(e[3], s);
     if (st == TSNE_OK) st = launch_update(a, o.A, N, w, o, sc, b, o.V, o.G, s);
     cudaEventRecord(e[4], s);

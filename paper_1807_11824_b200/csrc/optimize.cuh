@@ -14,6 +14,20 @@ struct Sched {
 // Morton order of the current embedding (locality of the y_j gathers of the
 // attractive pass and of the tree build); `lab[k]` is the caller's index of
 // internal point k, and P is kept in internal labels (two CSR copies A/B).
+// The attractive pass's batches of one CSR, cut once (attract.cu,
+// k_attract_plan) and reused by every iteration until the CSR changes, so
+// the pipeline's producer only streams.  grid: the pass's CTAs.
+struct AtPlan {
+  void* batches = nullptr;
+  int4* cta = nullptr;
+  int grid = 0;
+};
+int attract_grid_sum(int64_t N, int64_t nnz);     // CTAs of launch_attract_sum
+int attract_grid_shard(int64_t n_local);          // CTAs of launch_attract_sum_shard
+void carve_attract_plan(Carver& c, AtPlan& p, int64_t n_rows, int64_t nnz_cap, int grid);
+tsne_status attract_plan_build(const AtPlan& p, const int64_t* row_ptr, int64_t n_rows,
+                               cudaStream_t s);
+
 struct OptWS {
   int64_t N = 0, nnz = 0;
   int32_t* t_dev = nullptr;   // iteration counter read by the update kernel
@@ -31,6 +45,7 @@ struct OptWS {
   int64_t* rp[2] = {nullptr, nullptr};
   int32_t* col[2] = {nullptr, nullptr};
   float* val[2] = {nullptr, nullptr};
+  AtPlan plan[2];                        // the attractive pass's batches of P half h
   int64_t* len = nullptr;                // N+1 row lengths -> scanned row_ptr
   void* scan_tmp = nullptr;
   size_t scan_tmp_bytes = 0;
@@ -42,7 +57,8 @@ tsne_status launch_attract_grad(const int64_t* row_ptr, const int32_t* col, cons
                                 const float2* Y, int64_t N, const float2* rep, const double* Z,
                                 float alpha, float2* dY, cudaStream_t s);
 tsne_status launch_attract_sum(const int64_t* row_ptr, const int32_t* col, const float* val,
-                               const float2* Y, int64_t N, int64_t nnz, float2* A, cudaStream_t s);
+                               const float2* Y, int64_t N, int64_t nnz, float2* A,
+                               const AtPlan* plan, cudaStream_t s);
 tsne_status launch_update(const float2* Yin, const float2* A, int64_t N, TreeWS& w, OptWS& o,
                           const Sched& sc, float2* Yout, float2* V, float2* G, cudaStream_t s);
 

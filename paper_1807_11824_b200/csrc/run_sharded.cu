@@ -115,6 +115,7 @@ struct RankPlan {
   int64_t* rp_l;           // S + 1
   int32_t* col_l;          // cap (own rows)
   float* val_l;            // cap
+  AtPlan atp;              // the attractive pass's batches of the own rows
   float2* Yfull;           // G S
   float2* Yloc;            // S
   float2 *V, *Gn, *rep, *A;  // S each
@@ -154,6 +155,7 @@ size_t plan(RankPlan& p, void* base, int64_t N, int32_t D, int32_t K, int G) {
   p.rp_l = c.take<int64_t>(S + 1);
   p.col_l = c.take<int32_t>(p.cap + 4);
   p.val_l = c.take<float>(p.cap + 4);
+  carve_attract_plan(c, p.atp, S, p.cap, attract_grid_shard(S));
   p.Yfull = c.take<float2>(G * S);
   p.Yloc = c.take<float2>(S);
   p.V = c.take<float2>(S);
@@ -224,7 +226,7 @@ tsne_status iteration(RankPlan& p, ShardWS& w, const NcclApi* nc, ncclComm_t com
   TSNE_CUDA_TRY(cudaEventRecord(r.fork, s));
   TSNE_CUDA_TRY(cudaStreamWaitEvent(r.side, r.fork, 0));
   tsne_status st = launch_attract_sum_shard(p.rp_l, p.col_l, p.val_l, p.Yfull, p.N, r0, p.n_loc,
-                                            p.A, r.side);
+                                            p.A, &p.atp, r.side);
   if (st != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaEventRecord(r.join, r.side));
   if ((st = shard_forces(w, p.Yfull, p.N, r0, r1, theta, recentre, p.rep, p.zpart, s)) != TSNE_OK)
@@ -399,6 +401,8 @@ tsne_status tsne_run_sharded(const float* X_local, int64_t N_local, int64_t N, i
     TSNE_CUDA_TRY(cudaMemcpyAsync(p.val_l, p.val2 + e0, sizeof(float) * (e1 - e0),
                                   cudaMemcpyDeviceToDevice, s));
   }
+  p.atp.grid = attract_grid_shard(n_loc);   // <= the grid the plan was sized for
+  if ((st = attract_plan_build(p.atp, p.rp_l, n_loc, s)) != TSNE_OK) return st;
   TSNE_CUDA_TRY(cudaEventRecord(r.ev[3], s));
   // 4. iterations
   TSNE_CUDA_TRY(cudaMemsetAsync(p.Yfull, 0, sizeof(float2) * world * S, s));

@@ -16,7 +16,7 @@ tsne_status shard_forces(ShardWS& w, const float2* Y, int64_t N, int64_t row0, i
 tsne_status shard_recentre(ShardWS& w, float2* Y, int64_t N, cudaStream_t s);
 tsne_status launch_attract_sum_shard(const int64_t* row_ptr, const int32_t* col, const float* val,
                                      const float2* Y, int64_t N, int64_t row0, int64_t n_local,
-                                     float2* A, cudaStream_t s);
+                                     float2* A, const AtPlan* plan, cudaStream_t s);
 tsne_status launch_update_shard(const float2* A, const float2* Y, int64_t row0, int64_t n_local,
                                 const float2* rep, const double* zp, int world, int t,
                                 const Sched& sc, const BoxInfo* box, float2* V, float2* G,
