@@ -113,7 +113,10 @@ struct AtShared {            // the kernel's static shared memory
   int32_t lr0, lr1, wlo, wn;
 };
 // the window takes what the 227 KB per-CTA limit leaves
-constexpr int kAtSmemLimit = 232448;
+#ifndef TSNE_AT_SMEM_LIMIT
+#define TSNE_AT_SMEM_LIMIT 232448
+#endif
+constexpr int kAtSmemLimit = TSNE_AT_SMEM_LIMIT;
 constexpr int kAtWin =
     (int)(((kAtSmemLimit - (int)sizeof(AtShared) - 64 - kAtStages * kAtCap * 8) / 8) & ~63);
 static_assert(kAtWin >= 4096, "window");

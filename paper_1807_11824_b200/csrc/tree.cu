@@ -3,23 +3,27 @@
 //  k_bbox        step 1: exact min/max, root box (D8)         [H1]
 //  k_keys        fp64 quantisation -> 48-bit Morton key (D8, D9) [H2]
 //  radix sort    (key, point id) pairs                         [H2]
-//  k_gather      Y in Morton order + fixed-point coordinates + block sums
+//  k_gather      Y in Morton order, fixed-point coordinates, block sums,
+//                split deltas (common-prefix length of sorted neighbours)
 //  k_bscan       exclusive scan of the block sums (one block)
-//  k_karras      binary radix tree over the sorted keys        [H3], and the
-//                exclusive prefix sums of the fixed-point coordinates
-//                (integers: exact, deterministic)
-//  k_quad_rank   which binary nodes are quad cells; chain rank [H3]
-//  scan          quad-node count per start position -> pre-order index
+//  k_radix_build exclusive prefix sums of the fixed-point coordinates
+//                (integers: exact, deterministic) [H4], and the binary
+//                radix tree bottom-up: node ranges, quad-cell test,
+//                start-chain counts                              [H3]
+//  k_scan_cnt    quad nodes per start position -> pre-order base [H3]
 //  k_quad_emit   pre-order node records, counts, centres of mass [H3, H4]
 //
-// The compressed quadtree is derived from a Karras (2012) binary radix tree:
-// a binary node whose common prefix has length delta lies in the cell of
-// level L = min(delta, 48) / 2 (48-bit keys, 24 levels, D9); it is a quad
-// node iff its parent's level is smaller (otherwise it merges into the
-// parent).  Keys tie-break by index (delta >= 48 -> identical keys -> a
-// level-24 bucket).  DESIGN.md sec. 6.
+// The compressed quadtree is derived from the binary radix tree (Karras 2012)
+// over the sorted keys: a binary node whose common prefix has length delta
+// lies in the cell of level L = min(delta, 48) / 2 (48-bit keys, 24 levels,
+// D9); it is a quad node iff its parent's level is smaller (otherwise it
+// merges into the parent).  Keys tie-break by sorted position (delta >= 48 ->
+// identical keys -> a level-24 bucket).  The binary tree is built bottom-up
+// (Apetrei 2014): internal node p is the split between sorted positions p and
+// p + 1; a node [l, r]'s parent is the split next to it with the longer common
+// prefix (delta(r) vs delta(l - 1): never equal, so the tree is the unique
+// binary radix tree).  DESIGN.md sec. 6.2.
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include "tree.cuh"
 
@@ -33,22 +37,17 @@ struct LL2Sum {
   }
 };
 
-size_t tree_cub_bytes(int64_t N, size_t* sort_b, size_t* scan_b, size_t* scan2_b) {
-  size_t a = 0, b = 0, c = 0;
+size_t tree_cub_bytes(int64_t N) {
+  size_t a = 0;
   cub::DoubleBuffer<uint64_t> dk(nullptr, nullptr);
   cub::DoubleBuffer<int32_t> dv(nullptr, nullptr);
   cub::DeviceRadixSort::SortPairs(nullptr, a, dk, dv, (int)N, 0, kKeyBits);
-  cub::DeviceScan::ExclusiveSum(nullptr, c, (int32_t*)nullptr, (int32_t*)nullptr, (int)(N + 1));
-  if (sort_b) *sort_b = a;
-  if (scan_b) *scan_b = b;
-  if (scan2_b) *scan2_b = c;
-  return a + b + c;
+  return a;
 }
 
 void carve_tree(Carver& c, TreeWS& w, int64_t N) {
   w.N = N;
-  size_t sb, cb, c2b;
-  tree_cub_bytes(N, &sb, &cb, &c2b);
+  const size_t sb = tree_cub_bytes(N);
   w.keys_a = c.take<uint64_t>(N);
   w.keys_b = c.take<uint64_t>(N);
   w.vals_a = c.take<int32_t>(N);
@@ -59,17 +58,13 @@ void carve_tree(Carver& c, TreeWS& w, int64_t N) {
   w.fq = c.take<longlong2>(N + 1);
   w.S = c.take<longlong2>(N + 1);
   w.bsum = c.take<longlong2>((N + 1 + 255) / 256 + 1);
-  (void)cb;
-  w.bfirst = c.take<int32_t>(N);
-  w.blast = c.take<int32_t>(N);
-  w.bdelta = c.take<int32_t>(N);
-  w.bparent = c.take<int32_t>(N);
-  w.lparent = c.take<int32_t>(N);
-  w.rank = c.take<int32_t>(2 * N);
+  w.dl = c.take<uint8_t>(N);
+  w.slot = c.take<unsigned long long>(N);
+  w.nfo = c.take<int4>(N);
   w.cnt = c.take<int32_t>(N + 1);
   w.base = c.take<int32_t>(N + 1);
-  w.scan2_tmp = c.take<char>(c2b);
-  w.scan2_tmp_bytes = c2b;
+  w.tsum = c.take<int32_t>((N + 1 + kScanTile - 1) / kScanTile);
+  w.ctl = c.take<uint32_t>(2);
   w.nodes = c.take<float4>(2 * N);
   w.nfirst = c.take<int32_t>(2 * N);
   w.com64 = c.take<double2>(2 * N);
@@ -232,11 +227,16 @@ __device__ __forceinline__ uint32_t quantise(float y, double lo, double s) {
 // so the attractive pass may read Y concurrently.
 __global__ void k_keys(const float2* __restrict__ Y, int N, const BoxInfo* __restrict__ box,
                        int apply_shift, uint64_t* __restrict__ keys, int32_t* __restrict__ vals,
-                       int32_t* __restrict__ cnt, int32_t* __restrict__ has_bucket) {
+                       int32_t* __restrict__ cnt, int32_t* __restrict__ has_bucket,
+                       int32_t* __restrict__ tsum, int ntiles, uint32_t* __restrict__ ctl) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i > N) return;
   cnt[i] = 0;
-  if (i == 0) *has_bucket = 0;
+  if (i < ntiles) tsum[i] = 0;
+  if (i == 0) {
+    *has_bucket = 0;
+    ctl[0] = ctl[0] + 1u;                               // build epoch (k_radix_build)
+  }
   if (i == N) return;
   const BoxInfo b = *box;
   float2 y = Y[i];
@@ -252,11 +252,14 @@ __global__ void k_keys(const float2* __restrict__ Y, int N, const BoxInfo* __res
 
 tsne_status tree_ws_init(TreeWS& w, cudaStream_t s) {
   TSNE_CUDA_TRY(cudaMemsetAsync(w.counter, 0, 8 * sizeof(unsigned), s));
+  // the radix build's node slots are tagged with a build epoch counted from 0
+  TSNE_CUDA_TRY(cudaMemsetAsync(w.ctl, 0, 2 * sizeof(uint32_t), s));
+  TSNE_CUDA_TRY(cudaMemsetAsync(w.slot, 0, w.N * sizeof(unsigned long long), s));
   return TSNE_OK;
 }
 
 // ---------------------------------------------------------------- gather
-constexpr int kScanBlock = 256;   // k_gather / k_karras block = prefix-sum block
+constexpr int kScanBlock = 256;   // k_gather / k_radix_build block = prefix-sum block
 
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
 #pragma unroll
@@ -264,10 +267,64 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
   return v;
 }
 
+// Exclusive scan over the CTA in thread order (blockDim a multiple of 32,
+// <= 1024); *tot = the CTA total.  Integer sums: exact in any association.
+__device__ longlong2 cta_scan_ll2(long long x, long long y, longlong2* tot) {
+  __shared__ long long wx[32], wy[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  long long ix = x, iy = y;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long ax = __shfl_up_sync(0xffffffffu, ix, o);
+    const long long ay = __shfl_up_sync(0xffffffffu, iy, o);
+    if (lane >= o) { ix += ax; iy += ay; }
+  }
+  if (lane == 31) { wx[wid] = ix; wy[wid] = iy; }
+  __syncthreads();
+  long long ox = 0, oy = 0, tx = 0, ty = 0;
+  for (int q = 0; q < nw; ++q) {
+    if (q == wid) { ox = tx; oy = ty; }
+    tx += wx[q];
+    ty += wy[q];
+  }
+  __syncthreads();                                    // wx/wy reusable
+  *tot = make_longlong2(tx, ty);
+  return make_longlong2(ox + ix - x, oy + iy - y);
+}
+
+__device__ int cta_scan_i32(int x, int* tot) {
+  __shared__ int wv[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int ix = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, ix, o);
+    if (lane >= o) ix += a;
+  }
+  if (lane == 31) wv[wid] = ix;
+  __syncthreads();
+  int o = 0, t = 0;
+  for (int q = 0; q < nw; ++q) {
+    if (q == wid) o = t;
+    t += wv[q];
+  }
+  __syncthreads();
+  *tot = t;
+  return o + ix - x;
+}
+
+// split delta of sorted position pos (< N - 1): common-prefix length of the
+// (key, position) strings at pos and pos + 1
+__device__ __forceinline__ uint8_t delta_of(uint64_t a, uint64_t b, int pos) {
+  return (uint8_t)(a != b ? __clzll(a ^ b) - (64 - kKeyBits)
+                          : kKeyBits + __clz((uint32_t)pos ^ (uint32_t)(pos + 1)));
+}
+
 __global__ void __launch_bounds__(kScanBlock)
-k_gather(const float2* __restrict__ Y, const int32_t* __restrict__ perm, int N,
-         const BoxInfo* __restrict__ box, int apply_shift, float2* __restrict__ ys,
-         longlong2* __restrict__ fq, longlong2* __restrict__ bsum) {
+k_gather(const float2* __restrict__ Y, const int32_t* __restrict__ perm,
+         const uint64_t* __restrict__ keys, int N, const BoxInfo* __restrict__ box,
+         int apply_shift, float2* __restrict__ ys, longlong2* __restrict__ fq,
+         longlong2* __restrict__ bsum, uint8_t* __restrict__ dl) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   long long qx = 0, qy = 0;
   if (k < N) {
@@ -280,6 +337,7 @@ k_gather(const float2* __restrict__ Y, const int32_t* __restrict__ perm, int N,
     const double cx = box->cx, cy = box->cy, inv = kFixScale / box->r0;
     qx = __double2ll_rn(__dmul_rn(__dsub_rn((double)y.x, cx), inv));
     qy = __double2ll_rn(__dmul_rn(__dsub_rn((double)y.y, cy), inv));
+    if (k < N - 1) dl[k] = delta_of(keys[k], keys[k + 1], k);
   }
   if (k <= N) fq[k] = make_longlong2(qx, qy);      // fq[N] = 0
   // block sum (exact integer arithmetic: the order does not matter)
@@ -335,158 +393,183 @@ __global__ void __launch_bounds__(1024) k_bscan(longlong2* __restrict__ bsum, in
   }
 }
 
-// ---------------------------------------------------------------- H3 Karras
-// common-prefix length of sorted keys a, b within the kKeyBits-bit keys;
-// equal keys are told apart by their index (kKeyBits + prefix of a ^ b)
-// (the key of a is passed in a register: every search step of a node compares against it)
-__device__ __forceinline__ int kdelta_k(const uint64_t* __restrict__ k, int N, uint64_t ka, int a,
-                                        int b) {
-  if ((unsigned)b >= (unsigned)N) return -1;
-  const uint64_t kb = __ldg(k + b);
-  if (ka != kb) return __clzll(ka ^ kb) - (64 - kKeyBits);
-  return kKeyBits + __clz((uint32_t)a ^ (uint32_t)b);
-}
-
-__global__ void __launch_bounds__(kScanBlock)
-k_karras(const uint64_t* __restrict__ keys, int N, int32_t* __restrict__ bfirst,
-         int32_t* __restrict__ blast, int32_t* __restrict__ bdelta, int32_t* __restrict__ bparent,
-         int32_t* __restrict__ lparent, const longlong2* __restrict__ fq,
-         const longlong2* __restrict__ boff, longlong2* __restrict__ S) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  {
-    // S[i] = boff[block] + exclusive scan of fq within the block (i <= N)
-    const longlong2 v = i <= N ? fq[i] : make_longlong2(0, 0);
-    long long ix = v.x, iy = v.y;                    // inclusive warp scan
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long ax = __shfl_up_sync(0xffffffffu, ix, o);
-      const long long ay = __shfl_up_sync(0xffffffffu, iy, o);
-      if (lane >= o) { ix += ax; iy += ay; }
-    }
-    __shared__ long long wx[kScanBlock / 32], wy[kScanBlock / 32];
-    if (lane == 31) { wx[wid] = ix; wy[wid] = iy; }
-    __syncthreads();
-    long long ox = boff[blockIdx.x].x, oy = boff[blockIdx.x].y;
-    for (int q = 0; q < wid; ++q) { ox += wx[q]; oy += wy[q]; }
-    if (i <= N) S[i] = make_longlong2(ox + ix - v.x, oy + iy - v.y);
-  }
-  if (i >= N - 1) return;
-  const uint64_t ki = __ldg(keys + i);
-  int d = (kdelta_k(keys, N, ki, i, i + 1) - kdelta_k(keys, N, ki, i, i - 1)) >= 0 ? 1 : -1;
-  int dmin = kdelta_k(keys, N, ki, i, i - d);
-  int lmax = 2;
-  while (kdelta_k(keys, N, ki, i, i + lmax * d) > dmin) lmax <<= 1;
-  int l = 0;
-  for (int t = lmax >> 1; t >= 1; t >>= 1)
-    if (kdelta_k(keys, N, ki, i, i + (l + t) * d) > dmin) l += t;
-  int j = i + l * d;
-  int dnode = kdelta_k(keys, N, ki, i, j);
-  int s = 0, t = l;
-  do {
-    t = (t + 1) >> 1;
-    if (kdelta_k(keys, N, ki, i, i + (s + t) * d) > dnode) s += t;
-  } while (t > 1);
-  int gamma = i + s * d + (d < 0 ? -1 : 0);
-  int lo = min(i, j), hi = max(i, j);
-  bfirst[i] = lo;
-  blast[i] = hi;
-  bdelta[i] = dnode;
-  if (lo == gamma) lparent[gamma] = i; else bparent[gamma] = i;
-  if (hi == gamma + 1) lparent[gamma + 1] = i; else bparent[gamma + 1] = i;
-  if (i == 0) bparent[0] = -1;
-}
-
+// ---------------------------------------------------------------- H3 radix tree
 __device__ __forceinline__ int qlevel(int delta) {
   return (delta < kKeyBits ? delta : kKeyBits) >> 1;
 }
 
-// binary node ids: [0, N-1) internal, [N-1, 2N-1) leaves (sorted position id-(N-1))
-__device__ __forceinline__ bool internal_is_quad(const int32_t* bdelta, const int32_t* bparent,
-                                                 int a) {
-  int p = bparent[a];
-  return p < 0 || qlevel(bdelta[p]) < qlevel(bdelta[a]);
+__device__ __forceinline__ void add_tile(int pos, int cc, int32_t* tsum, int* st, int t_hi) {
+  const int t = pos / kScanTile;
+  if (t_hi - t < 8) atomicAdd(&st[t_hi - t], cc);
+  else atomicAdd(&tsum[t], cc);
 }
 
-__global__ void k_quad_rank(int N, const int32_t* __restrict__ bfirst,
-                            const int32_t* __restrict__ bdelta, const int32_t* __restrict__ bparent,
-                            const int32_t* __restrict__ lparent, int32_t* __restrict__ rank,
-                            int32_t* __restrict__ cnt) {
-  int id = blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= 2 * N - 1) return;
-  int s, p;
-  bool quad, deepest;
-  if (id < N - 1) {
-    s = bfirst[id];
-    p = bparent[id];
-    quad = internal_is_quad(bdelta, bparent, id);
-    deepest = bdelta[id] >= kKeyBits;                 // bucket top
-  } else {
-    int k = id - (N - 1);
-    s = k;
-    p = lparent[k];
-    quad = qlevel(bdelta[p]) < kLevels;               // not inside a bucket
-    deepest = true;
+__device__ void radix_climb(const uint8_t* __restrict__ dl, int N, const uint32_t* __restrict__ ctl,
+                            unsigned long long* __restrict__ slot, int4* __restrict__ nfo,
+                            int32_t* __restrict__ cnt, int32_t* __restrict__ tsum, int* st, int t_hi,
+                            int k) {
+  const unsigned long long tag = (unsigned long long)ctl[0] << 32;
+  const int dprev = k > 0 ? dl[k - 1] : -1;
+  const int dnext = k < N - 1 ? dl[k] : -1;
+  bool left = dnext > dprev;                           // leaf k is the left child of split k
+  int p = left ? k : k - 1;
+  int dp = left ? dnext : dprev;
+  int cc = dp < kKeyBits ? 1 : 0;                      // a leaf inside a bucket is no quad node
+  if (!left) {                                         // a right child tops its start chain
+    cnt[k] = cc;
+    if (cc) add_tile(k, cc, tsum, st, t_hi);
   }
-  if (!quad) { rank[id] = -1; return; }
-  int r = 0;
-  for (int a = p; a >= 0 && bfirst[a] == s; a = bparent[a])
-    if (internal_is_quad(bdelta, bparent, a)) ++r;
-  rank[id] = r;
-  if (deepest) cnt[s] = r + 1;
+  int l = k, r = k;
+  for (;;) {
+    const uint32_t mine = left ? ((uint32_t)l | ((uint32_t)cc << 25)) : (uint32_t)r;
+    const unsigned long long old = atomicExch(slot + p, tag | mine);
+    if ((old & 0xffffffff00000000ull) != tag) return;  // first to arrive
+    int ccl;
+    if (left) {
+      r = (int)(uint32_t)old;
+      ccl = cc;
+    } else {
+      l = (int)((uint32_t)old & ((1u << 25) - 1u));
+      ccl = (int)((uint32_t)old >> 25);
+    }
+    // node p = [l, r], delta dp; its parent
+    int pp, dpp;
+    bool pleft;
+    const int dr = r < N - 1 ? dl[r] : -1, dlf = l > 0 ? dl[l - 1] : -1;
+    if (dr < 0 && dlf < 0) {
+      pp = -1; dpp = -1; pleft = false;
+    } else {
+      pleft = dr > dlf;
+      pp = pleft ? r : l - 1;
+      dpp = pleft ? dr : dlf;
+    }
+    const bool quad = pp < 0 || qlevel(dpp) < qlevel(dp);
+    cc = ccl + (quad ? 1 : 0);
+    nfo[p] = make_int4(l, r, quad ? cc : -1, dpp);
+    if (!pleft) {                                      // right child or root: chain top
+      cnt[l] = cc;
+      if (cc) add_tile(l, cc, tsum, st, t_hi);
+    }
+    if (pp < 0) return;
+    p = pp;
+    dp = dpp;
+    left = pleft;
+  }
 }
 
-__global__ void k_quad_emit(int N, const int32_t* __restrict__ bfirst,
-                            const int32_t* __restrict__ blast, const int32_t* __restrict__ bdelta,
-                            const int32_t* __restrict__ bparent, const int32_t* __restrict__ rank,
-                            const int32_t* __restrict__ base, const float2* __restrict__ ys,
-                            const longlong2* __restrict__ S, const BoxInfo* __restrict__ box,
-                            float4* __restrict__ nodes, int32_t* __restrict__ nfirst,
-                            double2* __restrict__ com64, int32_t* __restrict__ leafnode,
-                            int32_t* __restrict__ has_bucket) {
-  int id = blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= 2 * N - 1) return;
-  int r = rank[id];
-  if (r < 0) return;
-  int s, e, level;
-  if (id < N - 1) {
-    s = bfirst[id];
-    e = blast[id];
-    int dl = bdelta[id];
-    if (dl < kKeyBits) {
-      level = qlevel(dl);
-    } else {                                          // bucket top
-      int p = bparent[id];
-      level = (p < 0 || bdelta[p] <= kKeyBits - 3) ? kLevelBucketTest : kLevelBucket;
+// (k_radix_build first writes S = the exclusive prefix sums of the fixed-point
+// coordinates over its block of kScanBlock positions, offset by the block's
+// scanned sum.)  One thread per leaf climbs while it is the second child to reach a node
+// (atomic exchange on the node's slot, tagged with the build epoch; the first
+// leaves its range end there and stops).  For the node [l, r] it resolves it
+// records (l, r, cc, delta(parent)), cc = quad nodes on the chain of nodes
+// starting at l from the bottom up to it (-1 if it is not a quad node), and
+// at the top of a start chain cnt[l] = the chain's quad-node count (added to
+// the sum of its kScanTile tile, tsum).
+__global__ void __launch_bounds__(kScanBlock)
+k_radix_build(const uint8_t* __restrict__ dl, int N, const uint32_t* __restrict__ ctl,
+              unsigned long long* __restrict__ slot, int4* __restrict__ nfo,
+              int32_t* __restrict__ cnt, int32_t* __restrict__ tsum,
+              const longlong2* __restrict__ fq, const longlong2* __restrict__ boff,
+              longlong2* __restrict__ S) {
+  // chain counts are summed per kScanTile tile: in shared memory for the 8
+  // tiles ending at the CTA's own, in global memory beyond
+  __shared__ int st[8];
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  {
+    const longlong2 v = k <= N ? fq[k] : make_longlong2(0, 0);
+    longlong2 tot;
+    const longlong2 ex = cta_scan_ll2(v.x, v.y, &tot);
+    const longlong2 o = boff[blockIdx.x];
+    if (k <= N) S[k] = make_longlong2(o.x + ex.x, o.y + ex.y);
+  }
+  const int t_hi = (blockIdx.x * blockDim.x + blockDim.x - 1) / kScanTile;
+  if (threadIdx.x < 8) st[threadIdx.x] = 0;
+  __syncthreads();
+  if (k < N) radix_climb(dl, N, ctl, slot, nfo, cnt, tsum, st, t_hi, k);
+  __syncthreads();
+  if (threadIdx.x < 8 && st[threadIdx.x] && t_hi - (int)threadIdx.x >= 0)
+    atomicAdd(&tsum[t_hi - threadIdx.x], st[threadIdx.x]);
+}
+
+// exclusive scan of cnt[0..n) -> base[0..n) (n = N + 1: base[N] = node count);
+// a tile's prefix is the sum of the tile sums before it (k_radix_build)
+__global__ void __launch_bounds__(kSortThreads)
+k_scan_cnt(const int32_t* __restrict__ cnt, int n, int32_t* __restrict__ base,
+           const int32_t* __restrict__ tsum) {
+  constexpr int kPer = kScanTile / kSortThreads;      // 16, as 4 int4
+  const int t = blockIdx.x;
+  int pp = 0;
+  for (int q = threadIdx.x; q < t; q += blockDim.x) pp += tsum[q];
+  int ptot;
+  (void)cta_scan_i32(pp, &ptot);                      // ptot = sum of the tiles before t
+  const int i0 = t * kScanTile + threadIdx.x * kPer;
+  int v[kPer], sum = 0;
+  if (i0 + kPer <= n) {
+#pragma unroll
+    for (int q = 0; q < kPer / 4; ++q) {
+      const int4 a = reinterpret_cast<const int4*>(cnt + i0)[q];
+      v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
     }
   } else {
-    s = e = id - (N - 1);
-    level = kLevelLeaf;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) v[q] = i0 + q < n ? cnt[i0 + q] : 0;
   }
-  int pre = base[s] + r;
-  int skip = base[e + 1];
-  uint32_t count = (uint32_t)(e - s + 1);
-  float cxf, cyf;
-  double2 c64;
-  if (count == 1) {
-    float2 y = ys[s];
-    cxf = y.x; cyf = y.y;
-    c64 = make_double2((double)y.x, (double)y.y);
-    leafnode[s] = pre;
-  } else {
-    longlong2 a = S[e + 1], b = S[s];
-    const double sc = __ddiv_rn(box->r0, kFixScale);
-    double mx = __ddiv_rn(__dmul_rn((double)(a.x - b.x), sc), (double)count);
-    double my = __ddiv_rn(__dmul_rn((double)(a.y - b.y), sc), (double)count);
-    c64 = make_double2(__dadd_rn(box->cx, mx), __dadd_rn(box->cy, my));
-    cxf = (float)c64.x; cyf = (float)c64.y;
-    if (level >= kLevelLeaf) {
-      for (int k = s; k <= e; ++k) leafnode[k] = pre;
-      atomicOr(has_bucket, 1);
-    }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) sum += v[q];
+  int tot;
+  int ex = cta_scan_i32(sum, &tot) + ptot;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    if (i0 + q < n) base[i0 + q] = ex;
+    ex += v[q];
   }
-  nodes[pre] = make_float4(cxf, cyf, (float)count,
-                           __uint_as_float((uint32_t)skip | ((uint32_t)level << 27)));
+}
+
+// Pre-order records: quad node x starting at s sits at base[s] + cnt[s] - cc(x)
+// (the nodes starting at s come top-down after every node starting before s);
+// skip = the first node after its range = base[e + 1].  Thread k emits leaf k
+// and internal node (split) k.
+__global__ void __launch_bounds__(kSortThreads)
+k_quad_emit(int N, const uint8_t* __restrict__ dl, const int4* __restrict__ nfo,
+            const int32_t* __restrict__ cnt, const int32_t* __restrict__ base,
+            const float2* __restrict__ ys, const longlong2* __restrict__ S,
+            const BoxInfo* __restrict__ box, float4* __restrict__ nodes,
+            int32_t* __restrict__ nfirst, double2* __restrict__ com64,
+            int32_t* __restrict__ leafnode, int32_t* __restrict__ has_bucket) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const int dprev = k > 0 ? dl[k - 1] : -1;
+  const int dnext = k < N - 1 ? dl[k] : -1;
+  if (max(dprev, dnext) < kKeyBits) {                 // one-point leaf
+    const int pre = base[k] + cnt[k] - 1;
+    const float2 y = ys[k];
+    nodes[pre] = make_float4(y.x, y.y, 1.f,
+                             __uint_as_float((uint32_t)base[k + 1] | ((uint32_t)kLevelLeaf << 27)));
+    nfirst[pre] = k;
+    com64[pre] = make_double2((double)y.x, (double)y.y);
+    leafnode[k] = pre;
+  }
+  if (k >= N - 1) return;
+  const int4 f = nfo[k];
+  if (f.z < 0) return;
+  const int s = f.x, e = f.y, d = dnext;
+  int level;
+  if (d < kKeyBits) level = qlevel(d);
+  else level = (f.w < 0 || f.w <= kKeyBits - 3) ? kLevelBucketTest : kLevelBucket;   // bucket top
+  const int pre = base[s] + cnt[s] - f.z;
+  const uint32_t count = (uint32_t)(e - s + 1);
+  const longlong2 a = S[e + 1], b = S[s];
+  const double sc = __ddiv_rn(box->r0, kFixScale);
+  const double mx = __ddiv_rn(__dmul_rn((double)(a.x - b.x), sc), (double)count);
+  const double my = __ddiv_rn(__dmul_rn((double)(a.y - b.y), sc), (double)count);
+  const double2 c64 = make_double2(__dadd_rn(box->cx, mx), __dadd_rn(box->cy, my));
+  if (level >= kLevelLeaf) {
+    for (int q = s; q <= e; ++q) leafnode[q] = pre;
+    atomicOr(has_bucket, 1);
+  }
+  nodes[pre] = make_float4((float)c64.x, (float)c64.y, (float)count,
+                           __uint_as_float((uint32_t)base[e + 1] | ((uint32_t)level << 27)));
   nfirst[pre] = s;
   com64[pre] = c64;
 }
@@ -497,8 +580,9 @@ static inline int cdiv(int64_t a, int b) { return (int)((a + b - 1) / b); }
 tsne_status build_tree(TreeWS& w, const float2* Y, bool apply_shift, cudaStream_t s) {
   const int N = (int)w.N;
   const int T = 256;
+  const int ntiles = cdiv((int64_t)N + 1, kScanTile);
   k_keys<<<cdiv(N + 1, T), T, 0, s>>>(Y, N, w.box, apply_shift ? 1 : 0, w.keys_a, w.vals_a, w.cnt,
-                                      w.has_bucket);
+                                      w.has_bucket, w.tsum, ntiles, w.ctl);
   TSNE_LAUNCH_CHECK();
   cub::DoubleBuffer<uint64_t> dk(w.keys_a, w.keys_b);
   cub::DoubleBuffer<int32_t> dv(w.vals_a, w.vals_b);
@@ -507,21 +591,18 @@ tsne_status build_tree(TreeWS& w, const float2* Y, bool apply_shift, cudaStream_
   w.keys_sorted = dk.Current();
   w.perm = dv.Current();
   const int nb = cdiv(N + 1, kScanBlock);
-  k_gather<<<nb, kScanBlock, 0, s>>>(Y, w.perm, N, w.box, apply_shift ? 1 : 0, w.ys, w.fq, w.bsum);
+  k_gather<<<nb, kScanBlock, 0, s>>>(Y, w.perm, w.keys_sorted, N, w.box, apply_shift ? 1 : 0, w.ys,
+                                     w.fq, w.bsum, w.dl);
   TSNE_LAUNCH_CHECK();
   k_bscan<<<1, 1024, 0, s>>>(w.bsum, nb);
   TSNE_LAUNCH_CHECK();
-  k_karras<<<nb, kScanBlock, 0, s>>>(w.keys_sorted, N, w.bfirst, w.blast, w.bdelta, w.bparent,
-                                      w.lparent, w.fq, w.bsum, w.S);
+  k_radix_build<<<nb, kScanBlock, 0, s>>>(w.dl, N, w.ctl, w.slot, w.nfo, w.cnt, w.tsum, w.fq, w.bsum,
+                                          w.S);
   TSNE_LAUNCH_CHECK();
-  k_quad_rank<<<cdiv(2 * N - 1, T), T, 0, s>>>(N, w.bfirst, w.bdelta, w.bparent, w.lparent,
-                                                w.rank, w.cnt);
+  k_scan_cnt<<<ntiles, kSortThreads, 0, s>>>(w.cnt, N + 1, w.base, w.tsum);
   TSNE_LAUNCH_CHECK();
-  size_t c2 = w.scan2_tmp_bytes;
-  TSNE_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.scan2_tmp, c2, w.cnt, w.base, N + 1, s));
-  k_quad_emit<<<cdiv(2 * N - 1, T), T, 0, s>>>(N, w.bfirst, w.blast, w.bdelta, w.bparent, w.rank,
-                                                w.base, w.ys, w.S, w.box, w.nodes, w.nfirst,
-                                                w.com64, w.leafnode, w.has_bucket);
+  k_quad_emit<<<cdiv(N, T), T, 0, s>>>(N, w.dl, w.nfo, w.cnt, w.base, w.ys, w.S, w.box, w.nodes,
+                                       w.nfirst, w.com64, w.leafnode, w.has_bucket);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }

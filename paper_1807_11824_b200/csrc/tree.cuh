@@ -39,6 +39,8 @@ constexpr int kLevelCodes = kLevels + 3;       // level codes 0..26
 static_assert(kLevelBucket < 32, "level field");
 constexpr uint32_t kSkipMask = (1u << 27) - 1u;
 constexpr int kMaxParts = 4096;
+constexpr int kScanTile = 4096;               // k_scan_cnt tile (16 per thread)
+constexpr int kSortThreads = 256;
 constexpr double kFixScale = 274877906944.0;  // 2^38: fixed-point COM sums
 static_assert(2 * kMaxTreePoints < (int64_t)kSkipMask + 1, "node index must fit the skip field");
 static_assert(kMaxTreePoints < (int64_t(1) << (63 - 38)), "count * 2^38 must fit int64");
@@ -53,13 +55,13 @@ struct TreeWS {
   longlong2* fq = nullptr;     // fixed-point coordinates (N+1)
   longlong2* S = nullptr;      // exclusive prefix sums of fq (N+1)
   longlong2* bsum = nullptr;   // per 256-point block sums of fq, then their exclusive scan
-  int32_t *bfirst = nullptr, *blast = nullptr, *bdelta = nullptr;
-  int32_t *bparent = nullptr, *lparent = nullptr;
-  int32_t* rank = nullptr;     // 2N-1 binary nodes
-  int32_t* cnt = nullptr;      // N+1
-  int32_t* base = nullptr;     // N+1
-  void* scan2_tmp = nullptr;
-  size_t scan2_tmp_bytes = 0;
+  uint8_t* dl = nullptr;       // split deltas: common-prefix length of sorted positions i, i+1
+  unsigned long long* slot = nullptr;  // per split: epoch << 32 | the first arrival's range end
+  int4* nfo = nullptr;         // per split: (first, last, chain count or -1, parent delta)
+  int32_t* cnt = nullptr;      // N+1: quad nodes starting at each sorted position
+  int32_t* base = nullptr;     // N+1: exclusive scan of cnt (base[N] = node count)
+  int32_t* tsum = nullptr;     // per kScanTile tile of cnt: its sum
+  uint32_t* ctl = nullptr;     // [0] build epoch
   float4* nodes = nullptr;     // <= 2N-1 quad nodes
   int32_t* nfirst = nullptr;
   double2* com64 = nullptr;
@@ -81,7 +83,7 @@ struct TreeWS {
 void carve_tree(Carver& c, TreeWS& w, int64_t N);
 // Zeroes the last-block-done counters of a freshly carved tree workspace.
 tsne_status tree_ws_init(TreeWS& w, cudaStream_t s);
-size_t tree_cub_bytes(int64_t N, size_t* sort_b, size_t* scan_b, size_t* scan2_b);
+size_t tree_cub_bytes(int64_t N);
 
 // Bounding box + root box of Y (shift = 0), written to w.box.
 tsne_status launch_bbox(TreeWS& w, const float2* Y, cudaStream_t s);

@@ -219,3 +219,23 @@ def test_error_monotone_in_theta_gpu(T):
         errs.append(rel(g, g0))
     assert all(a < b for a, b in zip(errs, errs[1:])), errs
     assert errs[0] < 1e-3 and errs[-1] < 0.5
+
+
+@pytest.mark.parametrize("N", [12000, 40000])
+def test_sort_bucket_overflow(T, orc, N):
+    # Two far clusters whose members interleave in index order at a regular
+    # stride (every N/nsamp-th point in one, the rest in the other): a layout
+    # adversarial to any sort that samples regular positions of its input
+    # order (the exp/sample-sort-tree branch's tree build did; kept as a
+    # parity case for extreme, index-interleaved clusters).
+    nb = -(-N // 1843)
+    nsamp = 8 * nb
+    rng = np.random.default_rng(N)
+    Y = (rng.standard_normal((N, 2)) * 0.5 + 20.0).astype(np.float32)
+    samp = (np.arange(nsamp, dtype=np.int64) * N) // nsamp
+    Y[samp] = (rng.standard_normal((nsamp, 2)) * 0.5 - 20.0).astype(np.float32)
+    rp, col, v32, _ = synth.random_csr(N, 8, seed=11)
+    g, Z = gpu_grad(T, rp, col, v32, Y, 0.5, 4.0)
+    go, Zo = orc.gradient_bh(rp, col, v32, Y, 0.5, 4.0)
+    assert abs(Z - Zo) <= 1e-6 * Zo
+    assert rel(g, go) <= 1e-4
