@@ -61,9 +61,6 @@ constexpr int kAttrWarps = kAttrThreads / 32;
 #ifndef TSNE_AT_CAP
 #define TSNE_AT_CAP 4096
 #endif
-#ifndef TSNE_AT_ITEM
-#define TSNE_AT_ITEM 256
-#endif
 constexpr int kAtGroups = TSNE_AT_GROUPS;      // consumer groups take alternate batches
 constexpr int kAtConsumers = TSNE_AT_WARPS;    // consumer warps
 constexpr int kAtRows = kAtConsumers / kAtGroups;   // consumer warps per group
@@ -72,7 +69,7 @@ constexpr int kAtStages = TSNE_AT_STAGES;
 constexpr int kAtMetas = 2 * kAtStages;        // batch metadata slots (outlive their stage)
 constexpr int kAtCap = TSNE_AT_CAP;            // nonzeros per stage buffer
 constexpr int kAtBudget = kAtCap - 8;          // a batch's nonzeros (the 16-byte aligned span fits)
-constexpr int kAtItem = TSNE_AT_ITEM;          // nonzeros per item
+constexpr int kAtItem = kAtItemNz;             // nonzeros per item (optimize.cuh)
 constexpr int kAtEmax = kAtItem / 32;          // 32-entry groups of an item, loaded together
 constexpr int kAtItems = 32;                   // items per batch (one per producer lane)
 constexpr int kAtChunk = 56;                   // rows per row_ptr prefetch chunk
@@ -172,30 +169,41 @@ __device__ __forceinline__ void win_accum(float2 yi, float2 yj, float p, float& 
 // entries are the point itself with p = 0).  All loads first, then the
 // arithmetic: the window / L2 gathers of the item are in flight together.
 template <int E>
-__device__ __forceinline__ void row_block(const int32_t* __restrict__ cr,
-                                          const float* __restrict__ vr, int n_rem, int self,
+__device__ __forceinline__ void row_block(uint32_t scr, uint32_t svr, int n_rem, int self,
                                           float2 yi, uint32_t sbase, const float2* __restrict__ Y,
                                           int wlo, int wn, int lane, float& ax, float& ay) {
+  // scr / svr: shared addresses of the item's columns and values
   int c[E];
   float p[E];
 #pragma unroll
   for (int u = 0; u < E; ++u) {
     const int q = lane + 32 * u;
-    if (u < E - 1) {
-      c[u] = cr[q];
-      p[u] = vr[q];
+    if (u < E - 1 || q < n_rem) {
+      asm("ld.shared.b32 %0, [%1];" : "=r"(c[u]) : "r"(scr + 4u * q));
+      asm("ld.shared.f32 %0, [%1];" : "=f"(p[u]) : "r"(svr + 4u * q));
     } else {
       c[u] = self;
       p[u] = 0.f;
-      if (q < n_rem) {
-        c[u] = cr[q];
-        p[u] = vr[q];
-      }
     }
   }
-  float2 y[E];
+  // a round whose columns all fall inside the window (the usual case once the
+  // labels are in a locality order) gathers from shared memory only
+  unsigned o[E];
+  bool in = true;
 #pragma unroll
-  for (int u = 0; u < E; ++u) y[u] = win_y(sbase, Y, c[u], wlo, wn);
+  for (int u = 0; u < E; ++u) {
+    o[u] = (unsigned)(c[u] - wlo);
+    in = in && o[u] < (unsigned)wn;
+  }
+  float2 y[E];
+  if (__all_sync(0xffffffffu, in)) {
+#pragma unroll
+    for (int u = 0; u < E; ++u)
+      asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(y[u].x), "=f"(y[u].y) : "r"(sbase + o[u] * 8u));
+  } else {
+#pragma unroll
+    for (int u = 0; u < E; ++u) y[u] = win_y(sbase, Y, c[u], wlo, wn);
+  }
 #pragma unroll
   for (int u = 0; u < E; ++u) win_accum(yi, y[u], p[u], ax, ay);
 }
@@ -517,7 +525,7 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
     }
     int wlo = row0 + (lr0 + lr1) / 2 - kAtWin / 2;
     wlo = min(wlo, Ny - kAtWin);
-    wlo = max(wlo, 0) & ~1;                      // 16-byte aligned source
+    wlo = max(wlo, 0) & ~15;                     // 16-point aligned: entry j in bank pair j mod 16
     const int wn = min(kAtWin, Ny - wlo) & ~1;   // 16-byte multiple
     if (lane == 0) {
       sh.lr0 = lr0;
@@ -616,6 +624,12 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
   // -------------------------------------------------------------- consumers
   mbar_wait_spin(&sh.win, 0);
   const int wlo = sh.wlo, wn = sh.wn;
+  // the window's shared address held in a register (otherwise rematerialised
+  // from the CTA id for every item)
+  uint32_t swin, scol0, sval0;
+  asm volatile("mov.u32 %0, %1;" : "=r"(swin) : "r"(sbase));
+  asm volatile("mov.u32 %0, %1;" : "=r"(scol0) : "r"(smem_u32(s_col)));
+  asm volatile("mov.u32 %0, %1;" : "=r"(sval0) : "r"(smem_u32(s_val)));
   const bool own_in_win = row0 + sh.lr0 >= wlo && row0 + sh.lr1 <= wlo + wn;
   const int grp = wid / kAtRows;
   for (int k = grp;; k += kAtGroups) {
@@ -627,8 +641,8 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
       if (lane == 0) mbar_arrive(&sh.done[ms]);
       break;
     }
-    const int32_t* cs = s_col + s * kAtCap;
-    const float* vs = s_val + s * kAtCap;
+    const uint32_t scs = scol0 + 4u * (uint32_t)(s * kAtCap);
+    const uint32_t svs = sval0 + 4u * (uint32_t)(s * kAtCap);
     int t = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(&m.next, 1) : 0, 0);
     while (t < ni) {
       const int2 d = m.b.item[t];
@@ -637,18 +651,17 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
       float2 yi;                                // the row's own point
       if (own_in_win) {                         // whenever the window covers the CTA's rows
         asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(yi.x), "=f"(yi.y)
-            : "r"(sbase + (unsigned)(i - wlo) * 8u));
+            : "r"(swin + (unsigned)(i - wlo) * 8u));
       } else {
-        yi = win_y(sbase, Y, i, wlo, wn);
+        yi = win_y(swin, Y, i, wlo, wn);
       }
       float ax = 0.f, ay = 0.f;
-      const int32_t* cr = cs + beg;
-      const float* vr = vs + beg;
+      const uint32_t scr = scs + 4u * (uint32_t)beg, svr = svs + 4u * (uint32_t)beg;
       switch ((len + 31) >> 5) {
 #define TSNE_RB(e)                                                                           \
   case e:                                                                                   \
     if (e <= kAtEmax)                                                                       \
-      row_block<(e <= kAtEmax ? e : 1)>(cr, vr, len, i, yi, sbase, Y, wlo, wn, lane, ax, ay); \
+      row_block<(e <= kAtEmax ? e : 1)>(scr, svr, len, i, yi, swin, Y, wlo, wn, lane, ax, ay); \
     break;
         TSNE_RB(1) TSNE_RB(2) TSNE_RB(3) TSNE_RB(4) TSNE_RB(5) TSNE_RB(6) TSNE_RB(7) TSNE_RB(8)
 #undef TSNE_RB

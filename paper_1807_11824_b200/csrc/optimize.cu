@@ -113,19 +113,64 @@ __global__ void k_perm_state(const int32_t* __restrict__ perm, int N, const floa
   len[k] = rp[o + 1] - rp[o];
 }
 
-__global__ void k_relabel_rows(const int32_t* __restrict__ perm, int N,
-                               const int64_t* __restrict__ rp_old, const int32_t* __restrict__ col_old,
-                               const float* __restrict__ val_old, const int32_t* __restrict__ inv,
-                               const int64_t* __restrict__ rp_new, int32_t* __restrict__ col_new,
-                               float* __restrict__ val_new) {
-  const int lane = threadIdx.x & 31;
+// Row k of the relabelled CSR = row perm[k] of the old one, columns mapped by
+// inv.  Within each attractive-pass item (kAtItem consecutive nonzeros from
+// the row's start) the entries are put in bank order for the pass's window
+// gathers: the window holds y_j at 8 bytes from a 16-point-aligned start, so
+// entry j sits in bank pair (j mod 16); ranking each entry among the earlier
+// entries of its bank pair (r) and ordering the item by (r, bank pair) puts 16
+// different bank pairs in every half-warp of a gather round wherever the item
+// allows (a random order: ~3-way conflicts).  The order is fixed by the CSR,
+// so the row sums stay deterministic.  One warp per row.
+__global__ void __launch_bounds__(256)
+k_relabel_rows(const int32_t* __restrict__ perm, int N, const int64_t* __restrict__ rp_old,
+               const int32_t* __restrict__ col_old, const float* __restrict__ val_old,
+               const int32_t* __restrict__ inv, const int64_t* __restrict__ rp_new,
+               int32_t* __restrict__ col_new, float* __restrict__ val_new) {
+  constexpr int kU = kAtItemNz / 32;
+  __shared__ int s_cnt[8][16];
+  const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 7;
   const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (k >= N) return;
   const int o = perm ? perm[k] : k;
   const int64_t e0 = rp_old[o], e1 = rp_old[o + 1], d0 = rp_new[k];
-  for (int64_t e = e0 + lane; e < e1; e += 32) {
-    col_new[d0 + (e - e0)] = inv[__ldcs(col_old + e)];
-    val_new[d0 + (e - e0)] = __ldcs(val_old + e);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t q0 = 0; q0 < e1 - e0; q0 += kAtItemNz) {
+    const int n = (int)min((int64_t)kAtItemNz, e1 - e0 - q0);
+    if (lane < 16) s_cnt[w][lane] = 0;
+    __syncwarp();
+    int c[kU], r[kU];
+    float v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int q = lane + 32 * u;
+      const bool ok = q < n;
+      c[u] = ok ? inv[__ldcs(col_old + e0 + q0 + q)] : 0;
+      v[u] = ok ? __ldcs(val_old + e0 + q0 + q) : 0.f;
+      const int b = ok ? (c[u] & 15) : 16 + lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      int base = ok ? s_cnt[w][b] : 0;
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) s_cnt[w][b] = base + __popc(peers);
+      __syncwarp();
+      r[u] = base + __popc(peers & lt);
+    }
+    int nb[16];
+#pragma unroll
+    for (int b = 0; b < 16; ++b) nb[b] = s_cnt[w][b];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int q = lane + 32 * u;
+      if (q < n) {
+        const int b = c[u] & 15, rr = r[u];
+        int pos = 0;
+#pragma unroll
+        for (int b2 = 0; b2 < 16; ++b2) pos += min(nb[b2], rr) + ((b2 < b && nb[b2] > rr) ? 1 : 0);
+        col_new[d0 + q0 + pos] = c[u];
+        val_new[d0 + q0 + pos] = v[u];
+      }
+    }
+    __syncwarp();
   }
 }
 

@@ -4,6 +4,14 @@
 
 namespace tsne {
 
+// attractive-pass item: consecutive nonzeros of a row, counted from the row's
+// start, reduced by one warp (attract.cu); the relabelled CSR orders the
+// entries of each item for the pass's window gathers (optimize.cu)
+#ifndef TSNE_AT_ITEM
+#define TSNE_AT_ITEM 256
+#endif
+constexpr int kAtItemNz = TSNE_AT_ITEM;
+
 // schedule and optimiser constants (D12-D16; the paper states none)
 struct Sched {
   int32_t exag_iters;
