@@ -225,23 +225,57 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   asm volatile("mov.u32 %0, %1;" : "=r"(lv_base) : "r"((uint32_t)__cvta_generic_to_shared(s_lv)));
   const float4* nodes_r;
   asm volatile("mov.b64 %0, %1;" : "=l"(nodes_r) : "l"(nodes));
-  while (cur < nnodes) {
-    if (stats) ++n_visit;
-    const float4 nd = __ldg(nodes_r + (unsigned)cur);
-    const uint32_t sw = __float_as_uint(nd.w);
-    const uint32_t lvl = sw >> 27;
-    const int skip = (int)(sw & kSkipMask);
+  // The walk in warp lockstep: a fast loop over the visits the fp32 test
+  // settles (outside the D25 band) that are not an unaccepted bucket --
+  // straight-line code, warp-uniform exits (votes), so no reconvergence
+  // per visit -- and, when any lane meets another kind of visit, one round of
+  // the general code in which every lane still walking finishes its current
+  // visit.  A lane that is done parks on the sentinel node at index nnodes
+  // (a one-point leaf of count 0 whose skip is itself, k_quad_emit): it takes
+  // nothing and stays there, so the fast loop needs no per-lane predicate.
+  while (__any_sync(0xffffffffu, cur < nnodes)) {
+    float4 nd;
+    uint32_t lvl;
+    int skip;
     float2 lv;
-    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(lv.x), "=f"(lv.y) : "r"(lv_base + 8u * lvl));
-    float dx = yi.x - nd.x, dy = yi.y - nd.y;
-    float D2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-    const bool self_in = (unsigned)(Li - cur) < (unsigned)(skip - cur);   // Li in [cur, skip)
-    // criterion (D10) in fp32 with the D25 margin
-    const float diff = D2 - lv.x;
+    float dx, dy, D2, diff;
+    bool self_in;
+    for (;;) {
+      if (stats && cur < nnodes) ++n_visit;
+      nd = __ldg(nodes_r + (unsigned)cur);
+      const uint32_t sw = __float_as_uint(nd.w);
+      lvl = sw >> 27;
+      skip = (int)(sw & kSkipMask);
+      asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(lv.x), "=f"(lv.y) : "r"(lv_base + 8u * lvl));
+      dx = yi.x - nd.x;
+      dy = yi.y - nd.y;
+      D2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+      self_in = (unsigned)(Li - cur) < (unsigned)(skip - cur);   // Li in [cur, skip)
+      // criterion (D10) in fp32 with the D25 margin
+      diff = D2 - lv.x;
+      const bool acc = diff > lv.y;
+      // (bitwise, not short-circuit: no branch region per visit)
+      const int rare = (int)!self_in &
+                       ((int)(fabsf(diff) <= lv.y) | ((int)(lvl > (uint32_t)kLevelLeaf) & (int)!acc));
+      if (__any_sync(0xffffffffu, rare)) break;
+      // accept a cell / take a one-point leaf, unless it contains i (D11)
+      const bool take = (int)acc & (int)!self_in;
+      cur = ((int)take | (int)(lvl >= (uint32_t)kLevelLeaf)) ? skip : cur + 1;
+      const float w = rcp_approx(1.f + D2);
+      const float nw = take ? nd.z * w : 0.f;
+      if (stats && take && nd.z > 0.f) ++n_take;
+      zf += nw;
+      const float nww = nw * w;
+      fx = fmaf(nww, dx, fx);
+      fy = fmaf(nww, dy, fy);
+      if (!__any_sync(0xffffffffu, cur < nnodes)) break;
+    }
+    if (cur >= nnodes) continue;
+    // this lane's current visit by the general code: inside the fp32 band, or
+    // a deep cell (its size approaches the fp32 spacing of the coordinates):
+    // the decision and the offset in fp64 (D25); and/or a bucket
     bool acc = diff > lv.y;
     if (fabsf(diff) <= lv.y && !self_in) {
-      // inside the fp32 band, or a deep cell (its size approaches the fp32
-      // spacing of the coordinates): the decision and the offset in fp64 (D25)
       const double2 c = com64[(unsigned)cur];
       const double ex = __dsub_rn((double)yi.x, c.x), ey = __dsub_rn((double)yi.y, c.y);
       const double D2d = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
@@ -251,7 +285,6 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
       D2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
       if (stats) ++n_f64;
     }
-    // accept a cell / take a one-point leaf, unless it contains i (D11)
     const bool take = acc && !self_in;
     const int node = cur;
     cur = (take || lvl >= (uint32_t)kLevelLeaf) ? skip : cur + 1;

@@ -538,6 +538,12 @@ k_quad_emit(int N, const uint8_t* __restrict__ dl, const int4* __restrict__ nfo,
             int32_t* __restrict__ nfirst, double2* __restrict__ com64,
             int32_t* __restrict__ leafnode, int32_t* __restrict__ has_bucket) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k == 0) {
+    // sentinel after the last node (the traversal parks finished lanes there):
+    // a one-point leaf of count 0 whose skip is itself
+    const int nn = base[N];
+    nodes[nn] = make_float4(0.f, 0.f, 0.f, __uint_as_float((uint32_t)nn | ((uint32_t)kLevelLeaf << 27)));
+  }
   if (k >= N) return;
   const int dprev = k > 0 ? dl[k - 1] : -1;
   const int dnext = k < N - 1 ? dl[k] : -1;
