@@ -24,7 +24,7 @@ namespace tsne {
 
 constexpr int kTravThreads = 256;
 #ifndef TSNE_TRAV_MINB
-#define TSNE_TRAV_MINB 5   // 48 registers, no spills: 40 warps per SM
+#define TSNE_TRAV_MINB 6   // 40 registers, no spills: 48 warps per SM (the lockstep walk; 5: 0.362 vs 0.343 ms at C5)
 #endif
 
 // diagnostics (traverse_stats): [0] sum of node visits, [1] sum over warps
