@@ -156,6 +156,26 @@ __device__ __forceinline__ void warp_sum2(float& a, float& b) {
   b = vb;
 }
 
+// (a, b, c, d) summed over the warp with 6 shuffles: the first step exchanges
+// (c, d) against (a, b) between the half-warps, the second splits each half
+// between its two values, then three steps reduce one value per 8 lanes.
+// Fixed order (deterministic); lane 0 / 8 / 16 / 24 end with the a / b / c / d sum.
+__device__ __forceinline__ float warp_sum4(float a, float b, float c, float d) {
+  const unsigned lane = threadIdx.x & 31u;
+  const bool hi = lane >= 16u;
+  const float s1 = hi ? a : c, s2 = hi ? b : d;
+  const float r1 = __shfl_xor_sync(0xffffffffu, s1, 16);
+  const float r2 = __shfl_xor_sync(0xffffffffu, s2, 16);
+  float x = hi ? c + r1 : a + r1;             // lanes < 16: a, b;  lanes >= 16: c, d
+  float y = hi ? d + r2 : b + r2;
+  const bool q = (lane & 8u) != 0u;
+  const float r3 = __shfl_xor_sync(0xffffffffu, q ? x : y, 8);
+  float v = q ? y + r3 : x + r3;              // lane bit 3 clear: x (a or c), set: y (b or d)
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __device__ __forceinline__ void win_accum(float2 yi, float2 yj, float p, float& ax, float& ay) {
   const float dx = yi.x - yj.x, dy = yi.y - yj.y;
   const float w = rcp_approx_f(fmaf(dy, dy, fmaf(dx, dx, 1.f)));   // 1/(1+d^2), d^2 >= 0
@@ -643,8 +663,8 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
     }
     const uint32_t scs = scol0 + 4u * (uint32_t)(s * kAtCap);
     const uint32_t svs = sval0 + 4u * (uint32_t)(s * kAtCap);
-    int t = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(&m.next, 1) : 0, 0);
-    while (t < ni) {
+    // one item's sum over the warp's lanes (before the reduction)
+    auto item_sum = [&](int t, float& ax, float& ay) {
       const int2 d = m.b.item[t];
       const int l = d.x, i = row0 + l;
       const int beg = d.y & 0x1fff, len = (d.y >> 13) & 0x1ff;
@@ -655,7 +675,6 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
       } else {
         yi = win_y(swin, Y, i, wlo, wn);
       }
-      float ax = 0.f, ay = 0.f;
       const uint32_t scr = scs + 4u * (uint32_t)beg, svr = svs + 4u * (uint32_t)beg;
       switch ((len + 31) >> 5) {
 #define TSNE_RB(e)                                                                           \
@@ -667,12 +686,20 @@ k_attract_tma(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ c
 #undef TSNE_RB
         default: break;
       }
-      warp_sum2(ax, ay);
+    };
+    // items are claimed in pairs (t even): both are summed, then reduced
+    // together in one fixed butterfly (a lone last item pairs with zeros)
+    int t = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(&m.next, 2) : 0, 0);
+    while (t < ni) {
+      float a0 = 0.f, b0 = 0.f, a1 = 0.f, b1 = 0.f;
+      item_sum(t, a0, b0);
+      const bool two = t + 1 < ni;
+      if (two) item_sum(t + 1, a1, b1);
+      const float r = warp_sum4(a0, b0, a1, b1);   // lanes 0 / 8 / 16 / 24: a0 / b0 / a1 / b1
+      if ((lane & 7) == 0 && (two || lane < 16))
+        reinterpret_cast<float*>(&m.part[t])[lane >> 3] = r;
       int tn = 0;
-      if (lane == 0) {
-        m.part[t] = make_float2(ax, ay);
-        tn = atomicAdd(&m.next, 1);
-      }
+      if (lane == 0) tn = atomicAdd(&m.next, 2);
       t = __shfl_sync(0xffffffffu, tn, 0);
     }
     __syncwarp();
