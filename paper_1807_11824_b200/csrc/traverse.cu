@@ -127,6 +127,7 @@ k_bucket_pairs(const float4* __restrict__ nodes, const int32_t* __restrict__ nfi
 }
 
 constexpr int kPend = 4;   // deferred buckets per lane
+constexpr int kMinLockstep = 4;   // a shorter lockstep run sends the warp to the per-lane walk
 constexpr int kDeepFp32 = 16;   // deeper cells: fp64 criterion and offsets
 
 
@@ -225,21 +226,68 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   asm volatile("mov.u32 %0, %1;" : "=r"(lv_base) : "r"((uint32_t)__cvta_generic_to_shared(s_lv)));
   const float4* nodes_r;
   asm volatile("mov.b64 %0, %1;" : "=l"(nodes_r) : "l"(nodes));
-  // The walk in warp lockstep: a fast loop over the visits the fp32 test
-  // settles (outside the D25 band) that are not an unaccepted bucket --
-  // straight-line code, warp-uniform exits (votes), so no reconvergence
-  // per visit -- and, when any lane meets another kind of visit, one round of
-  // the general code in which every lane still walking finishes its current
-  // visit.  A lane that is done parks on the sentinel node at index nnodes
-  // (a one-point leaf of count 0 whose skip is itself, k_quad_emit): it takes
+  // The general treatment of one visit (node cur, fp32 quantities computed):
+  // inside the fp32 band, or a deep cell (its size approaches the fp32 spacing
+  // of the coordinates), the decision and the offset in fp64 (D25); accept a
+  // cell / take a one-point leaf unless it contains i (D11); a bucket that is
+  // not accepted is evaluated pairwise (own bucket: k_bucket_pairs).
+  auto visit = [&](const float4& nd, uint32_t lvl, int skip, float2 lv, float dx, float dy,
+                   float D2, float diff, bool self_in) {
+    bool acc = diff > lv.y;
+    if (fabsf(diff) <= lv.y && !self_in) {
+      const double2 c = com64[(unsigned)cur];
+      const double ex = __dsub_rn((double)yi.x, c.x), ey = __dsub_rn((double)yi.y, c.y);
+      const double D2d = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
+      acc = s_r2d[lvl] < __dmul_rn(theta2d, D2d);
+      dx = (float)ex;
+      dy = (float)ey;
+      D2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+      if (stats) ++n_f64;
+    }
+    const bool take = acc && !self_in;
+    const int node = cur;
+    cur = (take || lvl >= (uint32_t)kLevelLeaf) ? skip : cur + 1;
+    const float w = rcp_approx(1.f + D2);
+    const float nw = take ? nd.z * w : 0.f;
+    if (stats && take && nd.z > 0.f) ++n_take;
+    zf += nw;
+    const float nww = nw * w;
+    fx = fmaf(nww, dx, fx);
+    fy = fmaf(nww, dy, fy);
+    if (!take && !self_in && lvl > (uint32_t)kLevelLeaf) {
+      const int s0 = nfirst[node];
+      const int cnt = (int)nd.z;
+      if (stats) n_pair += (unsigned)cnt;
+      if (npend < kPend) {      // deferred: processed warp-synchronously after the walk
+#pragma unroll
+        for (int q = 0; q < kPend; ++q)
+          if (q == npend) { pq_s[q] = s0; pq_c[q] = cnt; }
+        ++npend;
+      } else {
+        bucket_pairs(ys, s0, cnt, k, yi, true, fx, fy, z);
+      }
+    }
+  };
+  // The walk, first in warp lockstep: a fast loop over the visits the fp32
+  // test settles (outside the D25 band) that are not an unaccepted bucket --
+  // straight-line code, warp-uniform exits (votes), so no reconvergence per
+  // visit -- and, when any lane meets another kind of visit, one round of the
+  // general code in which every lane still walking finishes its current
+  // visit.  A lane that is done parks on the sentinel node at index nnodes (a
+  // one-point leaf of count 0 whose skip is itself, k_quad_emit): it takes
   // nothing and stays there, so the fast loop needs no per-lane predicate.
-  while (__any_sync(0xffffffffu, cur < nnodes)) {
+  // Where such visits are frequent (deep clusters, buckets: C2/C3 early in the
+  // run) a lockstep run ends within a few visits; the warp then walks on per
+  // lane.
+  bool lockstep = true;
+  while (lockstep && __any_sync(0xffffffffu, cur < nnodes)) {
     float4 nd;
     uint32_t lvl;
     int skip;
     float2 lv;
     float dx, dy, D2, diff;
     bool self_in;
+    int nfast = 0;
     for (;;) {
       if (stats && cur < nnodes) ++n_visit;
       nd = __ldg(nodes_r + (unsigned)cur);
@@ -258,7 +306,6 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
       const int rare = (int)!self_in &
                        ((int)(fabsf(diff) <= lv.y) | ((int)(lvl > (uint32_t)kLevelLeaf) & (int)!acc));
       if (__any_sync(0xffffffffu, rare)) break;
-      // accept a cell / take a one-point leaf, unless it contains i (D11)
       const bool take = (int)acc & (int)!self_in;
       cur = ((int)take | (int)(lvl >= (uint32_t)kLevelLeaf)) ? skip : cur + 1;
       const float w = rcp_approx(1.f + D2);
@@ -268,47 +315,24 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
       const float nww = nw * w;
       fx = fmaf(nww, dx, fx);
       fy = fmaf(nww, dy, fy);
+      ++nfast;
       if (!__any_sync(0xffffffffu, cur < nnodes)) break;
     }
-    if (cur >= nnodes) continue;
-    // this lane's current visit by the general code: inside the fp32 band, or
-    // a deep cell (its size approaches the fp32 spacing of the coordinates):
-    // the decision and the offset in fp64 (D25); and/or a bucket
-    bool acc = diff > lv.y;
-    if (fabsf(diff) <= lv.y && !self_in) {
-      const double2 c = com64[(unsigned)cur];
-      const double ex = __dsub_rn((double)yi.x, c.x), ey = __dsub_rn((double)yi.y, c.y);
-      const double D2d = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
-      acc = s_r2d[lvl] < __dmul_rn(theta2d, D2d);
-      dx = (float)ex;
-      dy = (float)ey;
-      D2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-      if (stats) ++n_f64;
-    }
-    const bool take = acc && !self_in;
-    const int node = cur;
-    cur = (take || lvl >= (uint32_t)kLevelLeaf) ? skip : cur + 1;
-    const float w = rcp_approx(1.f + D2);
-    const float nw = take ? nd.z * w : 0.f;
-    if (stats && take) ++n_take;
-    zf += nw;
-    const float nww = nw * w;
-    fx = fmaf(nww, dx, fx);
-    fy = fmaf(nww, dy, fy);
-    if (!take && !self_in && lvl > (uint32_t)kLevelLeaf) {
-      // another bucket, not accepted: exact pairs (own bucket: k_bucket_pairs)
-      const int s0 = nfirst[node];
-      const int cnt = (int)nd.z;
-      if (stats) n_pair += (unsigned)cnt;
-      if (npend < kPend) {      // deferred: processed warp-synchronously after the walk
-#pragma unroll
-        for (int q = 0; q < kPend; ++q)
-          if (q == npend) { pq_s[q] = s0; pq_c[q] = cnt; }
-        ++npend;
-      } else {
-        bucket_pairs(ys, s0, cnt, k, yi, true, fx, fy, z);
-      }
-    }
+    if (cur < nnodes) visit(nd, lvl, skip, lv, dx, dy, D2, diff, self_in);
+    lockstep = nfast >= kMinLockstep;                  // warp-uniform
+  }
+  while (cur < nnodes) {
+    if (stats) ++n_visit;
+    const float4 nd = __ldg(nodes_r + (unsigned)cur);
+    const uint32_t sw = __float_as_uint(nd.w);
+    const uint32_t lvl = sw >> 27;
+    const int skip = (int)(sw & kSkipMask);
+    float2 lv;
+    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(lv.x), "=f"(lv.y) : "r"(lv_base + 8u * lvl));
+    const float dx = yi.x - nd.x, dy = yi.y - nd.y;
+    const float D2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+    const bool self_in = (unsigned)(Li - cur) < (unsigned)(skip - cur);
+    visit(nd, lvl, skip, lv, dx, dy, D2, D2 - lv.x, self_in);
   }
   z += (double)zf;
   // Deferred buckets: lanes of the warp that share a bucket walk its members
