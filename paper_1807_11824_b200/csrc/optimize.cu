@@ -142,11 +142,19 @@ k_relabel_rows(const int32_t* __restrict__ perm, int N, const int64_t* __restric
     int c[kU], r[kU];
     float v[kU];
 #pragma unroll
+    for (int u = 0; u < kU; ++u) {                   // all loads in flight first
+      const int q = lane + 32 * u;
+      const bool ok = q < n;
+      c[u] = ok ? __ldcs(col_old + e0 + q0 + q) : 0;
+      v[u] = ok ? __ldcs(val_old + e0 + q0 + q) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (lane + 32 * u < n) c[u] = inv[c[u]];
+#pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int q = lane + 32 * u;
       const bool ok = q < n;
-      c[u] = ok ? inv[__ldcs(col_old + e0 + q0 + q)] : 0;
-      v[u] = ok ? __ldcs(val_old + e0 + q0 + q) : 0.f;
       const int b = ok ? (c[u] & 15) : 16 + lane;
       const unsigned peers = __match_any_sync(0xffffffffu, b);
       int base = ok ? s_cnt[w][b] : 0;
@@ -155,17 +163,41 @@ k_relabel_rows(const int32_t* __restrict__ perm, int N, const int64_t* __restric
       __syncwarp();
       r[u] = base + __popc(peers & lt);
     }
-    int nb[16];
+    // rank level r holds the bank pairs with more than r entries, M[r]; an entry
+    // of rank r in bank pair b lands at (entries of lower levels) + (banks
+    // below b in level r): Lp[r] + popc(M[r] & ((1 << b) - 1)).  Lane r holds
+    // level r < 32 (a bank pair with more than 32 entries of one item is rare:
+    // those levels are counted directly).
+    uint32_t M = 0;
 #pragma unroll
-    for (int b = 0; b < 16; ++b) nb[b] = s_cnt[w][b];
+    for (int b = 0; b < 16; ++b) M |= (s_cnt[w][b] > lane ? 1u : 0u) << b;
+    const int L = __popc(M);
+    int Lp = L;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, Lp, o);
+      if (lane >= o) Lp += t;
+    }
+    Lp -= L;
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int q = lane + 32 * u;
+      const int rr = r[u];
+      const int src = rr < 32 ? rr : 31;
+      const int lp = __shfl_sync(0xffffffffu, Lp, src);
+      const uint32_t m = __shfl_sync(0xffffffffu, M, src);
       if (q < n) {
-        const int b = c[u] & 15, rr = r[u];
-        int pos = 0;
-#pragma unroll
-        for (int b2 = 0; b2 < 16; ++b2) pos += min(nb[b2], rr) + ((b2 < b && nb[b2] > rr) ? 1 : 0);
+        const int b = c[u] & 15;
+        int pos;
+        if (rr < 32) {
+          pos = lp + __popc(m & ((1u << b) - 1u));
+        } else {
+          pos = 0;
+          for (int b2 = 0; b2 < 16; ++b2) {
+            const int nb2 = s_cnt[w][b2];
+            pos += min(nb2, rr) + ((b2 < b && nb2 > rr) ? 1 : 0);
+          }
+        }
         col_new[d0 + q0 + pos] = c[u];
         val_new[d0 + q0 + pos] = v[u];
       }
