@@ -133,10 +133,30 @@ constexpr int kDeepFp32 = 16;   // deeper cells: fp64 criterion and offsets
 
 // exact pairs of point k (y_i) with the members [s0, s0 + cnt) of a bucket;
 // lanes with take == false run the loop (warp-uniform trip count) adding 0
+// (members in groups of 4: their loads in flight together, z summed in fp32
+// per group and added to the fp64 z once per group, as k_bucket_pairs)
 __device__ __forceinline__ void bucket_pairs(const float2* __restrict__ ys, int s0, int cnt, int k,
                                              float2 yi, bool take, float& fx, float& fy,
                                              double& z) {
-  for (int m = s0; m < s0 + cnt; ++m) {
+  int m = s0;
+  const int me = s0 + cnt;
+  for (; m + 4 <= me; m += 4) {
+    float2 yj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) yj[u] = ys[m + u];
+    float zs = 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float ex = yi.x - yj[u].x, ey = yi.y - yj[u].y;
+      const float wj = (take && m + u != k) ? rcp_approx(1.f + ex * ex + ey * ey) : 0.f;
+      zs += wj;
+      const float ww = wj * wj;
+      fx = fmaf(ww, ex, fx);
+      fy = fmaf(ww, ey, fy);
+    }
+    z += (double)zs;
+  }
+  for (; m < me; ++m) {
     const float2 yj = ys[m];
     const float ex = yi.x - yj.x, ey = yi.y - yj.y;
     const float wj = (take && m != k) ? rcp_approx(1.f + ex * ex + ey * ey) : 0.f;
