@@ -126,7 +126,8 @@ k_bucket_pairs(const float4* __restrict__ nodes, const int32_t* __restrict__ nfi
   }
 }
 
-constexpr int kPend = 4;   // deferred buckets per lane
+constexpr int kPend = 4;   // deferred buckets per lane (registers)
+constexpr int kOvf = 12;   // and beyond, in the lane's overflow list (global memory)
 constexpr int kMinLockstep = 4;   // a shorter lockstep run sends the warp to the per-lane walk
 constexpr int kDeepFp32 = 16;   // deeper cells: fp64 criterion and offsets
 
@@ -176,7 +177,8 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            float theta, float2* __restrict__ rep, double* __restrict__ zpart,
            unsigned* __restrict__ counter, double* __restrict__ Zout,
            const int32_t* __restrict__ list, const int32_t* __restrict__ nlist, int row0,
-           const BucketSum* __restrict__ bsum, const int32_t* __restrict__ has_bucket) {
+           const BucketSum* __restrict__ bsum, const int32_t* __restrict__ has_bucket,
+           int2* __restrict__ ovf) {
   constexpr bool stats = STATS;
   // list (multi-GPU): the sorted positions of the points this rank owns
   // (original indices [row0, ...)); rep is then indexed by perm[k] - row0.
@@ -238,7 +240,9 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   int pq_s[kPend], pq_c[kPend];   // deferred buckets of this lane
 #pragma unroll
   for (int q = 0; q < kPend; ++q) { pq_s[q] = -1; pq_c[q] = 0; }
-  int npend = 0;
+  int npend = 0, novf = 0;
+  const int nthr = gridDim.x * kTravThreads;
+  const int gtid = blockIdx.x * kTravThreads + threadIdx.x;
   unsigned n_visit = 0, n_take = 0, n_f64 = 0, n_pair = 0;
   // loop-invariant addresses held in registers (the compiler would otherwise
   // rematerialise them on every visit)
@@ -283,6 +287,9 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
         for (int q = 0; q < kPend; ++q)
           if (q == npend) { pq_s[q] = s0; pq_c[q] = cnt; }
         ++npend;
+      } else if (novf < kOvf) { // (collapsed clusters: many neighbouring buckets)
+        ovf[(size_t)novf * nthr + gtid] = make_int2(s0, cnt);
+        ++novf;
       } else {
         bucket_pairs(ys, s0, cnt, k, yi, true, fx, fy, z);
       }
@@ -387,6 +394,26 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
       npend = ns;
     }
   }
+  // the overflow lists, the same way (each lane's buckets are in one list or
+  // the other, so each is walked once for it)
+  while (true) {
+    __syncwarp();
+    const unsigned ball = __ballot_sync(0xffffffffu, novf > 0);
+    if (!ball) break;
+    const int2 e = ovf[gtid - (threadIdx.x & 31) + __ffs(ball) - 1];   // its first entry
+    bool mine = false;
+    for (int q = 0; q < novf; ++q) mine |= ovf[(size_t)q * nthr + gtid].x == e.x;
+    bucket_pairs(ys, e.x, e.y, k, yi, mine, fx, fy, z);
+    __syncwarp();
+    if (mine) {
+      int ns = 0;
+      for (int q = 0; q < novf; ++q) {
+        const int2 v = ovf[(size_t)q * nthr + gtid];
+        if (v.x != e.x) ovf[(size_t)(ns++) * nthr + gtid] = v;
+      }
+      novf = ns;
+    }
+  }
   if (active) {
     if (*has_bucket) {
       const BucketSum b = bsum[k];
@@ -467,7 +494,7 @@ tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s) {
   k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
       w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0,
-      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket);
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }
@@ -486,7 +513,7 @@ tsne_status traverse_stats(TreeWS& w, float theta, double* out, cudaStream_t s) 
   k_traverse<true><<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
       w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0,
-      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket);
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf);
   TSNE_LAUNCH_CHECK();
   unsigned long long h[5];
   TSNE_CUDA_TRY(cudaMemcpyFromSymbolAsync(h, g_trav_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, s));
@@ -504,7 +531,7 @@ tsne_status launch_traverse_list(TreeWS& w, float theta, const int32_t* list, co
   k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta,
       rep_local, w.zpart, w.counter + 1, z_partial, list, nlist, row0,
-      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket);
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf);
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }

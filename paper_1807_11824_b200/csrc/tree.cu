@@ -73,6 +73,7 @@ void carve_tree(Carver& c, TreeWS& w, int64_t N) {
   w.has_bucket = c.take<int32_t>(1);
   w.rep = c.take<float2>(N);
   w.zpart = c.take<double>(traverse_blocks(N));
+  w.ovf = c.take<int2>((size_t)traverse_blocks(N) * 256 * 12);   // traversal bucket overflow
   w.Z = c.take<double>(2);
   w.counter = c.take<unsigned>(8);
   w.part4 = c.take<float4>(kMaxParts);

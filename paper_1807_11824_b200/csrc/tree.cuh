@@ -70,6 +70,7 @@ struct TreeWS {
   BoxInfo* box = nullptr;
   float2* rep = nullptr;       // N repulsive numerators f_i (original order)
   double* zpart = nullptr;     // per traversal block
+  int2* ovf = nullptr;         // per traversal thread: deferred buckets beyond the registers
   double* Z = nullptr;         // [0] = Z, [1] = 1/Z
   unsigned* counter = nullptr; // last-block-done counters (zeroed once)
   float4* part4 = nullptr;     // per-block min/max partials (kMaxParts)

@@ -136,6 +136,22 @@ def fixed_y(kind: str, N: int, seed: int = 7, labels=None) -> np.ndarray:
         lab = torch.randint(0, C, (N,), generator=g)
         mu = 50.0 * torch.randn(C, 2, generator=g)
         Y = mu[lab] + 0.5 * torch.randn(N, 2, generator=g)
+    elif kind.startswith("collapsed"):
+        # a transient collapse of the exaggeration phase: the blobs of 'blobs'
+        # plus N // 9 points packed into a 6 x 6 patch of adjacent finest
+        # (level-24) cells near the origin, so the tree holds 36 neighbouring
+        # buckets of ~N/324 points each (exact pairs with every bucket a point
+        # cannot accept)
+        C = max(1, N // 100)
+        lab = torch.randint(0, C, (N,), generator=g)
+        mu = 50.0 * torch.randn(C, 2, generator=g)
+        Y = (mu[lab] + 0.5 * torch.randn(N, 2, generator=g)).to(torch.float64)
+        M = N // 9
+        span = float((Y.max(0).values - Y.min(0).values).max())
+        h = span * (1 + 2.0 ** -20) / 2.0 ** 24          # finest cell side (D9)
+        cell = torch.randint(0, 6, (M, 2), generator=g).to(torch.float64)
+        off = 0.25 + 0.5 * torch.rand(M, 2, generator=g, dtype=torch.float64)
+        Y[:M] = 0.5 + (cell + off) * h
     else:
         raise ValueError(kind)
     return Y.to(torch.float32).numpy()

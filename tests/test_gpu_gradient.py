@@ -239,3 +239,17 @@ def test_sort_bucket_overflow(T, orc, N):
     go, Zo = orc.gradient_bh(rp, col, v32, Y, 0.5, 4.0)
     assert abs(Z - Zo) <= 1e-6 * Zo
     assert rel(g, go) <= 1e-4
+
+
+def test_collapsed_cluster_buckets(T, orc):
+    # a collapsed cluster over 36 adjacent finest cells (synth 'collapsed'):
+    # each point takes exact pairs with the neighbouring buckets it cannot
+    # accept -- more than the traversal's per-lane deferral list holds
+    N = 20000
+    Y = synth.fixed_y("collapsed", N, seed=21)
+    rp, col, v32, _ = synth.random_csr(N, 8, seed=12)
+    for theta in (0.5, 0.8):
+        g, Z = gpu_grad(T, rp, col, v32, Y, theta, 12.0)
+        go, Zo = orc.gradient_bh(rp, col, v32, Y, theta, 12.0)
+        assert abs(Z - Zo) <= 1e-6 * Zo
+        assert rel(g, go) <= 1e-4
