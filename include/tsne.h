@@ -44,7 +44,7 @@ typedef enum {
   TSNE_ERR_CUDA = 2,       /* CUDA runtime / launch failure, or no device   */
   TSNE_ERR_WORKSPACE = 3,  /* ws == NULL or ws_bytes < required size        */
   TSNE_ERR_NONFINITE = 4,  /* NaN/Inf appeared in Y during optimisation     */
-  TSNE_ERR_NCCL = 5,       /* reserved for the collective path              */
+  TSNE_ERR_NCCL = 5,       /* a failed NCCL communicator or collective (tsne_run_sharded) */
   TSNE_ERR_DEGENERATE = 6  /* non-fatal: some rows had no finite beta (D3)  */
 } tsne_status;
 
