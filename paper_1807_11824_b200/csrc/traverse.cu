@@ -128,6 +128,8 @@ k_bucket_pairs(const float4* __restrict__ nodes, const int32_t* __restrict__ nfi
 
 constexpr int kPend = 4;   // deferred buckets per lane (registers)
 constexpr int kOvf = 12;   // and beyond, in the lane's overflow list (global memory)
+constexpr int kLargeBucket = 64;   // deferred buckets this large go to k_defer_large
+constexpr int kLg = 16;            // per traversal thread
 constexpr int kMinLockstep = 4;   // a shorter lockstep run sends the warp to the per-lane walk
 constexpr int kDeepFp32 = 16;   // deeper cells: fp64 criterion and offsets
 
@@ -178,7 +180,8 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            unsigned* __restrict__ counter, double* __restrict__ Zout,
            const int32_t* __restrict__ list, const int32_t* __restrict__ nlist, int row0,
            const BucketSum* __restrict__ bsum, const int32_t* __restrict__ has_bucket,
-           int2* __restrict__ ovf) {
+           int2* __restrict__ ovf, int2* __restrict__ lg, int2* __restrict__ dlist,
+           unsigned* __restrict__ dcount) {
   constexpr bool stats = STATS;
   // list (multi-GPU): the sorted positions of the points this rank owns
   // (original indices [row0, ...)); rep is then indexed by perm[k] - row0.
@@ -240,7 +243,7 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   int pq_s[kPend], pq_c[kPend];   // deferred buckets of this lane
 #pragma unroll
   for (int q = 0; q < kPend; ++q) { pq_s[q] = -1; pq_c[q] = 0; }
-  int npend = 0, novf = 0;
+  int npend = 0, novf = 0, nlg = 0;
   const int nthr = gridDim.x * kTravThreads;
   const int gtid = blockIdx.x * kTravThreads + threadIdx.x;
   unsigned n_visit = 0, n_take = 0, n_f64 = 0, n_pair = 0;
@@ -282,7 +285,12 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
       const int s0 = nfirst[node];
       const int cnt = (int)nd.z;
       if (stats) n_pair += (unsigned)cnt;
-      if (npend < kPend) {      // deferred: processed warp-synchronously after the walk
+      if (cnt >= kLargeBucket && nlg < kLg) {
+        // a large bucket (a collapsed cluster): walked by k_defer_large, a warp
+        // per point, so the few warps that hold them do not serialise the pass
+        lg[(size_t)nlg * nthr + gtid] = make_int2(s0, cnt);
+        ++nlg;
+      } else if (npend < kPend) {      // deferred: processed warp-synchronously after the walk
 #pragma unroll
         for (int q = 0; q < kPend; ++q)
           if (q == npend) { pq_s[q] = s0; pq_c[q] = cnt; }
@@ -414,6 +422,7 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
       novf = ns;
     }
   }
+  if (nlg > 0) dlist[atomicAdd(dcount, 1u)] = make_int2(gtid, nlg);
   if (active) {
     if (*has_bucket) {
       const BucketSum b = bsum[k];
@@ -475,6 +484,89 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
   }
 }
 
+// The large deferred buckets of the traversal threads in the list (k_traverse
+// appends them): one warp per thread, its buckets in list order, lanes over the
+// members; each bucket's sums are reduced by a fixed butterfly and added in
+// order, then added to the point's repulsive numerator.  The z terms enter Z
+// through an exact fixed-point sum (2^-24 units: integers, so the order of the
+// warps does not matter), folded into Z and 1/Z by the last CTA, which also
+// resets the list.
+constexpr int kDeferThreads = 128;
+__global__ void __launch_bounds__(kDeferThreads)
+k_defer_large(const float2* __restrict__ ys, const int32_t* __restrict__ perm,
+              const int32_t* __restrict__ list, int row0, const int2* __restrict__ lg, int nthr,
+              const int2* __restrict__ dlist, unsigned* __restrict__ dcount,
+              float2* __restrict__ rep, double* __restrict__ Zout,
+              unsigned long long* __restrict__ zacc, unsigned* __restrict__ done) {
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31;
+  const int n = (int)*dcount;
+  const int wpb = kDeferThreads / 32;
+  for (int it = blockIdx.x * wpb + (threadIdx.x >> 5); it < n; it += gridDim.x * wpb) {
+    const int2 e = dlist[it];
+    const int gtid = e.x, ne = e.y;
+    const int k = list ? list[gtid] : gtid;
+    const float2 yi = ys[k];
+    float tx = 0.f, ty = 0.f;
+    double tz = 0.0;
+    for (int q = 0; q < ne; ++q) {
+      const int2 b = lg[(size_t)q * nthr + gtid];
+      float fx = 0.f, fy = 0.f, zs = 0.f;
+      for (int m = b.x + lane; m < b.x + b.y; m += 32) {
+        const float2 yj = ys[m];
+        const float ex = yi.x - yj.x, ey = yi.y - yj.y;
+        const float wj = m != k ? rcp_approx(1.f + ex * ex + ey * ey) : 0.f;
+        zs += wj;
+        const float ww = wj * wj;
+        fx = fmaf(ww, ex, fx);
+        fy = fmaf(ww, ey, fy);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        fx += __shfl_xor_sync(0xffffffffu, fx, o);
+        fy += __shfl_xor_sync(0xffffffffu, fy, o);
+        zs += __shfl_xor_sync(0xffffffffu, zs, o);
+      }
+      tx += fx;
+      ty += fy;
+      tz += (double)zs;
+    }
+    if (lane == 0) {
+      float2* r = rep + (perm[k] - row0);
+      const float2 v = *r;
+      *r = make_float2(v.x + tx, v.y + ty);
+      atomicAdd(zacc, (unsigned long long)__double2ll_rn(tz * 16777216.0));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long a = *(volatile unsigned long long*)zacc;
+    if (a) {
+      const double Z = Zout[0] + (double)a * (1.0 / 16777216.0);
+      Zout[0] = Z;
+      Zout[1] = 1.0 / Z;
+    }
+    *zacc = 0ull;
+    *dcount = 0u;
+    *done = 0u;
+  }
+}
+
+static tsne_status launch_defer_large(TreeWS& w, const int32_t* list, int row0, float2* rep,
+                                      double* Zout, cudaStream_t s) {
+  k_defer_large<<<2 * kNumSMs, kDeferThreads, 0, s>>>(
+      w.ys, w.perm, list, row0, w.lg, traverse_blocks(w.N) * kTravThreads, w.dlist,
+      w.counter + 5, rep, Zout, w.zacc, w.counter + 4);
+  TSNE_LAUNCH_CHECK();
+  return TSNE_OK;
+}
+
 static tsne_status launch_bucket_pairs(TreeWS& w, const int32_t* list, const int32_t* nlist,
                                        cudaStream_t s) {
   const int N = (int)w.N;
@@ -494,9 +586,9 @@ tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s) {
   k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
       w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0,
-      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf);
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf, w.lg, w.dlist, w.counter + 5);
   TSNE_LAUNCH_CHECK();
-  return TSNE_OK;
+  return launch_defer_large(w, nullptr, 0, w.rep, w.Z, s);
 }
 
 // The same traversal with per-point counters (measurement only; synchronises s):
@@ -513,8 +605,9 @@ tsne_status traverse_stats(TreeWS& w, float theta, double* out, cudaStream_t s) 
   k_traverse<true><<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
       w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0,
-      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf);
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf, w.lg, w.dlist, w.counter + 5);
   TSNE_LAUNCH_CHECK();
+  if ((st = launch_defer_large(w, nullptr, 0, w.rep, w.Z, s)) != TSNE_OK) return st;
   unsigned long long h[5];
   TSNE_CUDA_TRY(cudaMemcpyFromSymbolAsync(h, g_trav_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, s));
   TSNE_CUDA_TRY(cudaStreamSynchronize(s));
@@ -531,9 +624,9 @@ tsne_status launch_traverse_list(TreeWS& w, float theta, const int32_t* list, co
   k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta,
       rep_local, w.zpart, w.counter + 1, z_partial, list, nlist, row0,
-      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf);
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf, w.lg, w.dlist, w.counter + 5);
   TSNE_LAUNCH_CHECK();
-  return TSNE_OK;
+  return launch_defer_large(w, list, row0, rep_local, z_partial, s);
 }
 
 }  // namespace tsne

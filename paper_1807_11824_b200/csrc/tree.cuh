@@ -71,8 +71,12 @@ struct TreeWS {
   float2* rep = nullptr;       // N repulsive numerators f_i (original order)
   double* zpart = nullptr;     // per traversal block
   int2* ovf = nullptr;         // per traversal thread: deferred buckets beyond the registers
+  int2* lg = nullptr;          // per traversal thread: large deferred buckets (k_defer_large)
+  int2* dlist = nullptr;       // traversal threads with large deferred buckets
+  unsigned long long* zacc = nullptr;  // their z terms, fixed point (2^-24)
   double* Z = nullptr;         // [0] = Z, [1] = 1/Z
-  unsigned* counter = nullptr; // last-block-done counters (zeroed once)
+  unsigned* counter = nullptr; // last-block-done counters (zeroed once); [4] k_defer_large
+                               // done, [5] its list length
   float4* part4 = nullptr;     // per-block min/max partials (kMaxParts)
   double2* part2 = nullptr;    // per-block fp64 sum partials (kMaxParts)
   // set by build(): which double-buffer half holds the sorted result
