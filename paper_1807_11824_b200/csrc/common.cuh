@@ -86,4 +86,30 @@ __device__ __forceinline__ T ldg_stream(const T* p) {  // read-once data
   return __ldcs(p);
 }
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may start
+// while its predecessor on the stream is finishing; it lets its own dependents
+// launch at once (pdl_trigger) and waits for the predecessor's completion and
+// memory (pdl_wait) before reading anything the predecessor wrote.  (Both are
+// no-ops in a kernel launched without the attribute.)
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace tsne

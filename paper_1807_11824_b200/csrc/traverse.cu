@@ -63,6 +63,8 @@ k_bucket_pairs(const float4* __restrict__ nodes, const int32_t* __restrict__ nfi
                const float2* __restrict__ ys, const int32_t* __restrict__ leafnode, int N,
                const int32_t* __restrict__ list, const int32_t* __restrict__ nlist,
                const int32_t* __restrict__ has_bucket, BucketSum* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   if (!*has_bucket) return;                         // no bucket in this tree (k_traverse knows)
   const int nact = list ? *nlist : N;
   // grid-stride over chunks of kBucketThreads points (a small grid, so a tree
@@ -182,6 +184,8 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
            const BucketSum* __restrict__ bsum, const int32_t* __restrict__ has_bucket,
            int2* __restrict__ ovf, int2* __restrict__ lg, int2* __restrict__ dlist,
            unsigned* __restrict__ dcount) {
+  pdl_trigger();
+  pdl_wait();
   constexpr bool stats = STATS;
   // list (multi-GPU): the sorted positions of the points this rank owns
   // (original indices [row0, ...)); rep is then indexed by perm[k] - row0.
@@ -498,6 +502,8 @@ k_defer_large(const float2* __restrict__ ys, const int32_t* __restrict__ perm,
               const int2* __restrict__ dlist, unsigned* __restrict__ dcount,
               float2* __restrict__ rep, double* __restrict__ Zout,
               unsigned long long* __restrict__ zacc, unsigned* __restrict__ done) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ bool last;
   const int lane = threadIdx.x & 31;
   const int n = (int)*dcount;
@@ -560,9 +566,10 @@ k_defer_large(const float2* __restrict__ ys, const int32_t* __restrict__ perm,
 
 static tsne_status launch_defer_large(TreeWS& w, const int32_t* list, int row0, float2* rep,
                                       double* Zout, cudaStream_t s) {
-  k_defer_large<<<2 * kNumSMs, kDeferThreads, 0, s>>>(
-      w.ys, w.perm, list, row0, w.lg, traverse_blocks(w.N) * kTravThreads, w.dlist,
-      w.counter + 5, rep, Zout, w.zacc, w.counter + 4);
+  TSNE_CUDA_TRY(launch_pdl(k_defer_large, 2 * kNumSMs, kDeferThreads, 0, s, (const float2*)w.ys,
+                            (const int32_t*)w.perm, list, row0, (const int2*)w.lg,
+                            traverse_blocks(w.N) * kTravThreads, (const int2*)w.dlist,
+                            w.counter + 5, rep, Zout, w.zacc, w.counter + 4));
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }
@@ -572,9 +579,10 @@ static tsne_status launch_bucket_pairs(TreeWS& w, const int32_t* list, const int
   const int N = (int)w.N;
   // the fixed-point coordinates are dead after the tree build: reuse them
   const int nb = (N + kBucketThreads - 1) / kBucketThreads;
-  k_bucket_pairs<<<nb < 16 * kNumSMs ? nb : 16 * kNumSMs, kBucketThreads, 0, s>>>(
-      w.nodes, w.nfirst, w.ys, w.leafnode, N, list, nlist, w.has_bucket,
-      reinterpret_cast<BucketSum*>(w.fq));
+  TSNE_CUDA_TRY(launch_pdl(k_bucket_pairs, nb < 16 * kNumSMs ? nb : 16 * kNumSMs, kBucketThreads,
+                            0, s, (const float4*)w.nodes, (const int32_t*)w.nfirst,
+                            (const float2*)w.ys, (const int32_t*)w.leafnode, N, list, nlist,
+                            (const int32_t*)w.has_bucket, reinterpret_cast<BucketSum*>(w.fq)));
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }
@@ -583,10 +591,10 @@ tsne_status launch_traverse(TreeWS& w, float theta, cudaStream_t s) {
   const int N = (int)w.N;
   tsne_status st = launch_bucket_pairs(w, nullptr, nullptr, s);
   if (st != TSNE_OK) return st;
-  k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
+  TSNE_CUDA_TRY(launch_pdl(k_traverse<false>, traverse_blocks(N), kTravThreads, 0, s,
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
       w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0,
-      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf, w.lg, w.dlist, w.counter + 5);
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf, w.lg, w.dlist, w.counter + 5));
   TSNE_LAUNCH_CHECK();
   return launch_defer_large(w, nullptr, 0, w.rep, w.Z, s);
 }
@@ -602,10 +610,10 @@ tsne_status traverse_stats(TreeWS& w, float theta, double* out, cudaStream_t s) 
                                         cudaMemcpyHostToDevice, s));
   tsne_status st = launch_bucket_pairs(w, nullptr, nullptr, s);
   if (st != TSNE_OK) return st;
-  k_traverse<true><<<traverse_blocks(N), kTravThreads, 0, s>>>(
+  TSNE_CUDA_TRY(launch_pdl(k_traverse<true>, traverse_blocks(N), kTravThreads, 0, s,
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta, w.rep,
       w.zpart, w.counter + 1, w.Z, nullptr, nullptr, 0,
-      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf, w.lg, w.dlist, w.counter + 5);
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf, w.lg, w.dlist, w.counter + 5));
   TSNE_LAUNCH_CHECK();
   if ((st = launch_defer_large(w, nullptr, 0, w.rep, w.Z, s)) != TSNE_OK) return st;
   unsigned long long h[5];
@@ -621,10 +629,10 @@ tsne_status launch_traverse_list(TreeWS& w, float theta, const int32_t* list, co
   const int N = (int)w.N;
   tsne_status st = launch_bucket_pairs(w, list, nlist, s);
   if (st != TSNE_OK) return st;
-  k_traverse<false><<<traverse_blocks(N), kTravThreads, 0, s>>>(
+  TSNE_CUDA_TRY(launch_pdl(k_traverse<false>, traverse_blocks(N), kTravThreads, 0, s,
       w.nodes, w.nfirst, w.com64, w.ys, w.leafnode, w.perm, w.base + N, N, w.box, theta,
       rep_local, w.zpart, w.counter + 1, z_partial, list, nlist, row0,
-      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf, w.lg, w.dlist, w.counter + 5);
+      reinterpret_cast<const BucketSum*>(w.fq), w.has_bucket, w.ovf, w.lg, w.dlist, w.counter + 5));
   TSNE_LAUNCH_CHECK();
   return launch_defer_large(w, list, row0, rep_local, z_partial, s);
 }

@@ -330,6 +330,8 @@ k_gather(const float2* __restrict__ Y, const int32_t* __restrict__ perm,
          const uint64_t* __restrict__ keys, int N, const BoxInfo* __restrict__ box,
          int apply_shift, float2* __restrict__ ys, longlong2* __restrict__ fq,
          longlong2* __restrict__ bsum, uint8_t* __restrict__ dl) {
+  pdl_trigger();
+  pdl_wait();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   long long qx = 0, qy = 0;
   if (k < N) {
@@ -362,6 +364,8 @@ k_gather(const float2* __restrict__ Y, const int32_t* __restrict__ perm,
 // exclusive scan of the nb block sums, in place (one block): per-thread
 // serial sums, warp shuffle scans, one warp over the 32 warp totals
 __global__ void __launch_bounds__(1024) k_bscan(longlong2* __restrict__ bsum, int nb) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ long long wx[32], wy[32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int per = (nb + 1023) / 1024;
@@ -477,6 +481,8 @@ k_radix_build(const uint8_t* __restrict__ dl, int N, const uint32_t* __restrict_
               int32_t* __restrict__ cnt, int32_t* __restrict__ tsum,
               const longlong2* __restrict__ fq, const longlong2* __restrict__ boff,
               longlong2* __restrict__ S) {
+  pdl_trigger();
+  pdl_wait();
   // chain counts are summed per kScanTile tile: in shared memory for the 8
   // tiles ending at the CTA's own, in global memory beyond
   __shared__ int st[8];
@@ -502,6 +508,8 @@ k_radix_build(const uint8_t* __restrict__ dl, int N, const uint32_t* __restrict_
 __global__ void __launch_bounds__(kSortThreads)
 k_scan_cnt(const int32_t* __restrict__ cnt, int n, int32_t* __restrict__ base,
            const int32_t* __restrict__ tsum) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int kPer = kScanTile / kSortThreads;      // 16, as 4 int4
   const int t = blockIdx.x;
   int pp = 0;
@@ -542,6 +550,8 @@ k_quad_emit(int N, const uint8_t* __restrict__ dl, const int4* __restrict__ nfo,
             const BoxInfo* __restrict__ box, float4* __restrict__ nodes,
             int32_t* __restrict__ nfirst, double2* __restrict__ com64,
             int32_t* __restrict__ leafnode, int32_t* __restrict__ has_bucket) {
+  pdl_trigger();
+  pdl_wait();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k == 0) {
     // sentinel after the last node (the traversal parks finished lanes there):
@@ -602,18 +612,23 @@ tsne_status build_tree(TreeWS& w, const float2* Y, bool apply_shift, cudaStream_
   w.keys_sorted = dk.Current();
   w.perm = dv.Current();
   const int nb = cdiv(N + 1, kScanBlock);
-  k_gather<<<nb, kScanBlock, 0, s>>>(Y, w.perm, w.keys_sorted, N, w.box, apply_shift ? 1 : 0, w.ys,
-                                     w.fq, w.bsum, w.dl);
+  TSNE_CUDA_TRY(launch_pdl(k_gather, nb, kScanBlock, 0, s, Y, (const int32_t*)w.perm,
+                            (const uint64_t*)w.keys_sorted, N, (const BoxInfo*)w.box,
+                            apply_shift ? 1 : 0, w.ys, w.fq, w.bsum, w.dl));
   TSNE_LAUNCH_CHECK();
-  k_bscan<<<1, 1024, 0, s>>>(w.bsum, nb);
+  TSNE_CUDA_TRY(launch_pdl(k_bscan, 1, 1024, 0, s, w.bsum, nb));
   TSNE_LAUNCH_CHECK();
-  k_radix_build<<<nb, kScanBlock, 0, s>>>(w.dl, N, w.ctl, w.slot, w.nfo, w.cnt, w.tsum, w.fq, w.bsum,
-                                          w.S);
+  TSNE_CUDA_TRY(launch_pdl(k_radix_build, nb, kScanBlock, 0, s, (const uint8_t*)w.dl, N,
+                            (const uint32_t*)w.ctl, w.slot, w.nfo, w.cnt, w.tsum,
+                            (const longlong2*)w.fq, (const longlong2*)w.bsum, w.S));
   TSNE_LAUNCH_CHECK();
-  k_scan_cnt<<<ntiles, kSortThreads, 0, s>>>(w.cnt, N + 1, w.base, w.tsum);
+  TSNE_CUDA_TRY(launch_pdl(k_scan_cnt, ntiles, kSortThreads, 0, s, (const int32_t*)w.cnt, N + 1,
+                            w.base, (const int32_t*)w.tsum));
   TSNE_LAUNCH_CHECK();
-  k_quad_emit<<<cdiv(N, T), T, 0, s>>>(N, w.dl, w.nfo, w.cnt, w.base, w.ys, w.S, w.box, w.nodes,
-                                       w.nfirst, w.com64, w.leafnode, w.has_bucket);
+  TSNE_CUDA_TRY(launch_pdl(k_quad_emit, cdiv(N, T), T, 0, s, N, (const uint8_t*)w.dl,
+                            (const int4*)w.nfo, (const int32_t*)w.cnt, (const int32_t*)w.base,
+                            (const float2*)w.ys, (const longlong2*)w.S, (const BoxInfo*)w.box,
+                            w.nodes, w.nfirst, w.com64, w.leafnode, w.has_bucket));
   TSNE_LAUNCH_CHECK();
   return TSNE_OK;
 }
