@@ -241,11 +241,12 @@ def test_sort_bucket_overflow(T, orc, N):
     assert rel(g, go) <= 1e-4
 
 
-def test_collapsed_cluster_buckets(T, orc):
+@pytest.mark.parametrize("N", [20000, 40000])
+def test_collapsed_cluster_buckets(T, orc, N):
     # a collapsed cluster over 36 adjacent finest cells (synth 'collapsed'):
     # each point takes exact pairs with the neighbouring buckets it cannot
-    # accept -- more than the traversal's per-lane deferral list holds
-    N = 20000
+    # accept -- more than the traversal's per-lane deferral list holds; at
+    # N = 40000 the buckets (~120 points) take the k_defer_large path
     Y = synth.fixed_y("collapsed", N, seed=21)
     rp, col, v32, _ = synth.random_csr(N, 8, seed=12)
     for theta in (0.5, 0.8):

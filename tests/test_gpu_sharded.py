@@ -144,3 +144,34 @@ def test_nccl_world1_sharded_run_end_to_end(T):
         assert rel(Yh.numpy(), Yr.numpy().astype(np.float64)) < 1e-4
     finally:
         dist.destroy_process_group()
+
+
+def test_virtual_shards_collapsed_cluster(T, orc):
+    # The shard path's repulsive forces (the traversal over a rank's list of
+    # owned points, with large deferred buckets walked by k_defer_large into the
+    # rank's local numerators and Z partial) on a collapsed cluster: 3 virtual
+    # shards assembled into the gradient 4 (alpha A - f / Z) vs the oracle's.
+    from paper_1807_11824_b200.sharded import GpuShardOps, local_csr, shard_range
+    N, G, exag = 40000, 3, 12.0          # ~120 points per finest cell: large buckets
+    Y = synth.fixed_y("collapsed", N, seed=23)
+    rp, col, v32, _ = synth.random_csr(N, 8, seed=13)
+    dev = torch.device("cuda")
+    rp_d, col_d, val_d = (torch.as_tensor(a, device=dev) for a in (rp, col, v32))
+    Yd = torch.as_tensor(Y, device=dev)
+    zp = torch.zeros(2 * G, dtype=torch.float64, device=dev)
+    parts = []
+    for r in range(G):
+        a, b, _ = shard_range(N, G, r)
+        o = GpuShardOps(N, dev)
+        rpl, cl, vl = local_csr(rp_d, col_d, val_d, a, b)
+        A = torch.zeros(b - a, 2, device=dev)
+        rep = torch.zeros(b - a, 2, device=dev)
+        o.attract(rpl, cl, vl, N, a, b, Yd, A)
+        o.forces(Yd, N, a, b, 0.5, False, rep, zp[2 * r:2 * r + 2])
+        parts.append((A, rep))
+    torch.cuda.synchronize()
+    Z = float(sum(zp[2 * r].item() for r in range(G)))
+    g = torch.cat([4.0 * (exag * A.double() - rep.double() / Z) for A, rep in parts]).cpu().numpy()
+    go, Zo = orc.gradient_bh(rp, col, v32, Y, 0.5, exag)
+    assert abs(Z - Zo) <= 1e-6 * Zo
+    assert rel(g, go) <= 1e-4
