@@ -492,9 +492,9 @@ k_traverse(const float4* __restrict__ nodes, const int32_t* __restrict__ nfirst,
 // appends them): one warp per thread, its buckets in list order, lanes over the
 // members; each bucket's sums are reduced by a fixed butterfly and added in
 // order, then added to the point's repulsive numerator.  The z terms enter Z
-// through an exact fixed-point sum (2^-24 units: integers, so the order of the
-// warps does not matter), folded into Z and 1/Z by the last CTA, which also
-// resets the list.
+// through an exact fixed-point sum (integer part and 2^-32 units: integers, so
+// the order of the warps does not matter), folded into Z and 1/Z by the last
+// CTA, which also resets the list.
 constexpr int kDeferThreads = 128;
 __global__ void __launch_bounds__(kDeferThreads)
 k_defer_large(const float2* __restrict__ ys, const int32_t* __restrict__ perm,
@@ -541,7 +541,11 @@ k_defer_large(const float2* __restrict__ ys, const int32_t* __restrict__ perm,
       float2* r = rep + (perm[k] - row0);
       const float2 v = *r;
       *r = make_float2(v.x + tx, v.y + ty);
-      atomicAdd(zacc, (unsigned long long)__double2ll_rn(tz * 16777216.0));
+      // exact in two words: the integer part (z <= 16 N per point, so the sum
+      // over points stays below 2^63 for N < 2^25) and 2^-32 units of the rest
+      const double zi = floor(tz);
+      atomicAdd(zacc, (unsigned long long)zi);
+      atomicAdd(zacc + 1, (unsigned long long)__double2ll_rn((tz - zi) * 4294967296.0));
     }
   }
   __syncthreads();
@@ -552,13 +556,15 @@ k_defer_large(const float2* __restrict__ ys, const int32_t* __restrict__ perm,
   __syncthreads();
   if (last && threadIdx.x == 0) {
     __threadfence();
-    const unsigned long long a = *(volatile unsigned long long*)zacc;
-    if (a) {
-      const double Z = Zout[0] + (double)a * (1.0 / 16777216.0);
+    const unsigned long long ai = *(volatile unsigned long long*)zacc;
+    const unsigned long long af = *(volatile unsigned long long*)(zacc + 1);
+    if (ai | af) {
+      const double Z = Zout[0] + ((double)ai + (double)af * (1.0 / 4294967296.0));
       Zout[0] = Z;
       Zout[1] = 1.0 / Z;
     }
-    *zacc = 0ull;
+    zacc[0] = 0ull;
+    zacc[1] = 0ull;
     *dcount = 0u;
     *done = 0u;
   }

@@ -76,7 +76,7 @@ void carve_tree(Carver& c, TreeWS& w, int64_t N) {
   w.ovf = c.take<int2>((size_t)traverse_blocks(N) * 256 * 12);   // traversal bucket overflow
   w.lg = c.take<int2>((size_t)traverse_blocks(N) * 256 * 16);    // traversal large buckets
   w.dlist = c.take<int2>((size_t)traverse_blocks(N) * 256);
-  w.zacc = c.take<unsigned long long>(1);
+  w.zacc = c.take<unsigned long long>(2);
   w.Z = c.take<double>(2);
   w.counter = c.take<unsigned>(8);
   w.part4 = c.take<float4>(kMaxParts);
@@ -256,7 +256,7 @@ __global__ void k_keys(const float2* __restrict__ Y, int N, const BoxInfo* __res
 
 tsne_status tree_ws_init(TreeWS& w, cudaStream_t s) {
   TSNE_CUDA_TRY(cudaMemsetAsync(w.counter, 0, 8 * sizeof(unsigned), s));
-  TSNE_CUDA_TRY(cudaMemsetAsync(w.zacc, 0, sizeof(unsigned long long), s));
+  TSNE_CUDA_TRY(cudaMemsetAsync(w.zacc, 0, 2 * sizeof(unsigned long long), s));
   // the radix build's node slots are tagged with a build epoch counted from 0
   TSNE_CUDA_TRY(cudaMemsetAsync(w.ctl, 0, 2 * sizeof(uint32_t), s));
   TSNE_CUDA_TRY(cudaMemsetAsync(w.slot, 0, w.N * sizeof(unsigned long long), s));

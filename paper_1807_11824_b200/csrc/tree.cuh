@@ -73,7 +73,7 @@ struct TreeWS {
   int2* ovf = nullptr;         // per traversal thread: deferred buckets beyond the registers
   int2* lg = nullptr;          // per traversal thread: large deferred buckets (k_defer_large)
   int2* dlist = nullptr;       // traversal threads with large deferred buckets
-  unsigned long long* zacc = nullptr;  // their z terms, fixed point (2^-24)
+  unsigned long long* zacc = nullptr;  // their z terms: [0] integer part, [1] 2^-32 units
   double* Z = nullptr;         // [0] = Z, [1] = 1/Z
   unsigned* counter = nullptr; // last-block-done counters (zeroed once); [4] k_defer_large
                                // done, [5] its list length
